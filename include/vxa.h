@@ -1,0 +1,224 @@
+/*
+ * vxa.h — C ABI of the voxanim-b200 CUDA layer (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference is
+ * a C++20 library whose frame entry point is
+ *     voxanim::Image voxanim::render_frame(const Scene&, const RenderOptions&, FrameStats&)
+ *     (proj/include/voxanim/renderer.hpp:126, proj/src/renderer.cpp:218-300)
+ * and whose per-ray kernel is
+ *     std::optional<TraversalHit> voxanim::traverse(const SvoModel&, const Ray&, const OctreeBounds&)
+ *     (proj/include/voxanim/traversal.hpp:62-63, proj/src/traversal.cpp:249-252).
+ * Host C++ (libvoxanim.so, the same voxanim:: API) calls into this ABI; a
+ * maintainer of the reference who wants the GPU path links libvxa.so and
+ * replaces those two functions with the calls below.
+ *
+ * Conventions: plain C types only; every call returns a vxa_status; on
+ * failure vxa_last_error() returns a thread-local message. No exceptions
+ * cross this boundary. All FP inputs are IEEE doubles exactly as held by
+ * the reference types (RigidTransform, Camera, Ray); the library derives its
+ * FP32 working set from them.
+ */
+#ifndef VXA_H
+#define VXA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VXA_ABI_VERSION 1
+
+typedef enum vxa_status {
+    VXA_OK = 0,
+    VXA_ERR_INVALID = 1,   /* bad argument / dimension mismatch  -> voxanim::ValidationError */
+    VXA_ERR_MODEL = 2,     /* model violates the SVO invariants  -> voxanim::ValidationError */
+    VXA_ERR_CUDA = 3,      /* CUDA runtime failure               -> voxanim::DeviceError */
+    VXA_ERR_OOM = 4,       /* device allocation failed           -> voxanim::DeviceError */
+    VXA_ERR_NO_DEVICE = 5  /* no usable sm_100 device            -> voxanim::DeviceError */
+} vxa_status;
+
+typedef enum vxa_precision {
+    VXA_FP32 = 0, /* production kernel: FP32 traversal, decisions identical except slab-test ties */
+    VXA_FP64 = 1  /* parity kernel: reference operation order in FP64, bit-exact vs the CPU renderer */
+} vxa_precision;
+
+typedef struct vxa_ctx vxa_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+
+/* One context drives one CUDA device (one process per GPU; multi-GPU frames
+ * use the screen-tile partition in vxa_frame_desc plus vxa_fb_export/import).
+ * device < 0 selects VOXANIM_DEVICE or 0. */
+int vxa_create(int device, vxa_ctx** out);
+int vxa_destroy(vxa_ctx* ctx);
+const char* vxa_last_error(void);
+int vxa_abi_version(void);
+/* Device ordinal, SM count, and the kernel build tag (for logs). */
+int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t name_len);
+
+/* ---- models ------------------------------------------------------------- */
+
+/* Uploads one SvoModel. `nodes` is node_count records in the 12-byte
+ * voxanim::SvoNode layout {u32 child_base, u32 attr_base, u8 valid, u8 leaf,
+ * u16 pad} (proj/include/voxanim/svo.hpp:28-35); `attrs` is attr_count RGBA8
+ * records (VoxelAttribute). The model is checked with the reference's
+ * validate() rules (proj/src/svo.cpp:134-172) and repacked on the device.
+ * Node indices on the device equal indices into `nodes`. */
+int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const void* attrs,
+                     uint32_t attr_count, uint32_t depth, uint32_t* handle_out);
+int vxa_release_model(vxa_ctx* ctx, uint32_t handle);
+/* Device-side size of a model: bytes of the packed node words and attributes,
+ * and which packed format was chosen (1 = 4-byte words, 2 = 8-byte words). */
+int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32_t* node_format);
+
+/* ---- frame -------------------------------------------------------------- */
+
+/* voxanim::Camera (proj/include/voxanim/scene.hpp:35-42). */
+typedef struct vxa_camera {
+    double position[3];
+    double orientation[9]; /* row-major; columns right, up, back */
+    double vertical_fov_deg;
+    int32_t width;
+    int32_t height;
+} vxa_camera;
+
+/* One voxanim::SceneObject (scene.hpp:17-23): model + id + RigidTransform
+ * (math.hpp:158-169) + dirty flag. */
+typedef struct vxa_instance {
+    uint32_t model;
+    int32_t id;
+    double rotation[9];
+    double translation[3];
+    double scale[3];
+    uint8_t dirty;
+    uint8_t pad[7];
+} vxa_instance;
+
+/* Per-pixel hit record in the host voxanim::HitRecord layout
+ * (renderer.hpp:32-41): 48 bytes. Used for the hit buffer (HBO). */
+typedef struct vxa_hit_record {
+    uint8_t color[4];
+    uint8_t pad0[4];
+    double normal[3];
+    double t;
+    int32_t object_id;
+    uint8_t kind; /* 0 Miss, 1 SingleSphere, 2 MultiSphere */
+    uint8_t pad1[3];
+} vxa_hit_record;
+
+typedef struct vxa_frame_desc {
+    vxa_camera camera;
+    uint8_t background[3];
+    uint8_t culling;      /* RenderOptions::culling */
+    uint8_t sorting;      /* RenderOptions::sorting */
+    uint8_t precision;    /* vxa_precision */
+    uint8_t camera_dirty; /* Camera::dirty, read by the HBO reuse rule */
+    uint8_t pad0;
+    int32_t tile_rank;    /* screen-tile partition: this device renders the 64x64 */
+    int32_t tile_world;   /* super-tiles s with s % tile_world == tile_rank (1 = all) */
+    /* Host hit buffer (width*height records) or NULL (RenderOptions::hbo).
+     * Read before and written after the frame, in place. */
+    vxa_hit_record* hbo;
+} vxa_frame_desc;
+
+/* voxanim::FrameStats (renderer.hpp:62-68) plus device evidence. */
+typedef struct vxa_stats {
+    uint64_t rays;
+    uint64_t sphere_tests;
+    uint64_t svo_traversals;
+    uint64_t pixels_reused;
+    uint64_t node_fetches;   /* internal-node words loaded (8 B algorithmic each) */
+    uint64_t leaf_hits;      /* attribute fetches (4 B each) */
+    uint64_t kernel_launches;/* kernels this call launched */
+    double gpu_ms;           /* CUDA-event time of the frame kernels on the context stream */
+} vxa_stats;
+
+/* Per-pixel parity outputs (host array of width*height, row-major). */
+typedef struct vxa_pixel_aov {
+    double t;             /* hit parameter (world == local, rotations preserve length) */
+    int32_t object_id;    /* -1: miss */
+    uint32_t node_index;  /* parent node of the hit leaf (index into SvoModel::nodes) */
+    uint32_t attr_index;  /* index into SvoModel::attributes */
+    uint32_t voxel[3];    /* leaf_path_to_voxel of the hit path */
+    uint8_t level;        /* path_len */
+    uint8_t kind;         /* HitKind */
+    uint16_t traversals;  /* SVO traversals started for this pixel */
+    uint32_t node_fetches;/* internal-node words loaded for this pixel */
+} vxa_pixel_aov;
+
+/* Renders one frame synchronously. instances are in scene order. rgb_out:
+ * host RGB8 (width*height*3) or NULL to keep the frame on the device only.
+ * aov_out: host array or NULL. stats may be NULL. */
+int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* instances,
+               uint32_t instance_count, uint8_t* rgb_out, vxa_pixel_aov* aov_out, vxa_stats* stats);
+
+/* Asynchronous form for benchmarking: enqueues the frame on the context
+ * stream (framebuffer stays in HBM), no host outputs, no HBO. */
+int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* instances,
+               uint32_t instance_count);
+int vxa_synchronize(vxa_ctx* ctx);
+/* Device counters accumulated since the last vxa_stats_reset. */
+int vxa_stats_read(vxa_ctx* ctx, vxa_stats* stats);
+int vxa_stats_reset(vxa_ctx* ctx);
+/* Copies the resident RGBA8 framebuffer to host RGB8 (width*height*3). */
+int vxa_read_framebuffer(vxa_ctx* ctx, uint8_t* rgb_out, int32_t width, int32_t height);
+
+/* Timing helpers on the context stream (CUDA events). */
+int vxa_timer_begin(vxa_ctx* ctx);
+int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms);
+/* Writes a scratch buffer larger than L2 on the context stream. */
+int vxa_flush_l2(vxa_ctx* ctx);
+/* Raw cudaStream_t of the context (for callers that record their own events). */
+void* vxa_stream(vxa_ctx* ctx);
+
+/* ---- multi-GPU framebuffer gather over NVLink --------------------------- */
+
+/* Rank 0 exports its framebuffer (allocated for width x height) as a CUDA IPC
+ * handle (64 bytes); every other rank imports it, after which its frames
+ * store their super-tiles straight into rank 0's framebuffer through the
+ * peer mapping (NVLink / NVSwitch). */
+int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_out);
+int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle);
+
+/* ---- single-ray traversal (voxanim::traverse / traverse_debug) ---------- */
+
+typedef struct vxa_local_ray {
+    double origin[3];
+    double direction[3];
+    double half_extent[3]; /* OctreeBounds::half_extent */
+} vxa_local_ray;
+
+typedef struct vxa_traverse_hit {
+    double t_hit, t_enter, t_exit;
+    double normal_local[3];
+    uint8_t attribute[4];
+    uint32_t attr_index;
+    uint32_t node_index;  /* parent node of the hit leaf */
+    uint8_t leaf_path[16];
+    uint8_t path_len;
+    uint8_t hit;          /* 0: std::nullopt */
+    uint16_t pad;
+    uint32_t node_fetches;
+    uint32_t log_count;   /* visits recorded (<= capacity) */
+    uint32_t log_total;   /* visits that occurred */
+} vxa_traverse_hit;
+
+typedef struct vxa_visit {
+    double t_enter;
+    uint8_t level;
+    uint8_t leaf;
+    uint8_t pad[6];
+} vxa_visit;
+
+/* Batched traversal of local rays against one model. log may be NULL;
+ * otherwise ray i writes up to log_capacity visits at log[i*log_capacity]. */
+int vxa_traverse(vxa_ctx* ctx, uint32_t model, const vxa_local_ray* rays, uint32_t ray_count,
+                 uint32_t precision, vxa_traverse_hit* hits, vxa_visit* log, uint32_t log_capacity);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VXA_H */

@@ -1,0 +1,606 @@
+// TEST INFRASTRUCTURE — the parity oracle. Not part of the product.
+//
+// Glue that exposes the REFERENCE implementation (proj/src/*.cpp compiled in
+// place from /root/reference by oracle/Makefile into oracle/_ref/) through a
+// flat C interface for tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference leg. Nothing in the product links this.
+//
+// What it provides, all computed by the reference's own functions:
+//   * models: deserialize (svo.cpp:231-291), dense sphere / shell / random
+//     grids -> build_from_grid (svo.cpp:80-132, ingest.cpp:193-266,
+//     tests/support/oracles.hpp:265-279);
+//   * scenes: bench_scenes.cpp compiled against the reference headers;
+//     evaluate_animation (scene.cpp:370-385);
+//   * frames: render_frame (renderer.cpp:218-300), timed by FrameStats::render_ms;
+//   * per-pixel AOV dump: shade_pixel's candidate order and skip rule
+//     (renderer.cpp:143-214, 63-100) replayed with traverse_debug so the hit
+//     voxel (leaf_path_to_voxel), level (path_len), parent node and attribute
+//     index (node_child replay, svo.cpp:27-39) and internal-node fetches are
+//     known; its RGB must equal render_frame's image (checked by the tests);
+//   * single rays: traverse / traverse_debug (traversal.cpp:249-258) and the
+//     independent DDA oracle (oracles.hpp:68-149);
+//   * the FP32 tie classifier (SURVEY.md §8(a) "Tie classification").
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "support/oracles.hpp"
+#include "voxanim/renderer.hpp"
+#include "voxanim/scene.hpp"
+#include "voxanim/svo.hpp"
+#include "voxanim/traversal.hpp"
+
+#include "bench_scenes.hpp"
+
+using namespace voxanim;
+
+struct vref_model {
+    std::shared_ptr<const SvoModel> m;
+};
+struct vref_scene {
+    Scene s;
+};
+struct vref_hbo {
+    HitBuffer b;
+};
+
+// Same layouts as include/vxa.h (kept independent on purpose: the oracle does
+// not include product headers).
+struct AovRec {
+    double t;
+    int32_t object_id;
+    uint32_t node_index;
+    uint32_t attr_index;
+    uint32_t voxel[3];
+    uint8_t level;
+    uint8_t kind;
+    uint16_t traversals;
+    uint32_t node_fetches;
+};
+static_assert(sizeof(AovRec) == 40);
+
+struct LocalRayRec {
+    double origin[3], direction[3], half_extent[3];
+};
+struct TravRec {
+    double t_hit, t_enter, t_exit;
+    double normal_local[3];
+    uint8_t attribute[4];
+    uint32_t attr_index;
+    uint32_t node_index;
+    uint8_t leaf_path[16];
+    uint8_t path_len;
+    uint8_t hit;
+    uint16_t pad;
+    uint32_t node_fetches;
+    uint32_t log_count;
+    uint32_t log_total;
+};
+static_assert(sizeof(TravRec) == 96);
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F> auto guard(F&& f, decltype(f()) on_error) -> decltype(f()) {
+    try {
+        return f();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+    } catch (...) {
+        g_err = "unknown exception";
+    }
+    return on_error;
+}
+
+vref_model* wrap(SvoModel&& m) { return new vref_model{std::make_shared<const SvoModel>(std::move(m))}; }
+
+int hw_threads(int t) {
+    if (t > 0) return t;
+    const int h = static_cast<int>(std::thread::hardware_concurrency());
+    return h > 0 ? h : 1;
+}
+
+template <class F> void parallel_rows(int rows, int threads, F&& body) {
+    threads = std::max(1, std::min(threads, rows));
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w) {
+        const int a = static_cast<int>(static_cast<long long>(rows) * w / threads);
+        const int b = static_cast<int>(static_cast<long long>(rows) * (w + 1) / threads);
+        pool.emplace_back([&, a, b] { body(a, b); });
+    }
+    for (auto& t : pool) t.join();
+}
+
+// Replays node_child down a leaf path: parent node index and attribute index.
+void replay_path(const SvoModel& m, const TraversalHit& h, uint32_t& parent, uint32_t& attr) {
+    uint32_t node = 0;
+    for (int l = 0; l + 1 < h.path_len; ++l) node = node_child(m, node, h.leaf_path[static_cast<std::size_t>(l)]).index;
+    parent = node;
+    attr = node_child(m, node, h.leaf_path[static_cast<std::size_t>(h.path_len - 1)]).index;
+}
+
+// Internal nodes fetched by one traversal = root (if the box is hit) + pushes.
+uint32_t fetches_of(const SvoModel& m, const Ray& local, const OctreeBounds& b, const std::vector<TraversalVisit>& log) {
+    if (!ray_box_params(local, b)) return 0;
+    uint32_t n = 1;
+    for (const TraversalVisit& v : log)
+        if (!v.leaf && v.level < m.depth && v.level < kMaxTreeDepth) ++n;
+    return n;
+}
+
+struct PixelOracle {
+    AovRec aov{};
+    std::array<std::uint8_t, 3> rgb{};
+};
+
+// shade_pixel without a hit buffer (renderer.cpp:143-214) + trace_ray (:63-100).
+PixelOracle oracle_pixel(const Scene& scene, const std::vector<BoundingSphere>& spheres, const RenderOptions& opts,
+                         const Ray& ray) {
+    const bool sphere_pass = opts.culling || opts.sorting;
+    std::vector<SphereHit> hits;
+    if (sphere_pass) {
+        for (std::size_t i = 0; i < scene.objects.size(); ++i)
+            if (auto h = ray_sphere_test(ray, spheres[i])) {
+                h->object_id = scene.objects[i].id;
+                hits.push_back(*h);
+            }
+    }
+    std::vector<SphereHit> cand;
+    if (opts.culling) {
+        cand = hits;
+    } else {
+        for (std::size_t i = 0; i < scene.objects.size(); ++i) {
+            SphereHit e;
+            e.object_id = scene.objects[i].id;
+            if (opts.sorting) {
+                if (auto h = ray_sphere_test(ray, spheres[i])) {
+                    e.d = h->d;
+                    e.t_center = h->t_center;
+                    e.t_boundary = h->t_boundary;
+                } else {
+                    e.t_center = (spheres[i].center - ray.origin).dot(ray.direction);
+                }
+            }
+            cand.push_back(e);
+        }
+    }
+    if (opts.sorting) {
+        std::sort(cand.begin(), cand.end(), [](const SphereHit& a, const SphereHit& b) {
+            return a.t_center != b.t_center ? a.t_center < b.t_center : a.object_id < b.object_id;
+        });
+    } else {
+        std::sort(cand.begin(), cand.end(), [](const SphereHit& a, const SphereHit& b) { return a.object_id < b.object_id; });
+        for (auto& c : cand) c.t_boundary = 0.0;
+    }
+
+    PixelOracle out;
+    HitRecord best;
+    bool have = false;
+    TraversalHit best_hit{};
+    const SceneObject* best_obj = nullptr;
+    uint32_t trav = 0, fetch = 0;
+    for (const SphereHit& c : cand) {
+        if (have && best.t < c.t_boundary) continue;
+        const SceneObject* obj = scene.find_object(c.object_id);
+        if (!obj || !obj->model) continue;
+        const Ray local = transform_ray_world_to_local(ray, obj->transform);
+        ++trav;
+        const OctreeBounds b = bounds_from_scale(obj->transform.scale);
+        std::vector<TraversalVisit> log;
+        const auto hit = traverse_debug(*obj->model, local, b, log);
+        fetch += fetches_of(*obj->model, local, b, log);
+        if (!hit) continue;
+        if (!have || hit->t_hit < best.t || (hit->t_hit == best.t && obj->id < best.object_id)) {
+            have = true;
+            best.color = hit->attribute;
+            best.normal = obj->transform.rotation * hit->normal_local;
+            best.t = hit->t_hit;
+            best.object_id = obj->id;
+            best_hit = *hit;
+            best_obj = obj;
+        }
+    }
+    if (have) best.kind = cand.size() > 1 ? HitKind::MultiSphere : HitKind::SingleSphere;
+    out.rgb = shade(best, ray, scene.background);
+    AovRec& a = out.aov;
+    a.object_id = have ? best.object_id : -1;
+    a.t = have ? best.t : 0.0;
+    a.kind = static_cast<uint8_t>(best.kind);
+    a.traversals = static_cast<uint16_t>(trav);
+    a.node_fetches = fetch;
+    if (have) {
+        replay_path(*best_obj->model, best_hit, a.node_index, a.attr_index);
+        const auto v = leaf_path_to_voxel(std::span<const std::uint8_t>(best_hit.leaf_path.data(), best_hit.path_len));
+        a.voxel[0] = v[0];
+        a.voxel[1] = v[1];
+        a.voxel[2] = v[2];
+        a.level = best_hit.path_len;
+    }
+    return out;
+}
+
+// ---- tie classification ----------------------------------------------------
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+double tau(double t) { return 8.0 * std::ldexp(1.0, -23) * std::max(1.0, std::abs(t)); }
+
+struct Interval {
+    double in = kInf, out = -kInf;
+};
+
+// FP64 slab test of the voxel box (level `level` of the instance's octree)
+// against the local ray.
+Interval voxel_interval(const SceneObject& obj, const Ray& world, const uint32_t v[3], uint32_t level) {
+    const Ray r = transform_ray_world_to_local(world, obj.transform);
+    const OctreeBounds b = bounds_from_scale(obj.transform.scale);
+    Interval iv{-kInf, kInf};
+    for (int a = 0; a < 3; ++a) {
+        const double h = b.half_extent[a];
+        const double cell = 2.0 * h / std::ldexp(1.0, static_cast<int>(level));
+        const double lo = -h + v[a] * cell, hi = lo + cell;
+        const double o = r.origin[a], d = r.direction[a];
+        if (d == 0.0) {
+            if (o < lo || o >= hi) return {kInf, -kInf};
+            continue;
+        }
+        double t0 = (lo - o) / d, t1 = (hi - o) / d;
+        if (t0 > t1) std::swap(t0, t1);
+        iv.in = std::max(iv.in, t0);
+        iv.out = std::min(iv.out, t1);
+    }
+    return iv;
+}
+
+bool sphere_grazed(const SceneObject& obj, const Ray& ray, double t_ref) {
+    const BoundingSphere s = bounding_sphere(obj);
+    const Vec3 l = s.center - ray.origin;
+    const double tc = l.dot(ray.direction);
+    const double d2 = l.norm2() - tc * tc;
+    const double r2 = s.radius * s.radius;
+    return std::abs(d2 - r2) <= tau(t_ref) * std::max(1.0, r2) * 16.0;
+}
+
+bool box_grazed(const SceneObject& obj, const Ray& world, double t_ref) {
+    const Ray r = transform_ray_world_to_local(world, obj.transform);
+    const OctreeBounds b = bounds_from_scale(obj.transform.scale);
+    double tin = -kInf, tout = kInf;
+    for (int a = 0; a < 3; ++a) {
+        const double h = b.half_extent[a], o = r.origin[a], d = r.direction[a];
+        if (d == 0.0) {
+            if (std::abs(o - h) <= tau(t_ref) || std::abs(o + h) <= tau(t_ref)) return true;
+            continue;
+        }
+        double t0 = (-h - o) / d, t1 = (h - o) / d;
+        if (t0 > t1) std::swap(t0, t1);
+        tin = std::max(tin, t0);
+        tout = std::min(tout, t1);
+    }
+    return std::abs(tout - tin) <= tau(t_ref) || std::abs(tout) <= tau(t_ref);
+}
+
+// FP64 entry parameter of an instance for this ray (reference traverse).
+bool instance_t(const SceneObject& obj, const Ray& world, double& t) {
+    if (!obj.model) return false;
+    const Ray local = transform_ray_world_to_local(world, obj.transform);
+    const auto h = traverse(*obj.model, local, bounds_from_scale(obj.transform.scale));
+    if (!h) return false;
+    t = h->t_hit;
+    return true;
+}
+
+// 0: equal; 1: documented slab-test tie; 2: unexplained (a bug); 3: same hit but t out of tolerance.
+int classify_pixel(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
+    const bool ho = o.object_id >= 0, hg = g.object_id >= 0;
+    if (!ho && !hg) return 0;
+    if (ho && hg && o.object_id == g.object_id && o.voxel[0] == g.voxel[0] && o.voxel[1] == g.voxel[1] &&
+        o.voxel[2] == g.voxel[2] && o.level == g.level && o.node_index == g.node_index && o.attr_index == g.attr_index) {
+        const double tol = t_rel * std::max(1.0, std::abs(o.t));
+        return std::abs(o.t - g.t) <= tol ? 0 : 3;
+    }
+    const double tref = ho ? o.t : g.t;
+    const double tt = tau(tref);
+    const SceneObject* oo = ho ? scene.find_object(o.object_id) : nullptr;
+    const SceneObject* og = hg ? scene.find_object(g.object_id) : nullptr;
+    // sphere / box grazes of either instance
+    for (const SceneObject* obj : {oo, og})
+        if (obj && (sphere_grazed(*obj, ray, tref) || box_grazed(*obj, ray, tref))) return 1;
+    Interval vo, vg;
+    if (oo) {
+        vo = voxel_interval(*oo, ray, o.voxel, o.level);
+        if (vo.out - vo.in <= tt) return 1; // V_o grazed
+    }
+    if (og) {
+        vg = voxel_interval(*og, ray, g.voxel, g.level);
+        if (std::abs(vg.in - vg.out) <= tt) return 1; // V_g near-miss or graze
+        if (vg.out < 0.0 && vg.out > -tt) return 1;  // behind-origin boundary
+    }
+    if (oo && og) {
+        const double ti = std::max(vo.in, 0.0), tg = std::max(vg.in, 0.0);
+        if (std::abs(ti - tg) <= tt) return 1; // both voxels entered at the same parameter
+        if (o.object_id != g.object_id) {
+            double t64 = 0.0;
+            if (instance_t(*og, ray, t64) && std::abs(t64 - o.t) <= tt) return 1; // nearest-instance tie
+        }
+    }
+    if (!hg && oo) {
+        // GPU missed: the oracle's voxel must be (nearly) grazed or a neighbour gap
+        if (vo.out - vo.in <= 4 * tt) return 1;
+    }
+    return 2;
+}
+
+} // namespace
+
+#define VREF_API __attribute__((visibility("default")))
+
+extern "C" {
+
+VREF_API const char* vref_last_error(void) { return g_err.c_str(); }
+
+VREF_API vref_model* vref_model_deserialize(const uint8_t* bytes, size_t n) {
+    return guard([&] { return wrap(deserialize(std::span<const std::uint8_t>(bytes, n))); }, (vref_model*)nullptr);
+}
+
+VREF_API vref_model* vref_model_dense_sphere(uint32_t depth) {
+    return guard([&] { return wrap(build_from_grid(gen_primitive(PrimitiveKind::Sphere, depth), depth)); },
+                 (vref_model*)nullptr);
+}
+
+// Shell of the reference's sphere: solid voxels with a 6-neighbour outside the
+// solid or outside the grid.
+VREF_API vref_model* vref_model_shell_grid(uint32_t depth) {
+    return guard(
+        [&] {
+            const VoxelGrid solid = gen_primitive(PrimitiveKind::Sphere, depth);
+            const int n = static_cast<int>(solid.resolution());
+            VoxelGrid shell(solid.resolution());
+            const auto in = [&](int x, int y, int z) {
+                return x >= 0 && y >= 0 && z >= 0 && x < n && y < n && z < n &&
+                       solid.is_set(static_cast<uint32_t>(x), static_cast<uint32_t>(y), static_cast<uint32_t>(z));
+            };
+            for (int x = 0; x < n; ++x)
+                for (int y = 0; y < n; ++y)
+                    for (int z = 0; z < n; ++z)
+                        if (in(x, y, z) && !(in(x - 1, y, z) && in(x + 1, y, z) && in(x, y - 1, z) && in(x, y + 1, z) &&
+                                             in(x, y, z - 1) && in(x, y, z + 1)))
+                            shell.set(static_cast<uint32_t>(x), static_cast<uint32_t>(y), static_cast<uint32_t>(z));
+            return wrap(build_from_grid(shell, depth));
+        },
+        (vref_model*)nullptr);
+}
+
+VREF_API vref_model* vref_model_random(uint64_t seed, uint32_t depth, double fill) {
+    return guard(
+        [&] {
+            std::mt19937_64 rng(seed);
+            return wrap(build_from_grid(oracles::random_grid(rng, depth, fill), depth));
+        },
+        (vref_model*)nullptr);
+}
+
+VREF_API int64_t vref_model_serialize(const vref_model* m, uint8_t* out, size_t cap) {
+    return guard(
+        [&]() -> int64_t {
+            const auto b = serialize(*m->m);
+            if (out) {
+                if (cap < b.size()) throw ValidationError("buffer too small");
+                std::memcpy(out, b.data(), b.size());
+            }
+            return static_cast<int64_t>(b.size());
+        },
+        int64_t{-1});
+}
+
+VREF_API void vref_model_free(vref_model* m) { delete m; }
+
+VREF_API vref_scene* vref_scene_config(int config, vref_model* const* models, uint32_t n, uint64_t seed, int w, int h) {
+    return guard(
+        [&] {
+            std::vector<std::shared_ptr<const SvoModel>> ms;
+            for (uint32_t i = 0; i < n; ++i) ms.push_back(models[i]->m);
+            return new vref_scene{bench::make_config_scene(config, ms, seed, w, h)};
+        },
+        (vref_scene*)nullptr);
+}
+
+VREF_API int vref_scene_evaluate(vref_scene* s, double t) {
+    return guard(
+        [&] {
+            evaluate_animation(s->s, t);
+            return 0;
+        },
+        -1);
+}
+
+VREF_API int vref_scene_mark_clean(vref_scene* s) {
+    mark_clean(s->s);
+    return 0;
+}
+
+VREF_API int vref_scene_set_camera_dirty(vref_scene* s, int dirty) {
+    s->s.camera.dirty = dirty != 0;
+    return 0;
+}
+
+VREF_API int vref_scene_get_object(const vref_scene* s, int index, int32_t* id, double* tf, int* dirty) {
+    if (index < 0 || index >= static_cast<int>(s->s.objects.size())) return -1;
+    const SceneObject& o = s->s.objects[static_cast<std::size_t>(index)];
+    if (id) *id = o.id;
+    if (tf) std::memcpy(tf, static_cast<const void*>(&o.transform), sizeof(o.transform));
+    if (dirty) *dirty = o.dirty ? 1 : 0;
+    return 0;
+}
+
+VREF_API int vref_scene_set_object(vref_scene* s, int index, const double* tf, int dirty) {
+    if (index < 0 || index >= static_cast<int>(s->s.objects.size())) return -1;
+    SceneObject& o = s->s.objects[static_cast<std::size_t>(index)];
+    if (tf) std::memcpy(static_cast<void*>(&o.transform), tf, sizeof(o.transform));
+    o.dirty = dirty != 0;
+    return 0;
+}
+
+VREF_API void vref_scene_free(vref_scene* s) { delete s; }
+
+VREF_API vref_hbo* vref_hbo_create(int w, int h) {
+    return guard([&] { return new vref_hbo{HitBuffer(w, h)}; }, (vref_hbo*)nullptr);
+}
+
+VREF_API void vref_hbo_free(vref_hbo* h) { delete h; }
+
+// The reference frame: render_frame with its own timing (FrameStats::render_ms).
+VREF_API int vref_render(vref_scene* s, int culling, int sorting, int threads, vref_hbo* hbo, uint8_t* rgb, uint64_t* fs4,
+                double* render_ms) {
+    return guard(
+        [&] {
+            RenderOptions opts;
+            opts.culling = culling != 0;
+            opts.sorting = sorting != 0;
+            opts.threads = threads;
+            opts.hbo = hbo ? &hbo->b : nullptr;
+            FrameStats st;
+            const Image img = render_frame(s->s, opts, st);
+            if (rgb) std::memcpy(rgb, img.rgb.data(), img.rgb.size());
+            if (fs4) {
+                fs4[0] = st.rays;
+                fs4[1] = st.sphere_tests;
+                fs4[2] = st.svo_traversals;
+                fs4[3] = st.pixels_reused;
+            }
+            if (render_ms) *render_ms = st.render_ms;
+            return 0;
+        },
+        -1);
+}
+
+// Per-pixel oracle over the rows [row_begin, row_end) (whole frame if both 0).
+VREF_API int vref_dump(const vref_scene* s, int culling, int sorting, int threads, int row_begin, int row_end, AovRec* aov,
+              uint8_t* rgb) {
+    return guard(
+        [&] {
+            const Scene& scene = s->s;
+            const int W = scene.camera.width;
+            if (row_begin == 0 && row_end == 0) row_end = scene.camera.height;
+            RenderOptions opts;
+            opts.culling = culling != 0;
+            opts.sorting = sorting != 0;
+            std::vector<BoundingSphere> spheres;
+            for (const SceneObject& o : scene.objects) spheres.push_back(bounding_sphere(o));
+            parallel_rows(row_end - row_begin, hw_threads(threads), [&](int a, int b) {
+                for (int r = a; r < b; ++r) {
+                    const int py = row_begin + r;
+                    for (int px = 0; px < W; ++px) {
+                        const PixelOracle po = oracle_pixel(scene, spheres, opts, generate_primary_ray(scene.camera, px, py));
+                        const std::size_t i = static_cast<std::size_t>(r) * W + px;
+                        if (aov) aov[i] = po.aov;
+                        if (rgb) std::memcpy(rgb + 3 * i, po.rgb.data(), 3);
+                    }
+                }
+            });
+            return 0;
+        },
+        -1);
+}
+
+// Tie classification of GPU AOVs against oracle AOVs (rows as in vref_dump).
+VREF_API int vref_classify(const vref_scene* s, int row_begin, int row_end, const AovRec* oracle, const AovRec* gpu,
+                  double t_rel, uint8_t* cls) {
+    return guard(
+        [&] {
+            const Scene& scene = s->s;
+            const int W = scene.camera.width;
+            for (int py = row_begin; py < row_end; ++py)
+                for (int px = 0; px < W; ++px) {
+                    const std::size_t i = static_cast<std::size_t>(py - row_begin) * W + px;
+                    cls[i] = static_cast<uint8_t>(
+                        classify_pixel(scene, generate_primary_ray(scene.camera, px, py), oracle[i], gpu[i], t_rel));
+                }
+            return 0;
+        },
+        -1);
+}
+
+// Reference traverse (+ optional visit log) for a batch of local rays.
+VREF_API int vref_traverse(const vref_model* m, const LocalRayRec* rays, uint32_t n, TravRec* out, int with_fetches) {
+    return guard(
+        [&] {
+            for (uint32_t i = 0; i < n; ++i) {
+                const Ray r{{rays[i].origin[0], rays[i].origin[1], rays[i].origin[2]},
+                            {rays[i].direction[0], rays[i].direction[1], rays[i].direction[2]}};
+                const OctreeBounds b{{rays[i].half_extent[0], rays[i].half_extent[1], rays[i].half_extent[2]}};
+                std::vector<TraversalVisit> log;
+                const auto h = with_fetches ? traverse_debug(*m->m, r, b, log) : traverse(*m->m, r, b);
+                TravRec t{};
+                t.log_total = static_cast<uint32_t>(log.size());
+                if (with_fetches) t.node_fetches = fetches_of(*m->m, r, b, log);
+                if (h) {
+                    t.hit = 1;
+                    t.t_hit = h->t_hit;
+                    t.t_enter = h->t_enter;
+                    t.t_exit = h->t_exit;
+                    t.normal_local[0] = h->normal_local.x;
+                    t.normal_local[1] = h->normal_local.y;
+                    t.normal_local[2] = h->normal_local.z;
+                    t.attribute[0] = h->attribute.r;
+                    t.attribute[1] = h->attribute.g;
+                    t.attribute[2] = h->attribute.b;
+                    t.attribute[3] = h->attribute.a;
+                    std::copy(h->leaf_path.begin(), h->leaf_path.end(), t.leaf_path);
+                    t.path_len = h->path_len;
+                    replay_path(*m->m, *h, t.node_index, t.attr_index);
+                }
+                out[i] = t;
+            }
+            return 0;
+        },
+        -1);
+}
+
+// Independent DDA oracle on the random grid (seed, depth, fill): voxel + t per ray.
+VREF_API int vref_dda_random(uint64_t seed, uint32_t depth, double fill, const LocalRayRec* rays, uint32_t n, int32_t* hit,
+                    uint32_t* voxel, double* t) {
+    return guard(
+        [&] {
+            std::mt19937_64 rng(seed);
+            const VoxelGrid g = oracles::random_grid(rng, depth, fill);
+            for (uint32_t i = 0; i < n; ++i) {
+                const Ray r{{rays[i].origin[0], rays[i].origin[1], rays[i].origin[2]},
+                            {rays[i].direction[0], rays[i].direction[1], rays[i].direction[2]}};
+                const Vec3 h{rays[i].half_extent[0], rays[i].half_extent[1], rays[i].half_extent[2]};
+                const auto d = oracles::dda_trace(g, h, r);
+                hit[i] = d ? 1 : 0;
+                if (d) {
+                    voxel[3 * i] = d->x;
+                    voxel[3 * i + 1] = d->y;
+                    voxel[3 * i + 2] = d->z;
+                    t[i] = d->t;
+                }
+            }
+            return 0;
+        },
+        -1);
+}
+
+// The reference's primary ray for a pixel (renderer.cpp:11-23): origin, direction.
+VREF_API int vref_primary_ray(const vref_scene* s, int px, int py, double* o6) {
+    return guard(
+        [&] {
+            const Ray r = generate_primary_ray(s->s.camera, px, py);
+            o6[0] = r.origin.x, o6[1] = r.origin.y, o6[2] = r.origin.z;
+            o6[3] = r.direction.x, o6[4] = r.direction.y, o6[5] = r.direction.z;
+            return 0;
+        },
+        -1);
+}
+
+VREF_API int vref_hardware_threads(void) { return hw_threads(0); }
+
+} // extern "C"

@@ -1,0 +1,240 @@
+"""ctypes mirror of include/vxa.h and include/voxanim_capi.h.
+
+Python is plumbing here: tests and bench.py drive the native libraries
+(lib/libvxa.so — CUDA layer + C ABI; lib/libvoxanim.so — the drop-in
+voxanim:: C++ API) through these declarations. There is no Python compute
+path and no fallback: if a library is missing, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+
+VXA_OK, VXA_ERR_INVALID, VXA_ERR_MODEL, VXA_ERR_CUDA, VXA_ERR_OOM, VXA_ERR_NO_DEVICE = range(6)
+VXA_FP32, VXA_FP64 = 0, 1
+
+
+class vxa_camera(C.Structure):
+    _fields_ = [
+        ("position", C.c_double * 3),
+        ("orientation", C.c_double * 9),
+        ("vertical_fov_deg", C.c_double),
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+    ]
+
+
+class vxa_instance(C.Structure):
+    _fields_ = [
+        ("model", C.c_uint32),
+        ("id", C.c_int32),
+        ("rotation", C.c_double * 9),
+        ("translation", C.c_double * 3),
+        ("scale", C.c_double * 3),
+        ("dirty", C.c_uint8),
+        ("pad", C.c_uint8 * 7),
+    ]
+
+
+class vxa_hit_record(C.Structure):
+    _fields_ = [
+        ("color", C.c_uint8 * 4),
+        ("pad0", C.c_uint8 * 4),
+        ("normal", C.c_double * 3),
+        ("t", C.c_double),
+        ("object_id", C.c_int32),
+        ("kind", C.c_uint8),
+        ("pad1", C.c_uint8 * 3),
+    ]
+
+
+class vxa_frame_desc(C.Structure):
+    _fields_ = [
+        ("camera", vxa_camera),
+        ("background", C.c_uint8 * 3),
+        ("culling", C.c_uint8),
+        ("sorting", C.c_uint8),
+        ("precision", C.c_uint8),
+        ("camera_dirty", C.c_uint8),
+        ("pad0", C.c_uint8),
+        ("tile_rank", C.c_int32),
+        ("tile_world", C.c_int32),
+        ("hbo", C.POINTER(vxa_hit_record)),
+    ]
+
+
+class vxa_stats(C.Structure):
+    _fields_ = [
+        ("rays", C.c_uint64),
+        ("sphere_tests", C.c_uint64),
+        ("svo_traversals", C.c_uint64),
+        ("pixels_reused", C.c_uint64),
+        ("node_fetches", C.c_uint64),
+        ("leaf_hits", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
+        ("gpu_ms", C.c_double),
+    ]
+
+
+class vxa_pixel_aov(C.Structure):
+    _fields_ = [
+        ("t", C.c_double),
+        ("object_id", C.c_int32),
+        ("node_index", C.c_uint32),
+        ("attr_index", C.c_uint32),
+        ("voxel", C.c_uint32 * 3),
+        ("level", C.c_uint8),
+        ("kind", C.c_uint8),
+        ("traversals", C.c_uint16),
+        ("node_fetches", C.c_uint32),
+    ]
+
+
+class vxa_local_ray(C.Structure):
+    _fields_ = [
+        ("origin", C.c_double * 3),
+        ("direction", C.c_double * 3),
+        ("half_extent", C.c_double * 3),
+    ]
+
+
+class vxa_traverse_hit(C.Structure):
+    _fields_ = [
+        ("t_hit", C.c_double),
+        ("t_enter", C.c_double),
+        ("t_exit", C.c_double),
+        ("normal_local", C.c_double * 3),
+        ("attribute", C.c_uint8 * 4),
+        ("attr_index", C.c_uint32),
+        ("node_index", C.c_uint32),
+        ("leaf_path", C.c_uint8 * 16),
+        ("path_len", C.c_uint8),
+        ("hit", C.c_uint8),
+        ("pad", C.c_uint16),
+        ("node_fetches", C.c_uint32),
+        ("log_count", C.c_uint32),
+        ("log_total", C.c_uint32),
+    ]
+
+
+class vxa_visit(C.Structure):
+    _fields_ = [("t_enter", C.c_double), ("level", C.c_uint8), ("leaf", C.c_uint8), ("pad", C.c_uint8 * 6)]
+
+
+assert C.sizeof(vxa_instance) == 136
+assert C.sizeof(vxa_hit_record) == 48
+assert C.sizeof(vxa_pixel_aov) == 40
+assert C.sizeof(vxa_local_ray) == 72
+assert C.sizeof(vxa_traverse_hit) == 96
+
+# numpy dtypes with the same layouts (for bulk AOV / ray arrays)
+try:
+    import numpy as np
+
+    AOV_DTYPE = np.dtype(
+        [("t", "<f8"), ("object_id", "<i4"), ("node_index", "<u4"), ("attr_index", "<u4"), ("voxel", "<u4", (3,)),
+         ("level", "u1"), ("kind", "u1"), ("traversals", "<u2"), ("node_fetches", "<u4")]
+    )
+    RAY_DTYPE = np.dtype([("origin", "<f8", (3,)), ("direction", "<f8", (3,)), ("half_extent", "<f8", (3,))])
+    TRAV_DTYPE = np.dtype(
+        [("t_hit", "<f8"), ("t_enter", "<f8"), ("t_exit", "<f8"), ("normal_local", "<f8", (3,)),
+         ("attribute", "u1", (4,)), ("attr_index", "<u4"), ("node_index", "<u4"), ("leaf_path", "u1", (16,)),
+         ("path_len", "u1"), ("hit", "u1"), ("pad", "<u2"), ("node_fetches", "<u4"), ("log_count", "<u4"),
+         ("log_total", "<u4")],
+        align=True,
+    )
+    assert AOV_DTYPE.itemsize == 40 and RAY_DTYPE.itemsize == 72 and TRAV_DTYPE.itemsize == 96
+except ImportError:  # pragma: no cover
+    np = None
+
+# Every symbol include/vxa.h declares (checked by tests/test_abi.py).
+VXA_SYMBOLS = [
+    "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
+    "vxa_upload_model", "vxa_release_model", "vxa_model_info",
+    "vxa_render", "vxa_submit", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
+    "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
+    "vxa_fb_export", "vxa_fb_import", "vxa_traverse",
+]
+VXN_SYMBOLS = [
+    "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
+    "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
+    "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
+    "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free",
+    "vxn_hbo_create", "vxn_hbo_free", "vxn_render", "vxn_traverse", "vxn_context",
+]
+
+P = C.c_void_p
+
+
+def _declare(lib, name, restype, *argtypes):
+    f = getattr(lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+
+
+def load_vxa(path: str | None = None) -> C.CDLL:
+    path = path or os.path.join(LIB_DIR, "libvxa.so")
+    if not os.path.exists(path):
+        raise RuntimeError(f"voxanim-b200: CUDA library {path} is missing; run __graft_entry__.build()")
+    lib = C.CDLL(path, mode=C.RTLD_LOCAL)
+    i, u32, u64, d = C.c_int, C.c_uint32, C.c_uint64, C.c_double
+    _declare(lib, "vxa_create", i, i, C.POINTER(P))
+    _declare(lib, "vxa_destroy", i, P)
+    _declare(lib, "vxa_last_error", C.c_char_p)
+    _declare(lib, "vxa_abi_version", i)
+    _declare(lib, "vxa_device_info", i, P, C.POINTER(i), C.POINTER(i), C.c_char_p, C.c_size_t)
+    _declare(lib, "vxa_upload_model", i, P, P, u32, P, u32, u32, C.POINTER(u32))
+    _declare(lib, "vxa_release_model", i, P, u32)
+    _declare(lib, "vxa_model_info", i, P, u32, C.POINTER(u64), C.POINTER(u32))
+    _declare(lib, "vxa_render", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32, P, P,
+             C.POINTER(vxa_stats))
+    _declare(lib, "vxa_submit", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32)
+    _declare(lib, "vxa_synchronize", i, P)
+    _declare(lib, "vxa_stats_read", i, P, C.POINTER(vxa_stats))
+    _declare(lib, "vxa_stats_reset", i, P)
+    _declare(lib, "vxa_read_framebuffer", i, P, P, C.c_int32, C.c_int32)
+    _declare(lib, "vxa_timer_begin", i, P)
+    _declare(lib, "vxa_timer_end", i, P, C.POINTER(d))
+    _declare(lib, "vxa_flush_l2", i, P)
+    _declare(lib, "vxa_stream", P, P)
+    _declare(lib, "vxa_fb_export", i, P, C.c_int32, C.c_int32, P)
+    _declare(lib, "vxa_fb_import", i, P, C.c_int32, C.c_int32, P)
+    _declare(lib, "vxa_traverse", i, P, u32, P, u32, u32, P, P, u32)
+    return lib
+
+
+def load_voxanim(path: str | None = None) -> C.CDLL:
+    load_vxa()
+    path = path or os.path.join(LIB_DIR, "libvoxanim.so")
+    if not os.path.exists(path):
+        raise RuntimeError(f"voxanim-b200: host library {path} is missing; run __graft_entry__.build()")
+    lib = C.CDLL(path, mode=C.RTLD_LOCAL)
+    i, u32, u64, d = C.c_int, C.c_uint32, C.c_uint64, C.c_double
+    _declare(lib, "vxn_last_error", C.c_char_p)
+    _declare(lib, "vxn_model_procedural", P, i, u32)
+    _declare(lib, "vxn_model_dense_sphere", P, u32)
+    _declare(lib, "vxn_model_random", P, u64, u32, d)
+    _declare(lib, "vxn_model_full_cube", P)
+    _declare(lib, "vxn_model_deserialize", P, P, C.c_size_t)
+    _declare(lib, "vxn_model_serialize", C.c_int64, P, P, C.c_size_t)
+    _declare(lib, "vxn_model_info", i, P, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))
+    _declare(lib, "vxn_model_validate", i, P)
+    _declare(lib, "vxn_model_free", None, P)
+    _declare(lib, "vxn_scene_config", P, i, C.POINTER(P), u32, u64, i, i)
+    _declare(lib, "vxn_scene_evaluate", i, P, d)
+    _declare(lib, "vxn_scene_mark_clean", i, P)
+    _declare(lib, "vxn_scene_set_camera_dirty", i, P, i)
+    _declare(lib, "vxn_scene_object_count", i, P)
+    _declare(lib, "vxn_scene_get_object", i, P, i, C.POINTER(C.c_int32), C.POINTER(d), C.POINTER(i))
+    _declare(lib, "vxn_scene_set_object", i, P, i, C.POINTER(d), i)
+    _declare(lib, "vxn_scene_export", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32,
+             C.POINTER(u32))
+    _declare(lib, "vxn_scene_free", None, P)
+    _declare(lib, "vxn_hbo_create", P, i, i)
+    _declare(lib, "vxn_hbo_free", None, P)
+    _declare(lib, "vxn_render", i, P, i, i, i, P, P, P, C.POINTER(u64), C.POINTER(d), C.POINTER(vxa_stats))
+    _declare(lib, "vxn_traverse", i, P, P, u32, P)
+    _declare(lib, "vxn_context", P)
+    return lib

@@ -1,0 +1,34 @@
+// Production FP32 instantiation of the frame and traversal kernels
+// (compiled with FMA contraction enabled: -fmad=true).
+#include "frame_kernel.cuh"
+#include "traverse_kernel.cuh"
+
+namespace vxa {
+
+namespace {
+template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<float, A, H>); }
+void* pick(bool aov, bool hbo) {
+    if (aov) return hbo ? frame_fn<true, true>() : frame_fn<true, false>();
+    return hbo ? frame_fn<false, true>() : frame_fn<false, false>();
+}
+} // namespace
+
+cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l) {
+    void* args[] = {const_cast<FrameParams<float>*>(&p)};
+    return cudaLaunchKernel(pick(aov, hbo), dim3(l.grid), dim3(128), args, 0, l.stream);
+}
+
+int frame_blocks_per_sm_f32(bool aov, bool hbo) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, pick(aov, hbo), 128, 0) != cudaSuccess) return 1;
+    return b > 0 ? b : 1;
+}
+
+cudaError_t launch_traverse_f32(const DevModel& m, const TraverseRayIn* rays, uint32_t n, TraverseRayOut* out,
+                                VisitOut* log, uint32_t log_cap, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    traverse_kernel<float><<<(n + 127) / 128, 128, 0, s>>>(m, rays, n, out, log, log_cap);
+    return cudaGetLastError();
+}
+
+} // namespace vxa

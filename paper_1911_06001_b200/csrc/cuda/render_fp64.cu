@@ -1,0 +1,35 @@
+// FP64 parity instantiation of the frame and traversal kernels
+// (compiled with -fmad=false: no FMA contraction, like the reference x86-64 build, so
+// every operation rounds exactly as the CPU renderer does).
+#include "frame_kernel.cuh"
+#include "traverse_kernel.cuh"
+
+namespace vxa {
+
+namespace {
+template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<double, A, H>); }
+void* pick(bool aov, bool hbo) {
+    if (aov) return hbo ? frame_fn<true, true>() : frame_fn<true, false>();
+    return hbo ? frame_fn<false, true>() : frame_fn<false, false>();
+}
+} // namespace
+
+cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l) {
+    void* args[] = {const_cast<FrameParams<double>*>(&p)};
+    return cudaLaunchKernel(pick(aov, hbo), dim3(l.grid), dim3(128), args, 0, l.stream);
+}
+
+int frame_blocks_per_sm_f64(bool aov, bool hbo) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, pick(aov, hbo), 128, 0) != cudaSuccess) return 1;
+    return b > 0 ? b : 1;
+}
+
+cudaError_t launch_traverse_f64(const DevModel& m, const TraverseRayIn* rays, uint32_t n, TraverseRayOut* out,
+                                VisitOut* log, uint32_t log_cap, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    traverse_kernel<double><<<(n + 127) / 128, 128, 0, s>>>(m, rays, n, out, log, log_cap);
+    return cudaGetLastError();
+}
+
+} // namespace vxa

@@ -1,0 +1,689 @@
+// C ABI of the CUDA layer (include/vxa.h): device context, model cache and
+// repack, per-frame instance constants, frame submission, readback, timing
+// and the multi-GPU framebuffer mapping.
+//
+// Host arithmetic in this file feeds the FP64 parity kernel, so it is written
+// in the reference's operand order (bounding_sphere scene.cpp:16-20,
+// transform_ray_world_to_local math.hpp:206-224, bounds_from_scale
+// traversal.hpp:21-23, ray_box_params traversal.cpp:30-61) and compiled with
+// -ffp-contract=off.
+#include "vxa.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "vxa_internal.h"
+
+using namespace vxa;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+#define VXA_CUDA(call)                                                                                    \
+    do {                                                                                                  \
+        const cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? VXA_ERR_OOM : VXA_ERR_CUDA,                     \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                              \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device helper kernels
+
+// 12-byte SvoNode records -> packed {valid | leaf << 8 | mixed, base} words.
+__global__ void repack_nodes(const uint32_t* __restrict__ raw, uint32_t n, uint2* __restrict__ words,
+                             uint32_t* __restrict__ side) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t child_base = raw[3 * i], attr_base = raw[3 * i + 1], masks = raw[3 * i + 2];
+    const uint32_t valid = masks & 0xffu, leaf = (masks >> 8) & 0xffu;
+    const uint32_t internal = valid & ~leaf & 0xffu, leaves = valid & leaf;
+    uint2 w;
+    w.x = valid | (leaf << 8) | ((internal && leaves) ? kMixed : 0u);
+    w.y = internal ? child_base : attr_base;
+    words[i] = w;
+    if (side != nullptr) side[i] = attr_base;
+}
+
+// RGBA8 framebuffer -> RGB8 (four pixels per thread: 16 B in, 12 B out).
+__global__ void pack_rgb(const uint32_t* __restrict__ fb, uint8_t* __restrict__ rgb, size_t n_pix) {
+    const size_t q = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t p0 = q * 4;
+    if (p0 >= n_pix) return;
+    if (p0 + 4 <= n_pix) {
+        const uint4 v = reinterpret_cast<const uint4*>(fb)[q];
+        const uint32_t a = (v.x & 0xffffffu) | (v.y << 24);
+        const uint32_t b = ((v.y >> 8) & 0xffffu) | (v.z << 16);
+        const uint32_t c = ((v.z >> 16) & 0xffu) | (v.w << 8);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(rgb + p0 * 3);
+        dst[0] = a;
+        dst[1] = b;
+        dst[2] = c;
+    } else {
+        for (size_t p = p0; p < n_pix; ++p) {
+            const uint32_t v = fb[p];
+            rgb[3 * p] = static_cast<uint8_t>(v);
+            rgb[3 * p + 1] = static_cast<uint8_t>(v >> 8);
+            rgb[3 * p + 2] = static_cast<uint8_t>(v >> 16);
+        }
+    }
+}
+
+struct ModelEntry {
+    DevModel dev{};
+    uint2* words = nullptr;
+    uint32_t* side = nullptr;
+    uint32_t* attrs = nullptr;
+    uint64_t bytes = 0;
+};
+
+template <typename T> struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0; // elements
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        const cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+} // namespace
+
+struct vxa_ctx {
+    int device = 0;
+    int sm_count = 0;
+    char name[256] = {};
+    cudaStream_t stream = nullptr;
+    std::map<uint32_t, ModelEntry> models;
+    uint32_t next_handle = 1;
+
+    DevBuf<uint32_t> fb;  // resident RGBA8 framebuffer
+    int32_t fb_w = 0, fb_h = 0;
+    uint32_t* peer_fb = nullptr; // rank 0's framebuffer mapped via CUDA IPC
+    int32_t peer_w = 0, peer_h = 0;
+
+    DevBuf<uint32_t> tile_counter;
+    DevBuf<unsigned long long> counters;
+    DevBuf<unsigned char> inst_dev;
+    unsigned char* inst_host[2] = {nullptr, nullptr};
+    size_t inst_host_cap = 0;
+    cudaEvent_t inst_done[2] = {nullptr, nullptr};
+    int inst_slot = 0;
+
+    DevBuf<PixelAov> aov;
+    DevBuf<HitRec> hbo;
+    DevBuf<uint8_t> rgb;
+    DevBuf<unsigned char> l2_scratch;
+    DevBuf<TraverseRayIn> rays;
+    DevBuf<TraverseRayOut> hits;
+    DevBuf<VisitOut> visits;
+
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, t_a = nullptr, t_b = nullptr;
+    int occ[2][2][2] = {}; // [precision][aov][hbo]
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// per-frame instance constants
+
+template <typename Real> struct HostFrame {
+    std::vector<DevInstance<Real>> inst;
+};
+
+// Builds the device instance table in id order (index order == the
+// reference's id tie-break order). Returns VXA_OK or an error.
+template <typename Real>
+int build_instances(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n,
+                    std::vector<DevInstance<Real>>& out) {
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return in[a].id < in[b].id; });
+    out.resize(n);
+    const double* o = f->camera.position;
+    const double* C = f->camera.orientation;
+    for (uint32_t k = 0; k < n; ++k) {
+        const vxa_instance& s = in[order[k]];
+        DevInstance<Real>& d = out[k];
+        std::memset(&d, 0, sizeof(d));
+        d.id = s.id;
+        d.dirty = s.dirty;
+        const auto it = ctx->models.find(s.model);
+        if (it == ctx->models.end()) {
+            d.valid_model = 0; // reference: objects without a model are skipped (renderer.cpp:74-76)
+        } else {
+            d.valid_model = 1;
+            d.model = it->second.dev;
+        }
+        const double* R = s.rotation;
+        const double* t = s.translation;
+        // bounding sphere: centre = translation, r = 0.5 |scale|
+        const double l[3] = {t[0] - o[0], t[1] - o[1], t[2] - o[2]};
+        const double L2 = l[0] * l[0] + l[1] * l[1] + l[2] * l[2];
+        const double r = 0.5 * std::sqrt(s.scale[0] * s.scale[0] + s.scale[1] * s.scale[1] + s.scale[2] * s.scale[2]);
+        const double r2 = r * r;
+        // local ray origin: R^T (o + (-t))
+        const double v[3] = {o[0] + -t[0], o[1] + -t[1], o[2] + -t[2]};
+        double Rt[9];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) Rt[3 * i + j] = R[3 * j + i];
+        double ol[3];
+        for (int i = 0; i < 3; ++i) ol[i] = Rt[3 * i] * v[0] + Rt[3 * i + 1] * v[1] + Rt[3 * i + 2] * v[2];
+        const double h[3] = {s.scale[0] * 0.5, s.scale[1] * 0.5, s.scale[2] * 0.5};
+        for (int a = 0; a < 3; ++a) {
+            d.L[a] = static_cast<Real>(l[a]);
+            d.A_lo[a] = static_cast<Real>(-h[a] - ol[a]);
+            d.A_hi[a] = static_cast<Real>(h[a] - ol[a]);
+            d.zbits[a] = zero_dir_bits(ol[a], h[a]);
+            if (-h[a] > ol[a]) d.zflags |= 1u << a;
+            if (h[a] > ol[a]) d.zflags |= 1u << (3 + a);
+        }
+        d.L2 = static_cast<Real>(L2);
+        d.r = static_cast<Real>(r);
+        d.r2 = static_cast<Real>(r2);
+        for (int i = 0; i < 9; ++i) d.R[i] = static_cast<Real>(R[i]);
+        if constexpr (sizeof(Real) == 8) {
+            for (int i = 0; i < 9; ++i) d.M[i] = Rt[i];
+        } else {
+            // camera -> local rotation, folded in FP64 and rounded once
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    double acc = 0.0;
+                    for (int k2 = 0; k2 < 3; ++k2) acc += Rt[3 * i + k2] * C[3 * k2 + j];
+                    d.M[3 * i + j] = static_cast<float>(acc);
+                }
+        }
+    }
+    return VXA_OK;
+}
+
+template <typename Real> void fill_camera(FrameParams<Real>& p, const vxa_frame_desc* f) {
+    const vxa_camera& c = f->camera;
+    // std::tan on the host: the CUDA tan differs from glibc in the last ulp.
+    const double tan_half = std::tan(c.vertical_fov_deg * 3.14159265358979323846 / 360.0);
+    const double aspect = static_cast<double>(c.width) / c.height;
+    for (int k = 0; k < 3; ++k) p.cam_pos[k] = static_cast<Real>(c.position[k]);
+    for (int k = 0; k < 9; ++k) p.C[k] = static_cast<Real>(c.orientation[k]);
+    p.tan_half = static_cast<Real>(tan_half);
+    p.aspect = static_cast<Real>(aspect);
+    p.inv_w2 = static_cast<Real>(2.0 / c.width);
+    p.inv_h2 = static_cast<Real>(2.0 / c.height);
+    p.sx = static_cast<Real>(tan_half * aspect);
+    p.sy = static_cast<Real>(tan_half);
+    p.width = c.width;
+    p.height = c.height;
+}
+
+int ensure_staging(vxa_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->inst_host_cap) return VXA_OK;
+    for (int s = 0; s < 2; ++s) {
+        if (ctx->inst_host[s]) {
+            cudaEventSynchronize(ctx->inst_done[s]);
+            cudaFreeHost(ctx->inst_host[s]);
+            ctx->inst_host[s] = nullptr;
+        }
+    }
+    const size_t cap = std::max<size_t>(bytes, 64 * 1024);
+    for (int s = 0; s < 2; ++s) VXA_CUDA(cudaHostAlloc(&ctx->inst_host[s], cap, cudaHostAllocDefault));
+    ctx->inst_host_cap = cap;
+    return VXA_OK;
+}
+
+int check_frame(const vxa_frame_desc* f) {
+    if (f == nullptr) return fail(VXA_ERR_INVALID, "null frame descriptor");
+    if (f->camera.width < 1 || f->camera.height < 1) return fail(VXA_ERR_INVALID, "camera resolution must be at least 1x1");
+    if (f->tile_world < 1 || f->tile_rank < 0 || f->tile_rank >= f->tile_world)
+        return fail(VXA_ERR_INVALID, "tile partition rank/world out of range");
+    if (f->precision != VXA_FP32 && f->precision != VXA_FP64) return fail(VXA_ERR_INVALID, "unknown precision");
+    return VXA_OK;
+}
+
+// Enqueues one frame. aov/hbo are device buffers or null.
+template <typename Real>
+int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov,
+                  HitRec* hbo, bool reset_counters) {
+    std::vector<DevInstance<Real>> tab;
+    if (int rc = build_instances<Real>(ctx, f, in, n, tab); rc != VXA_OK) return rc;
+    const size_t bytes = tab.size() * sizeof(DevInstance<Real>);
+    if (int rc = ensure_staging(ctx, bytes); rc != VXA_OK) return rc;
+    VXA_CUDA(ctx->inst_dev.ensure(std::max<size_t>(bytes, 1)));
+    const int slot = ctx->inst_slot;
+    ctx->inst_slot ^= 1;
+    VXA_CUDA(cudaEventSynchronize(ctx->inst_done[slot])); // staging slot no longer read by an earlier copy
+    if (bytes) std::memcpy(ctx->inst_host[slot], tab.data(), bytes);
+
+    const int32_t W = f->camera.width, H = f->camera.height;
+    VXA_CUDA(ctx->fb.ensure(static_cast<size_t>(W) * H));
+    ctx->fb_w = W;
+    ctx->fb_h = H;
+    uint32_t* target = ctx->fb.ptr;
+    if (f->tile_world > 1 && ctx->peer_fb != nullptr) {
+        if (ctx->peer_w != W || ctx->peer_h != H) return fail(VXA_ERR_INVALID, "peer framebuffer size mismatch");
+        target = ctx->peer_fb;
+    }
+
+    FrameParams<Real> p{};
+    fill_camera(p, f);
+    p.inst = reinterpret_cast<const DevInstance<Real>*>(ctx->inst_dev.ptr);
+    p.n_inst = n;
+    p.background = f->background[0] | (uint32_t{f->background[1]} << 8) | (uint32_t{f->background[2]} << 16) | 0xff000000u;
+    p.culling = f->culling ? 1u : 0u;
+    p.sorting = f->sorting ? 1u : 0u;
+    p.sphere_pass = (f->culling || f->sorting || hbo != nullptr) ? 1u : 0u;
+    p.camera_dirty = f->camera_dirty ? 1u : 0u;
+    p.rank = f->tile_rank;
+    p.world = f->tile_world;
+    p.n_super_x = static_cast<uint32_t>((W + kSuper - 1) / kSuper);
+    const uint32_t n_super = p.n_super_x * static_cast<uint32_t>((H + kSuper - 1) / kSuper);
+    const uint32_t mine = (n_super + static_cast<uint32_t>(f->tile_world - f->tile_rank) - 1) / static_cast<uint32_t>(f->tile_world);
+    p.n_tiles = mine * static_cast<uint32_t>(kTilesPerSuper);
+    p.fb = target;
+    p.tile_counter = ctx->tile_counter.ptr;
+    p.counters = ctx->counters.ptr;
+    p.aov = aov;
+    p.hbo = hbo;
+
+    if (bytes) VXA_CUDA(cudaMemcpyAsync(ctx->inst_dev.ptr, ctx->inst_host[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    VXA_CUDA(cudaEventRecord(ctx->inst_done[slot], ctx->stream));
+    VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, sizeof(uint32_t), ctx->stream));
+    if (reset_counters) VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
+
+    const bool is64 = sizeof(Real) == 8;
+    const bool a = aov != nullptr, h = hbo != nullptr;
+    int& occ = ctx->occ[is64][a][h];
+    if (occ == 0) occ = is64 ? frame_blocks_per_sm_f64(a, h) : frame_blocks_per_sm_f32(a, h);
+    FrameLaunch l{ctx->sm_count * occ, ctx->stream};
+    cudaError_t e;
+    if constexpr (sizeof(Real) == 8)
+        e = launch_frame_f64(p, a, h, l);
+    else
+        e = launch_frame_f32(p, a, h, l);
+    if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
+    return VXA_OK;
+}
+
+int enqueue_any(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov, HitRec* hbo,
+                bool reset) {
+    if (f->precision == VXA_FP64) return enqueue_frame<double>(ctx, f, in, n, aov, hbo, reset);
+    return enqueue_frame<float>(ctx, f, in, n, aov, hbo, reset);
+}
+
+int read_counters(vxa_ctx* ctx, vxa_stats* s) {
+    unsigned long long c[8] = {};
+    VXA_CUDA(cudaMemcpyAsync(c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    s->rays = c[0];
+    s->sphere_tests = c[1];
+    s->svo_traversals = c[2];
+    s->pixels_reused = c[3];
+    s->node_fetches = c[4];
+    s->leaf_hits = c[5];
+    return VXA_OK;
+}
+
+} // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+const char* vxa_last_error(void) { return g_error.c_str(); }
+
+int vxa_abi_version(void) { return VXA_ABI_VERSION; }
+
+int vxa_create(int device, vxa_ctx** out) {
+    if (out == nullptr) return fail(VXA_ERR_INVALID, "null output pointer");
+    *out = nullptr;
+    if (device < 0) {
+        const char* env = std::getenv("VOXANIM_DEVICE");
+        device = env ? std::atoi(env) : 0;
+    }
+    int count = 0;
+    const cudaError_t ce = cudaGetDeviceCount(&count);
+    if (ce != cudaSuccess || count == 0)
+        return fail(VXA_ERR_NO_DEVICE, std::string("no CUDA device available: ") + cudaGetErrorString(ce));
+    if (device >= count) return fail(VXA_ERR_NO_DEVICE, "device ordinal out of range");
+    cudaDeviceProp prop{};
+    VXA_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(VXA_ERR_NO_DEVICE, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+    VXA_CUDA(cudaSetDevice(device));
+    auto ctx = std::make_unique<vxa_ctx>();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    std::snprintf(ctx->name, sizeof(ctx->name), "%s", prop.name);
+    VXA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    VXA_CUDA(ctx->tile_counter.ensure(1));
+    VXA_CUDA(ctx->counters.ensure(8));
+    VXA_CUDA(cudaMemset(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long)));
+    for (int s = 0; s < 2; ++s) {
+        VXA_CUDA(cudaEventCreateWithFlags(&ctx->inst_done[s], cudaEventDisableTiming));
+        VXA_CUDA(cudaEventRecord(ctx->inst_done[s], ctx->stream));
+    }
+    VXA_CUDA(cudaEventCreate(&ctx->ev_a));
+    VXA_CUDA(cudaEventCreate(&ctx->ev_b));
+    VXA_CUDA(cudaEventCreate(&ctx->t_a));
+    VXA_CUDA(cudaEventCreate(&ctx->t_b));
+    *out = ctx.release();
+    return VXA_OK;
+}
+
+int vxa_destroy(vxa_ctx* ctx) {
+    if (ctx == nullptr) return VXA_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& [h, m] : ctx->models) {
+        cudaFree(m.words);
+        cudaFree(m.side);
+        cudaFree(m.attrs);
+    }
+    if (ctx->peer_fb) cudaIpcCloseMemHandle(ctx->peer_fb);
+    ctx->fb.release();
+    ctx->tile_counter.release();
+    ctx->counters.release();
+    ctx->inst_dev.release();
+    ctx->aov.release();
+    ctx->hbo.release();
+    ctx->rgb.release();
+    ctx->l2_scratch.release();
+    ctx->rays.release();
+    ctx->hits.release();
+    ctx->visits.release();
+    for (int s = 0; s < 2; ++s) {
+        if (ctx->inst_host[s]) cudaFreeHost(ctx->inst_host[s]);
+        if (ctx->inst_done[s]) cudaEventDestroy(ctx->inst_done[s]);
+    }
+    for (cudaEvent_t e : {ctx->ev_a, ctx->ev_b, ctx->t_a, ctx->t_b})
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return VXA_OK;
+}
+
+int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t name_len) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    if (device) *device = ctx->device;
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (name && name_len) std::snprintf(name, name_len, "%s", ctx->name);
+    return VXA_OK;
+}
+
+int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const void* attrs, uint32_t attr_count,
+                     uint32_t depth, uint32_t* handle_out) {
+    if (ctx == nullptr || handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    if (nodes == nullptr || node_count == 0) return fail(VXA_ERR_MODEL, "model has no root node");
+    if (depth < 1 || depth > kMaxDepth) return fail(VXA_ERR_MODEL, "depth out of range [1, 16]");
+    if (attr_count > 0 && attrs == nullptr) return fail(VXA_ERR_INVALID, "null attribute array");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    // reference validate() rules (svo.cpp:134-172)
+    const auto* raw = static_cast<const uint8_t*>(nodes);
+    bool any_mixed = false;
+    for (uint32_t i = 0; i < node_count; ++i) {
+        uint32_t cb, ab;
+        std::memcpy(&cb, raw + 12 * size_t{i}, 4);
+        std::memcpy(&ab, raw + 12 * size_t{i} + 4, 4);
+        const uint32_t valid = raw[12 * size_t{i} + 8], leaf = raw[12 * size_t{i} + 9];
+        if (leaf & ~valid) return fail(VXA_ERR_MODEL, "node " + std::to_string(i) + ": leaf_mask outside valid_mask");
+        const uint32_t internal = valid & ~leaf & 0xffu, leaves = valid & leaf;
+        const int ni = __builtin_popcount(internal), nl = __builtin_popcount(leaves);
+        if (ni > 0 && (uint64_t{cb} + ni > node_count || cb <= i))
+            return fail(VXA_ERR_MODEL, "node " + std::to_string(i) + ": child_base out of range");
+        if (nl > 0 && uint64_t{ab} + nl > attr_count)
+            return fail(VXA_ERR_MODEL, "node " + std::to_string(i) + ": attr_base out of range");
+        any_mixed |= ni > 0 && nl > 0;
+    }
+    ModelEntry m;
+    uint32_t* raw_dev = nullptr;
+    const size_t raw_bytes = 12 * size_t{node_count};
+    VXA_CUDA(cudaMalloc(&raw_dev, raw_bytes));
+    cudaError_t e = cudaMalloc(&m.words, sizeof(uint2) * node_count);
+    if (e == cudaSuccess && any_mixed) e = cudaMalloc(&m.side, sizeof(uint32_t) * node_count);
+    if (e == cudaSuccess) e = cudaMalloc(&m.attrs, sizeof(uint32_t) * std::max<uint32_t>(attr_count, 1));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(raw_dev, nodes, raw_bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess && attr_count)
+        e = cudaMemcpyAsync(m.attrs, attrs, sizeof(uint32_t) * attr_count, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) {
+        repack_nodes<<<(node_count + 255) / 256, 256, 0, ctx->stream>>>(raw_dev, node_count, m.words, m.side);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(raw_dev);
+    if (e != cudaSuccess) {
+        cudaFree(m.words);
+        cudaFree(m.side);
+        cudaFree(m.attrs);
+        return fail(e == cudaErrorMemoryAllocation ? VXA_ERR_OOM : VXA_ERR_CUDA,
+                    std::string("model upload: ") + cudaGetErrorString(e));
+    }
+    m.dev.words = m.words;
+    m.dev.side = m.side;
+    m.dev.attrs = m.attrs;
+    m.dev.depth = depth;
+    m.dev.node_count = node_count;
+    m.bytes = sizeof(uint2) * uint64_t{node_count} + (any_mixed ? 4ull * node_count : 0) + 4ull * attr_count;
+    const uint32_t handle = ctx->next_handle++;
+    ctx->models[handle] = m;
+    *handle_out = handle;
+    return VXA_OK;
+}
+
+int vxa_release_model(vxa_ctx* ctx, uint32_t handle) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    const auto it = ctx->models.find(handle);
+    if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(it->second.words);
+    cudaFree(it->second.side);
+    cudaFree(it->second.attrs);
+    ctx->models.erase(it);
+    return VXA_OK;
+}
+
+int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32_t* node_format) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    const auto it = ctx->models.find(handle);
+    if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
+    if (device_bytes) *device_bytes = it->second.bytes;
+    if (node_format) *node_format = 2;
+    return VXA_OK;
+}
+
+int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, uint8_t* rgb_out,
+               vxa_pixel_aov* aov_out, vxa_stats* stats) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    if (int rc = check_frame(f); rc != VXA_OK) return rc;
+    if (n > 0 && in == nullptr) return fail(VXA_ERR_INVALID, "null instance array");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const size_t npix = static_cast<size_t>(f->camera.width) * f->camera.height;
+    PixelAov* aov = nullptr;
+    HitRec* hbo = nullptr;
+    if (aov_out) {
+        VXA_CUDA(ctx->aov.ensure(npix));
+        aov = ctx->aov.ptr;
+        VXA_CUDA(cudaMemsetAsync(aov, 0, npix * sizeof(PixelAov), ctx->stream));
+    }
+    if (f->hbo) {
+        VXA_CUDA(ctx->hbo.ensure(npix));
+        hbo = ctx->hbo.ptr;
+        VXA_CUDA(cudaMemcpyAsync(hbo, f->hbo, npix * sizeof(HitRec), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    VXA_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
+    if (int rc = enqueue_any(ctx, f, in, n, aov, hbo, true); rc != VXA_OK) return rc;
+    VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
+    uint64_t launches = 1;
+    if (rgb_out) {
+        VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
+        const size_t quads = (npix + 3) / 4;
+        pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rgb.ptr, npix);
+        VXA_CUDA(cudaGetLastError());
+        ++launches;
+        VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (aov_out)
+        VXA_CUDA(cudaMemcpyAsync(aov_out, aov, npix * sizeof(PixelAov), cudaMemcpyDeviceToHost, ctx->stream));
+    if (f->hbo) VXA_CUDA(cudaMemcpyAsync(f->hbo, hbo, npix * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (stats) {
+        if (int rc = read_counters(ctx, stats); rc != VXA_OK) return rc;
+        float ms = 0.f;
+        VXA_CUDA(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+        stats->gpu_ms = ms;
+        stats->kernel_launches = launches;
+    }
+    return VXA_OK;
+}
+
+int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    if (int rc = check_frame(f); rc != VXA_OK) return rc;
+    if (f->hbo) return fail(VXA_ERR_INVALID, "vxa_submit does not take a hit buffer");
+    if (n > 0 && in == nullptr) return fail(VXA_ERR_INVALID, "null instance array");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    return enqueue_any(ctx, f, in, n, nullptr, nullptr, false);
+}
+
+int vxa_synchronize(vxa_ctx* ctx) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VXA_OK;
+}
+
+int vxa_stats_read(vxa_ctx* ctx, vxa_stats* stats) {
+    if (ctx == nullptr || stats == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    *stats = vxa_stats{};
+    return read_counters(ctx, stats);
+}
+
+int vxa_stats_reset(vxa_ctx* ctx) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
+    return VXA_OK;
+}
+
+int vxa_read_framebuffer(vxa_ctx* ctx, uint8_t* rgb_out, int32_t width, int32_t height) {
+    if (ctx == nullptr || rgb_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    if (width != ctx->fb_w || height != ctx->fb_h) return fail(VXA_ERR_INVALID, "framebuffer size mismatch");
+    const size_t npix = static_cast<size_t>(width) * height;
+    VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
+    const size_t quads = (npix + 3) / 4;
+    pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rgb.ptr, npix);
+    VXA_CUDA(cudaGetLastError());
+    VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VXA_OK;
+}
+
+int vxa_timer_begin(vxa_ctx* ctx) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    VXA_CUDA(cudaEventRecord(ctx->t_a, ctx->stream));
+    return VXA_OK;
+}
+
+int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms) {
+    if (ctx == nullptr || elapsed_ms == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    VXA_CUDA(cudaEventRecord(ctx->t_b, ctx->stream));
+    VXA_CUDA(cudaEventSynchronize(ctx->t_b));
+    float ms = 0.f;
+    VXA_CUDA(cudaEventElapsedTime(&ms, ctx->t_a, ctx->t_b));
+    *elapsed_ms = ms;
+    return VXA_OK;
+}
+
+int vxa_flush_l2(vxa_ctx* ctx) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    const size_t bytes = size_t{256} << 20; // 2x the 126 MB L2
+    VXA_CUDA(ctx->l2_scratch.ensure(bytes));
+    VXA_CUDA(cudaMemsetAsync(ctx->l2_scratch.ptr, ctx->inst_slot, bytes, ctx->stream));
+    return VXA_OK;
+}
+
+void* vxa_stream(vxa_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_out) {
+    if (ctx == nullptr || ipc_handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    if (width < 1 || height < 1) return fail(VXA_ERR_INVALID, "bad framebuffer size");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    VXA_CUDA(ctx->fb.ensure(static_cast<size_t>(width) * height));
+    ctx->fb_w = width;
+    ctx->fb_h = height;
+    cudaIpcMemHandle_t h;
+    VXA_CUDA(cudaIpcGetMemHandle(&h, ctx->fb.ptr));
+    std::memcpy(ipc_handle_out, &h, sizeof(h));
+    return VXA_OK;
+}
+
+int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle) {
+    if (ctx == nullptr || ipc_handle == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    if (ctx->peer_fb) {
+        cudaIpcCloseMemHandle(ctx->peer_fb);
+        ctx->peer_fb = nullptr;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof(h));
+    void* p = nullptr;
+    VXA_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->peer_fb = static_cast<uint32_t*>(p);
+    ctx->peer_w = width;
+    ctx->peer_h = height;
+    return VXA_OK;
+}
+
+int vxa_traverse(vxa_ctx* ctx, uint32_t model, const vxa_local_ray* rays, uint32_t n, uint32_t precision,
+                 vxa_traverse_hit* hits, vxa_visit* log, uint32_t log_capacity) {
+    static_assert(sizeof(vxa_local_ray) == sizeof(TraverseRayIn));
+    static_assert(sizeof(vxa_traverse_hit) == sizeof(TraverseRayOut));
+    static_assert(sizeof(vxa_visit) == sizeof(VisitOut));
+    if (ctx == nullptr || (n > 0 && (rays == nullptr || hits == nullptr))) return fail(VXA_ERR_INVALID, "null argument");
+    const auto it = ctx->models.find(model);
+    if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
+    if (n == 0) return VXA_OK;
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    VXA_CUDA(ctx->rays.ensure(n));
+    VXA_CUDA(ctx->hits.ensure(n));
+    VisitOut* dlog = nullptr;
+    if (log != nullptr && log_capacity > 0) {
+        VXA_CUDA(ctx->visits.ensure(size_t{n} * log_capacity));
+        dlog = ctx->visits.ptr;
+    }
+    VXA_CUDA(cudaMemcpyAsync(ctx->rays.ptr, rays, sizeof(TraverseRayIn) * n, cudaMemcpyHostToDevice, ctx->stream));
+    const cudaError_t e = precision == VXA_FP64
+                              ? launch_traverse_f64(it->second.dev, ctx->rays.ptr, n, ctx->hits.ptr, dlog,
+                                                    dlog ? log_capacity : 0, ctx->stream)
+                              : launch_traverse_f32(it->second.dev, ctx->rays.ptr, n, ctx->hits.ptr, dlog,
+                                                    dlog ? log_capacity : 0, ctx->stream);
+    if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("traverse launch: ") + cudaGetErrorString(e));
+    VXA_CUDA(cudaMemcpyAsync(hits, ctx->hits.ptr, sizeof(TraverseRayOut) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (dlog)
+        VXA_CUDA(cudaMemcpyAsync(log, dlog, sizeof(VisitOut) * n * size_t{log_capacity}, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VXA_OK;
+}
+
+} // extern "C"

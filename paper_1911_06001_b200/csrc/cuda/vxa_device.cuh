@@ -1,0 +1,356 @@
+// Device-side data layout and the per-ray pipeline of the voxanim-b200 frame.
+//
+// One template serves two instantiations:
+//   Real = double : the parity kernel. Compiled with -fmad=false and written in
+//                   the reference's operand order, it reproduces the CPU
+//                   renderer bit for bit (ray generation renderer.cpp:11-23,
+//                   sphere test :25-43, candidate order :134-141,171-203,
+//                   trace_ray :63-100, shade :102-113, traversal
+//                   traversal.cpp:30-245).
+//   Real = float  : the production kernel. Same decision structure (mirror
+//                   mask, midpoint recurrence, strict-comparison tie rules,
+//                   skip-not-break, nearest (t, id)), FP32 arithmetic, with the
+//                   per-instance constants (local ray origin, slab plane
+//                   offsets, camera-to-local rotation) folded on the host in
+//                   FP64 so each frame's FP32 inputs are rounded once.
+//
+// HBM layout of a model (built by the upload kernel in vxa_abi.cu, node
+// numbering identical to SvoModel::nodes):
+//   words : uint2 per node  {x = valid | leaf << 8 | kMixed, y = base}
+//           base = child_base when the node has internal children, else
+//           attr_base; kMixed marks the rare node with both kinds, whose
+//           attr_base then lives in side[node].
+//   attrs : uint32 RGBA8 per attribute.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vxa {
+
+constexpr uint32_t kMaxDepth = 16;
+constexpr uint32_t kExit = 8;
+constexpr uint32_t kMixed = 1u << 16;
+
+// Work decomposition: 8x4-pixel warp tiles inside 64x64 super-tiles; super-tiles
+// are the unit of the multi-GPU screen partition.
+constexpr int kTileW = 8, kTileH = 4;
+constexpr int kSuper = 64;
+constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
+
+struct DevModel {
+    const uint2* words;
+    const uint32_t* side;
+    const uint32_t* attrs;
+    uint32_t depth;
+    uint32_t node_count;
+};
+
+// Per-instance frame constants, rebuilt on the host every frame from the FP64
+// RigidTransform + Camera (vxa_abi.cu: build_instances).
+template <typename Real> struct DevInstance {
+    DevModel model;
+    Real L[3];    // sphere centre - camera position
+    Real L2;      // |L|^2 (reference: l.norm2())
+    Real r, r2;   // radius, radius^2
+    Real M[9];    // FP64: R^T (world -> local); FP32: R^T C (camera -> local)
+    Real R[9];    // world rotation (FP64 normal = R n_local)
+    Real A_lo[3]; // -h - o_local  (o_local = R^T (cam - t), FP64)
+    Real A_hi[3]; //  h - o_local
+    uint32_t zbits[3]; // zero-direction path: bit L set iff o >= centre at level L
+    uint32_t zflags;   // bit a: (-h > o); bit 3+a: (h > o)   (zero-direction slab signs)
+    int32_t id;
+    uint32_t dirty;
+    uint32_t valid_model;
+    uint32_t pad;
+};
+
+template <typename Real> struct FrameParams {
+    const DevInstance<Real>* inst;
+    uint32_t n_inst;
+    int32_t width, height;
+    // camera
+    Real cam_pos[3];
+    Real C[9];         // camera orientation (row-major)
+    Real tan_half;     // std::tan(fov * pi / 360), host-evaluated
+    Real aspect;       // (double)W / H
+    Real inv_w2, inv_h2; // FP32 ray setup: 2/W, 2/H
+    Real sx, sy;       // FP32 ray setup: tan_half * aspect, tan_half
+    uint32_t background; // RGBA8
+    uint32_t culling, sorting, sphere_pass;
+    uint32_t camera_dirty;
+    // partition
+    int32_t rank, world;
+    uint32_t n_super_x;
+    uint32_t n_tiles; // warp tiles owned by this rank
+    // outputs
+    uint32_t* fb;                 // RGBA8 framebuffer (local or peer-mapped)
+    uint32_t* tile_counter;       // persistent-thread work counter
+    unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
+    void* aov;                    // vxa_pixel_aov* or null
+    void* hbo;                    // vxa_hit_record* (device copy) or null
+};
+
+// Host-layout records written by the kernel (match include/vxa.h).
+struct PixelAov {
+    double t;
+    int32_t object_id;
+    uint32_t node_index;
+    uint32_t attr_index;
+    uint32_t voxel[3];
+    uint8_t level;
+    uint8_t kind;
+    uint16_t traversals;
+    uint32_t node_fetches;
+};
+static_assert(sizeof(PixelAov) == 40, "vxa_pixel_aov layout");
+
+struct HitRec {
+    uint32_t color;
+    uint32_t pad0;
+    double normal[3];
+    double t;
+    int32_t object_id;
+    uint8_t kind;
+    uint8_t pad1[3];
+};
+static_assert(sizeof(HitRec) == 48, "voxanim::HitRecord layout");
+
+// ---------------------------------------------------------------------------
+// Node access
+
+__device__ __forceinline__ uint2 load_node(const DevModel& m, uint32_t idx) { return __ldg(m.words + idx); }
+
+__device__ __forceinline__ uint32_t popc8_below(uint32_t mask, uint32_t bit) { return __popc(mask & (bit - 1u)); }
+
+// ---------------------------------------------------------------------------
+// Traversal core: Revelles parametric traversal, iterative, explicit stack.
+// Follows proj/src/traversal.cpp:115-245 decision for decision.
+
+template <typename Real> struct LocalRay {
+    Real d[3];       // unmirrored local direction
+    Real t0[3], t1[3]; // root slab parameters of the mirrored ray
+    uint32_t mirror; // octant bits of mirrored axes
+    uint32_t zero;   // octant bits of zero-direction axes
+    uint32_t zbits[3];
+};
+
+template <typename Real> struct TravHit {
+    Real t;              // max(t_enter, 0)
+    Real t_enter_root, t_exit_root;
+    uint32_t attr;       // attribute index
+    uint32_t parent;     // node index of the leaf's parent
+    uint32_t level;      // path_len
+    uint32_t axis;       // entry axis
+    unsigned long long path; // octant per level, 4 bits each
+    uint32_t fetches;
+};
+
+__device__ __forceinline__ uint32_t axis_bit(int a) { return 4u >> a; } // x=4, y=2, z=1
+
+template <typename Real> __device__ __forceinline__ Real pos_inf() {
+    if constexpr (sizeof(Real) == 8)
+        return __longlong_as_double(0x7ff0000000000000ll);
+    else
+        return __int_as_float(0x7f800000);
+}
+
+// Root slab (traversal.cpp:30-61) from host-folded plane offsets:
+// unmirrored t0 = A_lo / d, t1 = A_hi / d; a mirrored axis (d < 0) swaps
+// them, which is bit-identical to the reference's (-h - (-o)) / (-d) form.
+template <typename Real>
+__device__ __forceinline__ void setup_root(LocalRay<Real>& r, const Real A_lo[3], const Real A_hi[3],
+                                           uint32_t zflags, const uint32_t zbits[3]) {
+    const Real inf = pos_inf<Real>();
+    r.mirror = 0;
+    r.zero = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r.zbits[a] = zbits[a];
+        const Real d = r.d[a];
+        if (d < Real(0)) r.mirror |= axis_bit(a);
+        if (d == Real(0)) {
+            r.zero |= axis_bit(a);
+            r.t0[a] = (zflags >> a) & 1u ? inf : -inf;
+            r.t1[a] = (zflags >> (3 + a)) & 1u ? inf : -inf;
+        } else if (d < Real(0)) {
+            r.t0[a] = A_hi[a] / d;
+            r.t1[a] = A_lo[a] / d;
+        } else {
+            r.t0[a] = A_lo[a] / d;
+            r.t1[a] = A_hi[a] / d;
+        }
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ Real midplane(const LocalRay<Real>& r, int a, const Real t0, const Real t1, int level) {
+    if (r.zero & axis_bit(a)) return ((r.zbits[a] >> level) & 1u) ? -pos_inf<Real>() : pos_inf<Real>();
+    return Real(0.5) * (t0 + t1);
+}
+
+// first_node (traversal.cpp:63-86): octant bit set iff the midplane was crossed
+// before the entry parameter.
+template <typename Real>
+__device__ __forceinline__ uint32_t first_child(const Real t0[3], const Real tm[3]) {
+    Real te = t0[0];
+    if (t0[1] > te) te = t0[1];
+    if (t0[2] > te) te = t0[2];
+    uint32_t q = 0;
+    if (tm[0] < te) q |= 4u;
+    if (tm[1] < te) q |= 2u;
+    if (tm[2] < te) q |= 1u;
+    return q;
+}
+
+// next_node (traversal.cpp:88-103): exit axis = argmin t1 (strict <, x first).
+template <typename Real> __device__ __forceinline__ uint32_t next_child(const Real t1[3], uint32_t q) {
+    uint32_t bit = 4u;
+    Real tx = t1[0];
+    if (t1[1] < tx) {
+        bit = 2u;
+        tx = t1[1];
+    }
+    if (t1[2] < tx) bit = 1u;
+    return (q & bit) ? kExit : (q | bit);
+}
+
+struct NoLog {
+    __device__ __forceinline__ void visit(double, uint32_t, bool) {}
+};
+
+// Returns true on a hit. The stack holds the ancestors of the current frame;
+// the current frame lives in registers.
+template <typename Real, class Log>
+__device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravHit<Real>& out, Log& log) {
+    Real te = r.t0[0];
+    if (r.t0[1] > te) te = r.t0[1];
+    if (r.t0[2] > te) te = r.t0[2];
+    Real tx = r.t1[0];
+    if (r.t1[1] < tx) tx = r.t1[1];
+    if (r.t1[2] < tx) tx = r.t1[2];
+    out.fetches = 0;
+    if (te >= tx || tx < Real(0)) return false;
+    out.t_enter_root = te;
+    out.t_exit_root = tx;
+
+    Real st0[kMaxDepth][3], st1[kMaxDepth][3];
+    uint2 sw[kMaxDepth];
+    uint32_t sidx[kMaxDepth], scur[kMaxDepth];
+
+    Real f0[3] = {r.t0[0], r.t0[1], r.t0[2]};
+    Real f1[3] = {r.t1[0], r.t1[1], r.t1[2]};
+    uint32_t fidx = 0;
+    uint2 fw = load_node(m, 0);
+    uint32_t fetches = 1;
+    uint32_t fcur;
+    {
+        Real tm[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) tm[a] = midplane(r, a, f0[a], f1[a], 0);
+        fcur = first_child(f0, tm);
+    }
+    int level = 0;
+    unsigned long long path = 0;
+    const int depth = static_cast<int>(m.depth);
+
+    while (true) {
+        if (fcur == kExit) {
+            if (level == 0) break;
+            --level;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                f0[a] = st0[level][a];
+                f1[a] = st1[level][a];
+            }
+            fw = sw[level];
+            fidx = sidx[level];
+            fcur = scur[level];
+            continue;
+        }
+        const uint32_t q = fcur;
+        Real c0[3], c1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const Real tm = midplane(r, a, f0[a], f1[a], level);
+            if (q & axis_bit(a)) {
+                c0[a] = tm;
+                c1[a] = f1[a];
+            } else {
+                c0[a] = f0[a];
+                c1[a] = tm;
+            }
+        }
+        fcur = next_child(c1, q);
+        int entry = 0;
+        Real t_enter = c0[0];
+        if (c0[1] > t_enter) {
+            entry = 1;
+            t_enter = c0[1];
+        }
+        if (c0[2] > t_enter) {
+            entry = 2;
+            t_enter = c0[2];
+        }
+        Real t_exit = c1[0];
+        if (c1[1] < t_exit) t_exit = c1[1];
+        if (c1[2] < t_exit) t_exit = c1[2];
+        if (!(t_enter < t_exit) || t_exit < Real(0)) continue;
+
+        const uint32_t oct = q ^ r.mirror;
+        const uint32_t bit = 1u << oct;
+        const uint32_t valid = fw.x & 0xffu;
+        const uint32_t leafm = (fw.x >> 8) & 0xffu;
+        if (!(valid & bit)) continue;
+        const bool is_leaf = (leafm & bit) != 0;
+        log.visit(static_cast<double>(t_enter), static_cast<uint32_t>(level + 1), is_leaf);
+        path = (path & ~(0xfull << (4 * level))) | (static_cast<unsigned long long>(oct) << (4 * level));
+        if (is_leaf) {
+            const uint32_t abase = (fw.x & kMixed) ? __ldg(m.side + fidx) : fw.y;
+            out.attr = abase + popc8_below(valid & leafm, bit);
+            out.t = t_enter < Real(0) ? Real(0) : t_enter;
+            out.parent = fidx;
+            out.level = static_cast<uint32_t>(level + 1);
+            out.axis = static_cast<uint32_t>(entry);
+            out.path = path;
+            out.fetches = fetches;
+            return true;
+        }
+        if (level + 1 >= depth || level + 1 >= static_cast<int>(kMaxDepth)) continue;
+        const uint32_t child = fw.y + popc8_below(valid & ~leafm, bit);
+        // push the current frame, descend
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            st0[level][a] = f0[a];
+            st1[level][a] = f1[a];
+            f0[a] = c0[a];
+            f1[a] = c1[a];
+        }
+        sw[level] = fw;
+        sidx[level] = fidx;
+        scur[level] = fcur;
+        ++level;
+        fidx = child;
+        fw = load_node(m, child);
+        ++fetches;
+        Real tm[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) tm[a] = midplane(r, a, f0[a], f1[a], level);
+        fcur = first_child(f0, tm);
+    }
+    out.fetches = fetches;
+    return false;
+}
+
+// Voxel coordinates of a hit path (leaf_path_to_voxel, traversal.cpp:260-268).
+__device__ __forceinline__ void path_to_voxel(unsigned long long path, uint32_t len, uint32_t v[3]) {
+    v[0] = v[1] = v[2] = 0;
+    for (uint32_t l = 0; l < len; ++l) {
+        const uint32_t o = static_cast<uint32_t>(path >> (4 * l)) & 0xfu;
+        v[0] = (v[0] << 1) | ((o >> 2) & 1u);
+        v[1] = (v[1] << 1) | ((o >> 1) & 1u);
+        v[2] = (v[2] << 1) | (o & 1u);
+    }
+}
+
+} // namespace vxa

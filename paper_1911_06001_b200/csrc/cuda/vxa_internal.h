@@ -1,0 +1,74 @@
+// Internal declarations shared by the C ABI (vxa_abi.cu) and the kernel
+// translation units (render_fp32.cu: production FP32 instantiation;
+// render_fp64.cu: FP64 parity instantiation, compiled with -fmad=false).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vxa_device.cuh"
+
+namespace vxa {
+
+// Zero-direction path bits of one axis (host + device, identical FP64 ops):
+// the reference tracks the node centre along an axis the ray never moves on
+// (centre_{L+1} = centre_L +/- ldexp(h, -(L+1)), traversal.cpp:135-170) and
+// takes the upper child iff !(centre > o). Only the child containing o can
+// have a non-empty interval, so the whole descent is this one bit sequence.
+__host__ __device__ inline uint32_t zero_dir_bits(double o, double h) {
+    uint32_t bits = 0;
+    double c = 0.0;
+    for (int L = 0; L < static_cast<int>(kMaxDepth); ++L) {
+        const bool upper = !(c > o);
+        if (upper) bits |= 1u << L;
+        const double q = ldexp(h, -(L + 1));
+        c = upper ? c + q : c - q;
+    }
+    return bits;
+}
+
+struct FrameLaunch {
+    int grid;
+    cudaStream_t stream;
+};
+
+cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l);
+cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l);
+int frame_blocks_per_sm_f32(bool aov, bool hbo);
+int frame_blocks_per_sm_f64(bool aov, bool hbo);
+
+struct TraverseRayIn {
+    double origin[3];
+    double direction[3];
+    double half_extent[3];
+};
+
+struct TraverseRayOut {
+    double t_hit, t_enter, t_exit;
+    double normal_local[3];
+    uint8_t attribute[4];
+    uint32_t attr_index;
+    uint32_t node_index;
+    uint8_t leaf_path[16];
+    uint8_t path_len;
+    uint8_t hit;
+    uint16_t pad;
+    uint32_t node_fetches;
+    uint32_t log_count;
+    uint32_t log_total;
+};
+
+struct VisitOut {
+    double t_enter;
+    uint8_t level;
+    uint8_t leaf;
+    uint8_t pad[6];
+};
+
+cudaError_t launch_traverse_f64(const DevModel& m, const TraverseRayIn* rays, uint32_t n, TraverseRayOut* out,
+                                VisitOut* log, uint32_t log_cap, cudaStream_t s);
+cudaError_t launch_traverse_f32(const DevModel& m, const TraverseRayIn* rays, uint32_t n, TraverseRayOut* out,
+                                VisitOut* log, uint32_t log_cap, cudaStream_t s);
+
+} // namespace vxa

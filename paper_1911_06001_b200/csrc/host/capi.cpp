@@ -1,0 +1,265 @@
+// Flat C binding of the voxanim C++ API (include/voxanim_capi.h).
+#include "voxanim_capi.h"
+
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "bench_scenes.hpp"
+#include "voxanim/gpu.hpp"
+#include "voxanim/procedural.hpp"
+#include "voxanim/renderer.hpp"
+#include "voxanim/svo.hpp"
+
+struct vxn_model {
+    std::shared_ptr<const voxanim::SvoModel> m;
+};
+struct vxn_scene {
+    voxanim::Scene s;
+};
+struct vxn_hbo {
+    voxanim::HitBuffer b;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F> auto guard(F&& f, decltype(f()) on_error) -> decltype(f()) {
+    try {
+        return f();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+    } catch (...) {
+        g_err = "unknown C++ exception";
+    }
+    return on_error;
+}
+
+vxn_model* wrap(voxanim::SvoModel&& m) {
+    return new vxn_model{std::make_shared<const voxanim::SvoModel>(std::move(m))};
+}
+
+} // namespace
+
+extern "C" {
+
+const char* vxn_last_error(void) { return g_err.c_str(); }
+
+vxn_model* vxn_model_procedural(int shell, uint32_t depth) {
+    return guard(
+        [&] {
+            return wrap(voxanim::build_procedural(
+                shell ? voxanim::ProceduralShape::ShellSphere : voxanim::ProceduralShape::SolidSphere, depth));
+        },
+        static_cast<vxn_model*>(nullptr));
+}
+
+vxn_model* vxn_model_dense_sphere(uint32_t depth) {
+    return guard(
+        [&] {
+            return wrap(voxanim::build_from_grid(voxanim::gen_primitive(voxanim::PrimitiveKind::Sphere, depth), depth));
+        },
+        static_cast<vxn_model*>(nullptr));
+}
+
+vxn_model* vxn_model_random(uint64_t seed, uint32_t depth, double fill) {
+    return guard(
+        [&] {
+            std::mt19937_64 rng(seed);
+            voxanim::VoxelGrid g(1u << depth);
+            std::uniform_real_distribution<double> coin(0.0, 1.0);
+            const std::uint32_t n = g.resolution();
+            for (std::uint32_t x = 0; x < n; ++x)
+                for (std::uint32_t y = 0; y < n; ++y)
+                    for (std::uint32_t z = 0; z < n; ++z)
+                        if (coin(rng) < fill) g.set(x, y, z);
+            return wrap(voxanim::build_from_grid(g, depth));
+        },
+        static_cast<vxn_model*>(nullptr));
+}
+
+vxn_model* vxn_model_full_cube(void) {
+    return guard(
+        [&] {
+            voxanim::VoxelGrid g(2);
+            for (std::uint32_t i = 0; i < 8; ++i) g.set(i >> 2, (i >> 1) & 1u, i & 1u);
+            return wrap(voxanim::build_from_grid(g, 1));
+        },
+        static_cast<vxn_model*>(nullptr));
+}
+
+vxn_model* vxn_model_deserialize(const uint8_t* bytes, size_t n) {
+    return guard([&] { return wrap(voxanim::deserialize(std::span<const std::uint8_t>(bytes, n))); },
+                 static_cast<vxn_model*>(nullptr));
+}
+
+int64_t vxn_model_serialize(const vxn_model* m, uint8_t* out, size_t cap) {
+    return guard(
+        [&]() -> int64_t {
+            const auto bytes = voxanim::serialize(*m->m);
+            if (out != nullptr) {
+                if (cap < bytes.size()) throw voxanim::ValidationError("serialize: buffer too small");
+                std::memcpy(out, bytes.data(), bytes.size());
+            }
+            return static_cast<int64_t>(bytes.size());
+        },
+        int64_t{-1});
+}
+
+int vxn_model_info(const vxn_model* m, uint32_t* depth, uint64_t* nodes, uint64_t* attrs) {
+    if (m == nullptr) return -1;
+    if (depth) *depth = m->m->depth;
+    if (nodes) *nodes = m->m->nodes.size();
+    if (attrs) *attrs = m->m->attributes.size();
+    return 0;
+}
+
+int vxn_model_validate(const vxn_model* m) { return static_cast<int>(voxanim::validate(*m->m).violations.size()); }
+
+void vxn_model_free(vxn_model* m) { delete m; }
+
+vxn_scene* vxn_scene_config(int config, vxn_model* const* models, uint32_t n_models, uint64_t seed, int width,
+                            int height) {
+    return guard(
+        [&] {
+            std::vector<std::shared_ptr<const voxanim::SvoModel>> ms;
+            for (uint32_t i = 0; i < n_models; ++i) ms.push_back(models[i]->m);
+            return new vxn_scene{voxanim::bench::make_config_scene(config, ms, seed, width, height)};
+        },
+        static_cast<vxn_scene*>(nullptr));
+}
+
+int vxn_scene_evaluate(vxn_scene* s, double time) {
+    return guard(
+        [&] {
+            voxanim::evaluate_animation(s->s, time);
+            return 0;
+        },
+        -1);
+}
+
+int vxn_scene_mark_clean(vxn_scene* s) {
+    voxanim::mark_clean(s->s);
+    return 0;
+}
+
+int vxn_scene_set_camera_dirty(vxn_scene* s, int dirty) {
+    s->s.camera.dirty = dirty != 0;
+    return 0;
+}
+
+int vxn_scene_object_count(const vxn_scene* s) { return static_cast<int>(s->s.objects.size()); }
+
+int vxn_scene_get_object(const vxn_scene* s, int index, int32_t* id, double* tf, int* dirty) {
+    if (index < 0 || index >= static_cast<int>(s->s.objects.size())) return -1;
+    const voxanim::SceneObject& o = s->s.objects[static_cast<std::size_t>(index)];
+    if (id) *id = o.id;
+    if (tf) std::memcpy(tf, &o.transform, sizeof(o.transform));
+    if (dirty) *dirty = o.dirty ? 1 : 0;
+    return 0;
+}
+
+int vxn_scene_set_object(vxn_scene* s, int index, const double* tf, int dirty) {
+    if (index < 0 || index >= static_cast<int>(s->s.objects.size())) return -1;
+    voxanim::SceneObject& o = s->s.objects[static_cast<std::size_t>(index)];
+    if (tf) std::memcpy(static_cast<void*>(&o.transform), tf, sizeof(o.transform));
+    o.dirty = dirty != 0;
+    return 0;
+}
+
+int vxn_scene_export(vxn_scene* s, vxa_frame_desc* f, vxa_instance* inst, uint32_t cap, uint32_t* count) {
+    return guard(
+        [&] {
+            const voxanim::Scene& sc = s->s;
+            if (count) *count = static_cast<uint32_t>(sc.objects.size());
+            if (f) {
+                *f = vxa_frame_desc{};
+                for (int k = 0; k < 3; ++k) f->camera.position[k] = sc.camera.position[k];
+                std::memcpy(f->camera.orientation, sc.camera.orientation.m.data(), 9 * sizeof(double));
+                f->camera.vertical_fov_deg = sc.camera.vertical_fov_deg;
+                f->camera.width = sc.camera.width;
+                f->camera.height = sc.camera.height;
+                std::memcpy(f->background, sc.background.data(), 3);
+                f->culling = 1;
+                f->sorting = 1;
+                f->camera_dirty = sc.camera.dirty ? 1 : 0;
+                f->tile_rank = 0;
+                f->tile_world = 1;
+            }
+            if (inst) {
+                if (cap < sc.objects.size()) throw voxanim::ValidationError("export: instance buffer too small");
+                for (std::size_t i = 0; i < sc.objects.size(); ++i) {
+                    const voxanim::SceneObject& o = sc.objects[i];
+                    vxa_instance& v = inst[i];
+                    v = vxa_instance{};
+                    v.id = o.id;
+                    v.model = o.model ? voxanim::gpu::model_handle(*o.model) : 0u;
+                    std::memcpy(v.rotation, o.transform.rotation.m.data(), 9 * sizeof(double));
+                    for (int k = 0; k < 3; ++k) {
+                        v.translation[k] = o.transform.translation[k];
+                        v.scale[k] = o.transform.scale[k];
+                    }
+                    v.dirty = o.dirty ? 1 : 0;
+                }
+            }
+            return 0;
+        },
+        -1);
+}
+
+void vxn_scene_free(vxn_scene* s) { delete s; }
+
+vxn_hbo* vxn_hbo_create(int width, int height) {
+    return guard([&] { return new vxn_hbo{voxanim::HitBuffer(width, height)}; }, static_cast<vxn_hbo*>(nullptr));
+}
+
+void vxn_hbo_free(vxn_hbo* h) { delete h; }
+
+int vxn_render(vxn_scene* s, int culling, int sorting, int precision, vxn_hbo* hbo, uint8_t* rgb, vxa_pixel_aov* aov,
+               uint64_t* fs4, double* render_ms, vxa_stats* ds) {
+    return guard(
+        [&] {
+            voxanim::RenderOptions opts;
+            opts.culling = culling != 0;
+            opts.sorting = sorting != 0;
+            opts.hbo = hbo ? &hbo->b : nullptr;
+            voxanim::gpu::RenderOptionsEx ex;
+            ex.precision = precision < 0 ? voxanim::gpu::default_precision()
+                                         : static_cast<voxanim::gpu::Precision>(precision);
+            ex.read_image = rgb != nullptr;
+            std::vector<vxa_pixel_aov> aovs;
+            if (aov) ex.aov = &aovs;
+            voxanim::FrameStats st;
+            voxanim::gpu::render_frame_into(s->s, opts, ex, st, rgb, ds);
+            if (aov) std::memcpy(aov, aovs.data(), aovs.size() * sizeof(vxa_pixel_aov));
+            if (fs4) {
+                fs4[0] = st.rays;
+                fs4[1] = st.sphere_tests;
+                fs4[2] = st.svo_traversals;
+                fs4[3] = st.pixels_reused;
+            }
+            if (render_ms) *render_ms = st.render_ms;
+            return 0;
+        },
+        -1);
+}
+
+int vxn_traverse(const vxn_model* m, const vxa_local_ray* rays, uint32_t n, vxa_traverse_hit* hits) {
+    return guard(
+        [&] {
+            const std::uint32_t h = voxanim::gpu::model_handle(*m->m);
+            voxanim::gpu::check(vxa_traverse(voxanim::gpu::context(), h, rays, n, VXA_FP64, hits, nullptr, 0),
+                                "vxa_traverse");
+            return 0;
+        },
+        -1);
+}
+
+vxa_ctx* vxn_context(void) {
+    return guard([&] { return voxanim::gpu::context(); }, static_cast<vxa_ctx*>(nullptr));
+}
+
+} // extern "C"

@@ -1,0 +1,180 @@
+// Renderer API. render_frame / render_frame_ex hand the whole frame to the
+// GPU (vxa_render); the single-ray helpers keep the reference's FP64
+// semantics for callers that use them directly:
+//   generate_primary_ray  renderer.cpp:11-23
+//   ray_sphere_test       renderer.cpp:25-43
+//   cull_and_sort         renderer.cpp:45-61 (order (t_center, id))
+//   trace_ray             renderer.cpp:63-100 (skip-not-break, nearest (t, id));
+//                         each candidate is traversed on the GPU (traverse()).
+//   shade                 renderer.cpp:102-113
+#include "voxanim/renderer.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <numbers>
+#include <unordered_map>
+
+#include "voxanim/gpu.hpp"
+
+namespace voxanim {
+
+Ray generate_primary_ray(const Camera& cam, int px, int py) {
+    if (px < 0 || py < 0 || px >= cam.width || py >= cam.height)
+        throw ValidationError("pixel (" + std::to_string(px) + ", " + std::to_string(py) + ") outside the " +
+                              std::to_string(cam.width) + "x" + std::to_string(cam.height) + " image");
+    const double tan_half = std::tan(cam.vertical_fov_deg * std::numbers::pi / 360.0);
+    const double aspect = static_cast<double>(cam.width) / cam.height;
+    const double ndc_x = (px + 0.5) / cam.width * 2.0 - 1.0;
+    const double ndc_y = 1.0 - (py + 0.5) / cam.height * 2.0;
+    const Vec3 through{ndc_x * tan_half * aspect, ndc_y * tan_half, -1.0};
+    return {cam.position, (cam.orientation * through).normalized()};
+}
+
+std::optional<SphereHit> ray_sphere_test(const Ray& ray, const BoundingSphere& sphere) {
+    const Vec3 l = sphere.center - ray.origin;
+    const double tc = l.dot(ray.direction);
+    const double d2 = l.norm2() - tc * tc;
+    const double r2 = sphere.radius * sphere.radius;
+    if (d2 >= r2 || tc + sphere.radius < 0.0) return std::nullopt; // off the line, or entirely behind
+    SphereHit h;
+    h.d = std::sqrt(std::max(d2, 0.0));
+    h.t_center = tc;
+    h.t_boundary = std::max(tc - std::sqrt(r2 - d2), 0.0);
+    return h;
+}
+
+namespace {
+
+bool front_to_back(const SphereHit& a, const SphereHit& b) {
+    return a.t_center != b.t_center ? a.t_center < b.t_center : a.object_id < b.object_id;
+}
+
+} // namespace
+
+std::vector<SphereHit> cull_and_sort(const Scene& scene, const Ray& ray) {
+    std::vector<SphereHit> out;
+    out.reserve(scene.objects.size());
+    for (const SceneObject& o : scene.objects) {
+        if (auto h = ray_sphere_test(ray, bounding_sphere(o))) {
+            h->object_id = o.id;
+            out.push_back(*h);
+        }
+    }
+    std::sort(out.begin(), out.end(), front_to_back);
+    return out;
+}
+
+HitRecord trace_ray(const Scene& scene, const Ray& ray, std::span<const SphereHit> candidates, FrameStats* stats) {
+    HitRecord best;
+    bool have = false;
+    for (const SphereHit& c : candidates) {
+        if (have && best.t < c.t_boundary) continue; // nothing inside this sphere can be nearer
+        const SceneObject* obj = scene.find_object(c.object_id);
+        if (obj == nullptr || !obj->model) continue;
+        const Ray local = transform_ray_world_to_local(ray, obj->transform);
+        if (stats) ++stats->svo_traversals;
+        const auto hit = traverse(*obj->model, local, bounds_from_scale(obj->transform.scale));
+        if (!hit) continue;
+        if (!have || hit->t_hit < best.t || (hit->t_hit == best.t && obj->id < best.object_id)) {
+            have = true;
+            best.color = hit->attribute;
+            best.normal = obj->transform.rotation * hit->normal_local;
+            best.t = hit->t_hit;
+            best.object_id = obj->id;
+        }
+    }
+    if (have) best.kind = candidates.size() > 1 ? HitKind::MultiSphere : HitKind::SingleSphere;
+    return best;
+}
+
+std::array<std::uint8_t, 3> shade(const HitRecord& rec, const Ray& ray, const std::array<std::uint8_t, 3>& background) {
+    if (rec.kind == HitKind::Miss) return background;
+    const double f = 0.2 + 0.8 * std::max(0.0, rec.normal.dot(-ray.direction));
+    const auto q = [f](std::uint8_t c) { return static_cast<std::uint8_t>(std::lround(c * f)); };
+    return {q(rec.color.r), q(rec.color.g), q(rec.color.b)};
+}
+
+namespace gpu {
+
+void render_frame_into(const Scene& scene, const RenderOptions& opts, const RenderOptionsEx& ex, FrameStats& stats,
+                       std::uint8_t* rgb_out, vxa_stats* device_stats) {
+    const Camera& cam = scene.camera;
+    if (opts.hbo && (opts.hbo->width() != cam.width || opts.hbo->height() != cam.height))
+        throw ValidationError("hit buffer dimensions do not match the camera");
+    const auto t0 = std::chrono::steady_clock::now();
+
+    std::vector<vxa_instance> inst(scene.objects.size());
+    std::unordered_map<const SvoModel*, std::uint32_t> handles;
+    for (std::size_t i = 0; i < scene.objects.size(); ++i) {
+        const SceneObject& o = scene.objects[i];
+        vxa_instance& v = inst[i];
+        v = vxa_instance{};
+        v.id = o.id;
+        if (o.model) {
+            auto [it, fresh] = handles.try_emplace(o.model.get(), 0u);
+            if (fresh) it->second = model_handle(*o.model);
+            v.model = it->second;
+        }
+        std::copy(o.transform.rotation.m.begin(), o.transform.rotation.m.end(), v.rotation);
+        for (int k = 0; k < 3; ++k) {
+            v.translation[k] = o.transform.translation[k];
+            v.scale[k] = o.transform.scale[k];
+        }
+        v.dirty = o.dirty ? 1 : 0;
+    }
+
+    vxa_frame_desc f{};
+    for (int k = 0; k < 3; ++k) f.camera.position[k] = cam.position[k];
+    std::copy(cam.orientation.m.begin(), cam.orientation.m.end(), f.camera.orientation);
+    f.camera.vertical_fov_deg = cam.vertical_fov_deg;
+    f.camera.width = cam.width;
+    f.camera.height = cam.height;
+    f.background[0] = scene.background[0];
+    f.background[1] = scene.background[1];
+    f.background[2] = scene.background[2];
+    f.culling = opts.culling ? 1 : 0;
+    f.sorting = opts.sorting ? 1 : 0;
+    f.precision = static_cast<std::uint8_t>(ex.precision);
+    f.camera_dirty = cam.dirty ? 1 : 0;
+    f.tile_rank = ex.tile_rank;
+    f.tile_world = ex.tile_world;
+    f.hbo = opts.hbo ? reinterpret_cast<vxa_hit_record*>(opts.hbo->data()) : nullptr;
+
+    if (ex.aov) ex.aov->resize(static_cast<std::size_t>(cam.width) * static_cast<std::size_t>(cam.height));
+    vxa_stats ds{};
+    check(vxa_render(context(), &f, inst.data(), static_cast<std::uint32_t>(inst.size()),
+                     rgb_out, ex.aov ? ex.aov->data() : nullptr, &ds),
+          "vxa_render");
+    stats = FrameStats{};
+    stats.rays = ds.rays;
+    stats.sphere_tests = ds.sphere_tests;
+    stats.svo_traversals = ds.svo_traversals;
+    stats.pixels_reused = ds.pixels_reused;
+    stats.render_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (device_stats) *device_stats = ds;
+}
+
+Image render_frame_ex(const Scene& scene, const RenderOptions& opts, const RenderOptionsEx& ex, FrameStats& stats,
+                      vxa_stats* device_stats) {
+    Image image;
+    if (ex.read_image) image = Image(scene.camera.width, scene.camera.height);
+    render_frame_into(scene, opts, ex, stats, ex.read_image ? image.rgb.data() : nullptr, device_stats);
+    return image;
+}
+
+} // namespace gpu
+
+Image render_frame(const Scene& scene, const RenderOptions& opts, FrameStats& stats) {
+    gpu::RenderOptionsEx ex;
+    ex.precision = gpu::default_precision();
+    return gpu::render_frame_ex(scene, opts, ex, stats);
+}
+
+std::string write_ppm(const Image& image) {
+    std::string out = "P6\n" + std::to_string(image.width) + " " + std::to_string(image.height) + "\n255\n";
+    out.append(reinterpret_cast<const char*>(image.rgb.data()), image.rgb.size());
+    return out;
+}
+
+} // namespace voxanim
