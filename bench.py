@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""voxanim-b200 benchmark: animated-SVO ray casting, SURVEY.md §8(d) configuration C4.
+
+A step is one animated frame of 64 rigid-body-animated instances of one
+depth-11 shell-sphere SVO at 3840x2160 (8,294,400 primary rays): the host
+update (evaluate_animation + instance table) and the GPU frame (ray
+generation, bounding-sphere cull + front-to-back order, Revelles traversal,
+nearest hit, shading, RGBA8 store). N GPUs split the frame into 64x64
+super-tiles (round-robin) and store their tiles straight into rank 0's
+framebuffer over NVLink (CUDA IPC peer mapping): strong scaling.
+
+Prints ONE JSON line on rank 0. --impl reference runs the reference CPU
+renderer (oracle/_ref, compiled from /root/reference) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (config id, shell?, depth, width, height, animated)
+    "c4": (4, True, 11, 3840, 2160, True),
+    "c2": (2, True, 10, 1920, 1080, True),
+    "c3": (3, True, 10, 1920, 1080, False),
+    "c1": (1, False, 8, 512, 512, False),
+}
+WORKLOAD_TEXT = {
+    "c4": "C4: 64 animated instances of a depth-11 shell-sphere SVO, 3840x2160, culling+sorting, nearest hit",
+    "c2": "C2: one depth-10 shell-sphere SVO animated (rotation+translation+anisotropic scale), 1920x1080",
+    "c3": "C3: C2's model and camera, static identity transform",
+    "c1": "C1: static depth-8 solid sphere, identity transform, 512x512",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between timed steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled in the background during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _poll(self):
+        cmd = ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+               "--format=csv,noheader,nounits"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(self.NAMES, s[2:]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- helpers
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per frame-kernel launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_frame_kernel.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(workload)
+    return e.get("dram_bytes_per_launch") if e else None
+
+
+def exchange_handle(dist, rank, handle: bytes) -> bytes:
+    """Broadcast rank 0's 64-byte CUDA IPC framebuffer handle to every rank."""
+    obj = [handle if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def build_scene(vx, workload):
+    cfg, shell, depth, W, H, animated = WORKLOADS[workload]
+    model = vx.Model.procedural(depth, shell=shell)
+    scene = vx.Scene(cfg, [model])
+    return model, scene, W, H, animated
+
+
+def frame_time(k, animated):
+    return ((k / 30.0) % 4.0) if animated else 0.0
+
+
+def cpu_baseline(model, workload, seconds, max_frames=5):
+    """Reference render_frame (oracle/_ref, all host threads) on a bounded sample of the workload."""
+    from oracle import ref
+
+    cfg, shell, depth, W, H, animated = WORKLOADS[workload]
+    rmodel = ref.RefModel.from_bytes(model.serialize())
+    rscene = ref.RefScene(cfg, [rmodel], 0, W, H)
+    threads = ref.hardware_threads()
+    total_ms, frames = 0.0, 0
+    t0 = time.perf_counter()
+    while frames < max_frames and (frames == 0 or time.perf_counter() - t0 < seconds):
+        rscene.evaluate(frame_time(frames, animated))
+        _, st = rscene.render(True, True, threads)
+        total_ms += st["render_ms"]
+        frames += 1
+    value = W * H * frames / (total_ms / 1e3) / 1e6
+    return {"value": round(value, 4), "unit": "Mrays/s", "cores": threads, "kind": "reference",
+            "sample": f"{frames} full {W}x{H} frames of {workload.upper()} (t=k/30), reference render_frame "
+                      f"(culling+sorting, no HBO), FrameStats::render_ms",
+            "ms_per_frame": round(total_ms / frames, 3)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_1911_06001_b200 as vx  # host code only: the procedural depth-11 model
+    from oracle import ref
+
+    cfg, shell, depth, W, H, animated = WORKLOADS[args.workload]
+    model = vx.Model.procedural(depth, shell=shell)
+    rmodel = ref.RefModel.from_bytes(model.serialize())
+    rscene = ref.RefScene(cfg, [rmodel], 0, W, H)
+    threads = ref.hardware_threads()
+    # First warm-up step: one full reference frame; it sizes the sample so the
+    # whole run stays within a few minutes.
+    rscene.evaluate(frame_time(0, animated))
+    _, st = rscene.render(True, True, threads)
+    full_ms = st["render_ms"]
+    per_step_ms = 150e3 / max(1, args.steps + args.warmup)
+    band = H if full_ms <= per_step_ms else max(8, min(H, int(H * per_step_ms / full_ms) // 8 * 8))
+
+    def step(k):
+        rscene.evaluate(frame_time(k, animated))
+        if band == H:
+            return rscene.render(True, True, threads)[1]["render_ms"]
+        a = (k * band) % (H - band + 1)
+        return rscene.render_rows(a, a + band, threads, rgb=False)[1]
+
+    for k in range(1, args.warmup):
+        step(k)
+    total_ms = sum(step(args.warmup + k) for k in range(args.steps))
+    ms = total_ms / args.steps
+    value = W * band / ms / 1e3
+    frame_ms = ms * H / band
+    sample = (f"{args.steps} full {W}x{H} frames" if band == H else
+              f"{args.steps} bands of {band} rows x {W} px (rotating, t=k/30) of the {W}x{H} frame")
+    line = {
+        "impl": "reference", "metric": "Mrays/s", "value": round(value, 4), "unit": "Mrays/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "fps": round(1000.0 / frame_ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
+                   "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mrays/s", "cores": threads, "kind": "reference",
+                         "sample": sample + f", reference render_frame/trace_ray on {threads} host threads"},
+        "e2e": {"value": round(value, 4), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    os.environ["VOXANIM_DEVICE"] = str(local)
+    import paper_1911_06001_b200 as vx
+    from paper_1911_06001_b200 import _abi
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    lib = vx.vxa()
+    model, scene, W, H, animated = build_scene(vx, args.workload)
+    ctx = vx.context()
+    f, inst, n = scene.export()
+    prec = _abi.VXA_FP64 if args.precision == "fp64" else _abi.VXA_FP32
+
+    def check(rc, what):
+        if rc != 0:
+            raise RuntimeError(f"{what}: {lib.vxa_last_error().decode()}")
+
+    # multi-GPU: map rank 0's framebuffer into every rank (NVLink peer stores)
+    if world > 1:
+        handle = (C.c_char * 64)()
+        if rank == 0:
+            check(lib.vxa_fb_export(ctx, W, H, handle), "fb_export")
+        got = exchange_handle(dist, rank, bytes(handle))
+        if rank != 0:
+            h2 = (C.c_char * 64).from_buffer_copy(got)
+            check(lib.vxa_fb_import(ctx, W, H, h2), "fb_import")
+
+    vxl = vx.voxanim()
+
+    def submit(k):
+        # host update (evaluate_animation) + instance table + frame submission, in C++
+        if vxl.vxn_scene_submit(scene._h, frame_time(k, animated), prec, rank, world) != 0:
+            raise RuntimeError(vxl.vxn_last_error().decode())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for k in range(args.warmup):
+        submit(k)
+    check(lib.vxa_synchronize(ctx), "sync")
+    barrier()
+
+    step_ms = []
+    lib.vxa_stats_reset(ctx)
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            if not args.no_flush:
+                check(lib.vxa_flush_l2(ctx), "flush")
+            check(lib.vxa_timer_begin(ctx), "timer")
+            submit(args.warmup + k)
+            if world > 1:
+                check(lib.vxa_synchronize(ctx), "sync")
+                barrier()  # the frame is complete in rank 0's framebuffer only when every rank is done
+            ms = C.c_double()
+            check(lib.vxa_timer_end(ctx, C.byref(ms)), "timer")
+            step_ms.append(ms.value)
+    st = _abi.vxa_stats()
+    check(lib.vxa_stats_read(ctx, C.byref(st)), "stats")
+    total_ms = sum(step_ms)
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    ms_per_step = total_ms / args.steps
+    rays = W * H
+    value = rays * args.steps / (total_ms / 1e3) / 1e6
+
+    # roofline of the frame kernel: algorithmic bytes / kernel time
+    kernel_ms = st.gpu_ms / max(1, st.kernel_launches)
+    frames = max(1, st.kernel_launches)
+    pixels_mine = st.rays / frames
+    alg_bytes = (8.0 * st.node_fetches + 4.0 * st.leaf_hits) / frames + 4.0 * pixels_mine
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = ncu_traffic(args.workload)
+
+    # end to end through the public API (voxanim::render_frame with host buffers)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        import numpy as np
+
+        host_img = np.empty((H, W, 3), np.uint8)
+        for k in range(3):
+            scene.evaluate(frame_time(k, animated))
+            scene.render(precision=prec, rgb=host_img)
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for k in range(args.e2e_steps):
+            scene.evaluate(frame_time(k, animated))
+            scene.render(precision=prec, rgb=host_img)
+        el = time.perf_counter() - t0
+        # bytes of the last call (identical every step)
+        st2 = _abi.vxa_stats()
+        lib.vxa_stats_read(ctx, C.byref(st2))
+        e2e = {"value": round(rays * args.e2e_steps / el / 1e6, 3), "unit": "Mrays/s",
+               "h2d_bytes_per_step": int(st2.h2d_bytes), "d2h_bytes_per_step": int(st2.d2h_bytes),
+               "ms_per_step": round(el * 1e3 / args.e2e_steps, 3),
+               "path": "voxanim::render_frame -> vxa_render (RGB8 image to pageable host memory)"}
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            base = cpu_baseline(model, args.workload, args.cpu_seconds)
+        except Exception as e:  # the baseline is reported, not required
+            base = {"value": None, "unit": "Mrays/s", "cores": None, "kind": "reference",
+                    "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        cfg, shell, depth, _, _, _ = WORKLOADS[args.workload]
+        line = {
+            "metric": "Mrays/s", "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "fps": round(1000.0 / ms_per_step, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
+                       "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False,
+                       "partition": f"64x64 super-tiles round-robin over {world} GPU(s), NVLink peer stores",
+                       "l2": "flushed between timed steps (256 MB write)" if not args.no_flush else "warm",
+                       "model_bytes_device": None},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 5), "traffic": traffic,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": round(alg_bytes),
+                         "kernel_ms": round(kernel_ms, 4),
+                         "per_ray": {"node_fetches": round(st.node_fetches / frames / pixels_mine, 4),
+                                     "leaf_hits": round(st.leaf_hits / frames / pixels_mine, 4),
+                                     "traversals": round(st.svo_traversals / frames / pixels_mine, 4),
+                                     "bytes": round(alg_bytes / pixels_mine, 3)}},
+            "cpu_baseline": base,
+            "e2e": e2e,
+            "gpu_launches": int(st.kernel_launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

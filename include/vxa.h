@@ -133,6 +133,8 @@ typedef struct vxa_stats {
     uint64_t leaf_hits;      /* attribute fetches (4 B each) */
     uint64_t kernel_launches;/* kernels this call launched */
     double gpu_ms;           /* CUDA-event time of the frame kernels on the context stream */
+    uint64_t h2d_bytes;      /* host->device bytes the call(s) copied (instance table, hit buffer) */
+    uint64_t d2h_bytes;      /* device->host bytes (image, AOVs, hit buffer, counters) */
 } vxa_stats;
 
 /* Per-pixel parity outputs (host array of width*height, row-major). */
@@ -144,8 +146,11 @@ typedef struct vxa_pixel_aov {
     uint32_t voxel[3];    /* leaf_path_to_voxel of the hit path */
     uint8_t level;        /* path_len */
     uint8_t kind;         /* HitKind */
-    uint16_t traversals;  /* SVO traversals started for this pixel */
+    uint8_t entry_axis;   /* axis of the entry face (normal_local axis), 0..2 */
+    uint8_t pad0;
+    uint32_t traversals;  /* SVO traversals started for this pixel */
     uint32_t node_fetches;/* internal-node words loaded for this pixel */
+    uint32_t pad1;
 } vxa_pixel_aov;
 
 /* Renders one frame synchronously. instances are in scene order. rgb_out:
@@ -181,6 +186,11 @@ void* vxa_stream(vxa_ctx* ctx);
  * peer mapping (NVLink / NVSwitch). */
 int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_out);
 int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle);
+
+/* Screen partition used when tile_world > 1: the rank that renders pixel
+ * (x, y) of a width-wide frame split over `world` devices (64x64 super-tiles,
+ * round-robin). Pure function, no device needed. */
+int32_t vxa_tile_owner(int32_t x, int32_t y, int32_t width, int32_t height, int32_t world);
 
 /* ---- single-ray traversal (voxanim::traverse / traverse_debug) ---------- */
 

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(HERE, "_ref", "libvoxanim_ref.so")
 
 AOV_DTYPE = np.dtype(
     [("t", "<f8"), ("object_id", "<i4"), ("node_index", "<u4"), ("attr_index", "<u4"), ("voxel", "<u4", (3,)),
-     ("level", "u1"), ("kind", "u1"), ("traversals", "<u2"), ("node_fetches", "<u4")]
+     ("level", "u1"), ("kind", "u1"), ("entry_axis", "u1"), ("pad0", "u1"), ("traversals", "<u4"),
+     ("node_fetches", "<u4"), ("pad1", "<u4")]
 )
 RAY_DTYPE = np.dtype([("origin", "<f8", (3,)), ("direction", "<f8", (3,)), ("half_extent", "<f8", (3,))])
 TRAV_DTYPE = np.dtype(
@@ -30,7 +31,7 @@ TRAV_DTYPE = np.dtype(
 
 # default resolutions of the bench_scenes.hpp configurations
 CONFIG_SIZES = {1: (512, 512), 2: (1920, 1080), 3: (1920, 1080), 4: (3840, 2160), 5: (160, 120), 6: (64, 48),
-                7: (96, 64)}
+                7: (96, 64), 8: (96, 64)}
 
 # classify() codes
 MATCH, TIE, BUG, T_OUT_OF_TOL = 0, 1, 2, 3
@@ -69,6 +70,8 @@ def lib() -> C.CDLL:
             "vref_hbo_free": (None, P),
             "vref_render": (i, P, i, i, i, P, P, C.POINTER(u64), C.POINTER(d)),
             "vref_dump": (i, P, i, i, i, i, i, P, P),
+            "vref_render_rows": (i, P, i, i, i, P, C.POINTER(d)),
+            "vref_explain": (i, P, i, i, P, P, C.c_char_p, C.c_size_t),
             "vref_classify": (i, P, i, i, P, P, d, P),
             "vref_traverse": (i, P, P, u32, P, i),
             "vref_dda_random": (i, u64, u32, d, P, u32, P, P, P),
@@ -176,6 +179,14 @@ class RefScene:
         return img, {"rays": fs[0], "sphere_tests": fs[1], "svo_traversals": fs[2], "pixels_reused": fs[3],
                      "render_ms": ms.value}
 
+    def render_rows(self, a, b, threads=0, rgb=True):
+        """Reference per-pixel pipeline (culling+sorting) over rows [a, b): (rgb, wall ms)."""
+        img = np.zeros((b - a, self.width, 3), np.uint8) if rgb else None
+        ms = C.c_double()
+        _ok(lib().vref_render_rows(self._h, threads, a, b, img.ctypes.data if rgb else None, C.byref(ms)),
+            "render_rows")
+        return img, ms.value
+
     def dump(self, culling=True, sorting=True, threads=0, rows=None):
         """Per-pixel oracle AOVs (+ RGB) for rows [a, b)."""
         W, H = self.width, self.height
@@ -193,6 +204,13 @@ class RefScene:
         cls = np.zeros((b - a, self.width), np.uint8)
         _ok(lib().vref_classify(self._h, a, b, o.ctypes.data, g.ctypes.data, t_rel, cls.ctypes.data), "classify")
         return cls
+
+    def explain(self, px, py, oracle_rec, gpu_rec):
+        o = np.ascontiguousarray(np.array([oracle_rec], AOV_DTYPE))
+        g = np.ascontiguousarray(np.array([gpu_rec], AOV_DTYPE))
+        buf = C.create_string_buffer(8192)
+        _ok(lib().vref_explain(self._h, px, py, o.ctypes.data, g.ctypes.data, buf, 8192), "explain")
+        return buf.value.decode()
 
     def primary_ray(self, px, py):
         o6 = (C.c_double * 6)()

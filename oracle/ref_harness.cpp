@@ -21,6 +21,8 @@
 //     independent DDA oracle (oracles.hpp:68-149);
 //   * the FP32 tie classifier (SURVEY.md §8(a) "Tie classification").
 #include <algorithm>
+#include <cstdio>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -61,10 +63,13 @@ struct AovRec {
     uint32_t voxel[3];
     uint8_t level;
     uint8_t kind;
-    uint16_t traversals;
+    uint8_t entry_axis;
+    uint8_t pad0;
+    uint32_t traversals;
     uint32_t node_fetches;
+    uint32_t pad1;
 };
-static_assert(sizeof(AovRec) == 40);
+static_assert(sizeof(AovRec) == 48);
 
 struct LocalRayRec {
     double origin[3], direction[3], half_extent[3];
@@ -214,7 +219,7 @@ PixelOracle oracle_pixel(const Scene& scene, const std::vector<BoundingSphere>& 
     a.object_id = have ? best.object_id : -1;
     a.t = have ? best.t : 0.0;
     a.kind = static_cast<uint8_t>(best.kind);
-    a.traversals = static_cast<uint16_t>(trav);
+    a.traversals = trav;
     a.node_fetches = fetch;
     if (have) {
         replay_path(*best_obj->model, best_hit, a.node_index, a.attr_index);
@@ -223,6 +228,7 @@ PixelOracle oracle_pixel(const Scene& scene, const std::vector<BoundingSphere>& 
         a.voxel[1] = v[1];
         a.voxel[2] = v[2];
         a.level = best_hit.path_len;
+        a.entry_axis = best_hit.normal_local.x != 0.0 ? 0 : (best_hit.normal_local.y != 0.0 ? 1 : 2);
     }
     return out;
 }
@@ -235,6 +241,7 @@ double tau(double t) { return 8.0 * std::ldexp(1.0, -23) * std::max(1.0, std::ab
 
 struct Interval {
     double in = kInf, out = -kInf;
+    double axis_in[3] = {-kInf, -kInf, -kInf}; // entry parameter of each axis' slab
 };
 
 // FP64 slab test of the voxel box (level `level` of the instance's octree)
@@ -254,6 +261,7 @@ Interval voxel_interval(const SceneObject& obj, const Ray& world, const uint32_t
         }
         double t0 = (lo - o) / d, t1 = (hi - o) / d;
         if (t0 > t1) std::swap(t0, t1);
+        iv.axis_in[a] = t0;
         iv.in = std::max(iv.in, t0);
         iv.out = std::min(iv.out, t1);
     }
@@ -304,7 +312,12 @@ int classify_pixel(const Scene& scene, const Ray& ray, const AovRec& o, const Ao
     if (ho && hg && o.object_id == g.object_id && o.voxel[0] == g.voxel[0] && o.voxel[1] == g.voxel[1] &&
         o.voxel[2] == g.voxel[2] && o.level == g.level && o.node_index == g.node_index && o.attr_index == g.attr_index) {
         const double tol = t_rel * std::max(1.0, std::abs(o.t));
-        return std::abs(o.t - g.t) <= tol ? 0 : 3;
+        if (std::abs(o.t - g.t) > tol) return 3;
+        if (o.entry_axis == g.entry_axis) return 0;
+        // same voxel entered through a different face: an edge/corner entry tie
+        const SceneObject* obj = scene.find_object(o.object_id);
+        const Interval iv = voxel_interval(*obj, ray, o.voxel, o.level);
+        return std::abs(iv.axis_in[o.entry_axis] - iv.axis_in[g.entry_axis]) <= tau(o.t) ? 1 : 2;
     }
     const double tref = ho ? o.t : g.t;
     const double tt = tau(tref);
@@ -481,6 +494,46 @@ VREF_API int vref_render(vref_scene* s, int culling, int sorting, int threads, v
         -1);
 }
 
+// The reference's per-pixel work of render_frame (no hit buffer) restricted to
+// rows [row_begin, row_end): generate_primary_ray, the sphere pass over
+// per-frame bounding spheres, (t_center, id) order, the reference trace_ray
+// and shade -- a bounded sample of a frame for the CPU baseline. Returns the
+// wall time in ms through *ms.
+VREF_API int vref_render_rows(const vref_scene* s, int threads, int row_begin, int row_end, uint8_t* rgb, double* ms) {
+    return guard(
+        [&] {
+            const auto t0 = std::chrono::steady_clock::now();
+            const Scene& scene = s->s;
+            const int W = scene.camera.width;
+            std::vector<BoundingSphere> spheres;
+            for (const SceneObject& o : scene.objects) spheres.push_back(bounding_sphere(o));
+            parallel_rows(row_end - row_begin, hw_threads(threads), [&](int a, int b) {
+                std::vector<SphereHit> cand;
+                for (int r = a; r < b; ++r) {
+                    const int py = row_begin + r;
+                    for (int px = 0; px < W; ++px) {
+                        const Ray ray = generate_primary_ray(scene.camera, px, py);
+                        cand.clear();
+                        for (std::size_t i = 0; i < scene.objects.size(); ++i)
+                            if (auto h = ray_sphere_test(ray, spheres[i])) {
+                                h->object_id = scene.objects[i].id;
+                                cand.push_back(*h);
+                            }
+                        std::sort(cand.begin(), cand.end(), [](const SphereHit& x, const SphereHit& y) {
+                            return x.t_center != y.t_center ? x.t_center < y.t_center : x.object_id < y.object_id;
+                        });
+                        const HitRecord rec = trace_ray(scene, ray, cand, nullptr);
+                        const auto c = shade(rec, ray, scene.background);
+                        if (rgb) std::memcpy(rgb + 3 * (static_cast<std::size_t>(r) * W + px), c.data(), 3);
+                    }
+                }
+            });
+            *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            return 0;
+        },
+        -1);
+}
+
 // Per-pixel oracle over the rows [row_begin, row_end) (whole frame if both 0).
 VREF_API int vref_dump(const vref_scene* s, int culling, int sorting, int threads, int row_begin, int row_end, AovRec* aov,
               uint8_t* rgb) {
@@ -523,6 +576,41 @@ VREF_API int vref_classify(const vref_scene* s, int row_begin, int row_end, cons
                     cls[i] = static_cast<uint8_t>(
                         classify_pixel(scene, generate_primary_ray(scene.camera, px, py), oracle[i], gpu[i], t_rel));
                 }
+            return 0;
+        },
+        -1);
+}
+
+// Human-readable breakdown of one pixel's classification (debugging aid).
+VREF_API int vref_explain(const vref_scene* s, int px, int py, const AovRec* o, const AovRec* g, char* buf, size_t n) {
+    return guard(
+        [&] {
+            const Scene& scene = s->s;
+            const Ray ray = generate_primary_ray(scene.camera, px, py);
+            std::string out;
+            char line[512];
+            const auto add = [&](const char* fmt, auto... a) {
+                std::snprintf(line, sizeof(line), fmt, a...);
+                out += line;
+            };
+            add("pixel (%d,%d) dir (%.17g %.17g %.17g)\n", px, py, ray.direction.x, ray.direction.y, ray.direction.z);
+            for (const AovRec* r : {o, g}) {
+                add("  %s: id %d t %.17g voxel (%u %u %u) level %u axis %u node %u attr %u trav %u fetch %u\n",
+                    r == o ? "oracle" : "gpu   ", r->object_id, r->t, r->voxel[0], r->voxel[1], r->voxel[2],
+                    r->level, r->entry_axis, r->node_index, r->attr_index, r->traversals, r->node_fetches);
+                if (r->object_id >= 0) {
+                    const SceneObject* obj = scene.find_object(r->object_id);
+                    const Interval iv = voxel_interval(*obj, ray, r->voxel, r->level);
+                    const Ray loc = transform_ray_world_to_local(ray, obj->transform);
+                    add("    voxel interval [%.17g, %.17g] len %.3g  local d (%.6g %.6g %.6g) o (%.6g %.6g %.6g)\n",
+                        iv.in, iv.out, iv.out - iv.in, loc.direction.x, loc.direction.y, loc.direction.z, loc.origin.x,
+                        loc.origin.y, loc.origin.z);
+                    double t64 = 0;
+                    if (instance_t(*obj, ray, t64)) add("    fp64 traverse t %.17g\n", t64);
+                }
+            }
+            add("  tau %.3g class %d\n", tau(o->object_id >= 0 ? o->t : g->t), classify_pixel(scene, ray, *o, *g, 1e-6));
+            std::snprintf(buf, n, "%s", out.c_str());
             return 0;
         },
         -1);

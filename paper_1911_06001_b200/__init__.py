@@ -59,6 +59,7 @@ class config:  # bench_scenes.hpp
     RANDOM = 5
     SORTED_TRACING = 6
     TWO_OBJECTS = 7
+    HBO = 8
 
 
 class Model:
@@ -175,7 +176,12 @@ class Scene:
         import numpy as np
 
         W, H = self.width, self.height
-        img = np.zeros((H, W, 3), np.uint8) if rgb else None
+        if isinstance(rgb, np.ndarray):
+            assert rgb.shape == (H, W, 3) and rgb.dtype == np.uint8 and rgb.flags.c_contiguous
+            img = rgb
+        else:
+            img = np.empty((H, W, 3), np.uint8) if rgb else None
+        rgb = img is not None
         aovs = np.zeros((H, W), AOV_DTYPE) if aov else None
         fs = (C.c_uint64 * 4)()
         ms = C.c_double()

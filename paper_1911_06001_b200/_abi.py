@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+# VOXANIM_LIB_DIR selects an alternative build (tuning experiments); default: the in-tree lib/.
+LIB_DIR = os.environ.get("VOXANIM_LIB_DIR") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 
 VXA_OK, VXA_ERR_INVALID, VXA_ERR_MODEL, VXA_ERR_CUDA, VXA_ERR_OOM, VXA_ERR_NO_DEVICE = range(6)
 VXA_FP32, VXA_FP64 = 0, 1
@@ -75,6 +76,8 @@ class vxa_stats(C.Structure):
         ("leaf_hits", C.c_uint64),
         ("kernel_launches", C.c_uint64),
         ("gpu_ms", C.c_double),
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
     ]
 
 
@@ -87,8 +90,11 @@ class vxa_pixel_aov(C.Structure):
         ("voxel", C.c_uint32 * 3),
         ("level", C.c_uint8),
         ("kind", C.c_uint8),
-        ("traversals", C.c_uint16),
+        ("entry_axis", C.c_uint8),
+        ("pad0", C.c_uint8),
+        ("traversals", C.c_uint32),
         ("node_fetches", C.c_uint32),
+        ("pad1", C.c_uint32),
     ]
 
 
@@ -125,7 +131,7 @@ class vxa_visit(C.Structure):
 
 assert C.sizeof(vxa_instance) == 136
 assert C.sizeof(vxa_hit_record) == 48
-assert C.sizeof(vxa_pixel_aov) == 40
+assert C.sizeof(vxa_pixel_aov) == 48
 assert C.sizeof(vxa_local_ray) == 72
 assert C.sizeof(vxa_traverse_hit) == 96
 
@@ -135,7 +141,8 @@ try:
 
     AOV_DTYPE = np.dtype(
         [("t", "<f8"), ("object_id", "<i4"), ("node_index", "<u4"), ("attr_index", "<u4"), ("voxel", "<u4", (3,)),
-         ("level", "u1"), ("kind", "u1"), ("traversals", "<u2"), ("node_fetches", "<u4")]
+         ("level", "u1"), ("kind", "u1"), ("entry_axis", "u1"), ("pad0", "u1"), ("traversals", "<u4"),
+     ("node_fetches", "<u4"), ("pad1", "<u4")]
     )
     RAY_DTYPE = np.dtype([("origin", "<f8", (3,)), ("direction", "<f8", (3,)), ("half_extent", "<f8", (3,))])
     TRAV_DTYPE = np.dtype(
@@ -145,7 +152,7 @@ try:
          ("log_total", "<u4")],
         align=True,
     )
-    assert AOV_DTYPE.itemsize == 40 and RAY_DTYPE.itemsize == 72 and TRAV_DTYPE.itemsize == 96
+    assert AOV_DTYPE.itemsize == 48 and RAY_DTYPE.itemsize == 72 and TRAV_DTYPE.itemsize == 96
 except ImportError:  # pragma: no cover
     np = None
 
@@ -155,13 +162,13 @@ VXA_SYMBOLS = [
     "vxa_upload_model", "vxa_release_model", "vxa_model_info",
     "vxa_render", "vxa_submit", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
-    "vxa_fb_export", "vxa_fb_import", "vxa_traverse",
+    "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_traverse",
 ]
 VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
     "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
-    "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free",
+    "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit",
     "vxn_hbo_create", "vxn_hbo_free", "vxn_render", "vxn_traverse", "vxn_context",
 ]
 
@@ -202,6 +209,7 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_fb_export", i, P, C.c_int32, C.c_int32, P)
     _declare(lib, "vxa_fb_import", i, P, C.c_int32, C.c_int32, P)
     _declare(lib, "vxa_traverse", i, P, u32, P, u32, u32, P, P, u32)
+    _declare(lib, "vxa_tile_owner", C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32)
     return lib
 
 
@@ -232,6 +240,7 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_scene_export", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32,
              C.POINTER(u32))
     _declare(lib, "vxn_scene_free", None, P)
+    _declare(lib, "vxn_scene_submit", i, P, d, i, i, i)
     _declare(lib, "vxn_hbo_create", P, i, i)
     _declare(lib, "vxn_hbo_free", None, P)
     _declare(lib, "vxn_render", i, P, i, i, i, P, P, P, C.POINTER(u64), C.POINTER(d), C.POINTER(vxa_stats))

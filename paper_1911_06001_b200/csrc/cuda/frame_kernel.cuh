@@ -19,14 +19,32 @@ namespace vxa {
 
 enum : uint32_t { kMiss = 0, kSingle = 1, kMulti = 2 };
 
+constexpr int kBlock = 128;
+// Minimum resident blocks per SM requested from ptxas for the FP32 kernel
+// (register budget 65536 / (128 * n)); tuned by measurement.
+#ifndef VXA_MIN_BLOCKS
+#define VXA_MIN_BLOCKS 1
+#endif
+constexpr int kWarps = kBlock / 32;
+constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
+
 template <typename Real> struct Best {
     bool have;
+    bool pos_dir; // the unmirrored local direction is positive on the entry axis
     Real t;
     int32_t id;
-    uint32_t inst;
-    TravHit<Real> hit;
-    Real normal[3];
+    uint32_t inst, attr, parent, level, axis;
+    uint32_t vox[3];
 };
+
+// World normal of the nearest hit: R n_local with n_local = sign e_axis
+// opposing the unmirrored local direction (traversal.cpp:214-222, renderer.cpp:89).
+template <typename Real> __device__ __forceinline__ void best_normal(const FrameParams<Real>& p, const Best<Real>& b, Real n[3]) {
+    const DevInstance<Real>& in = p.inst[b.inst];
+    Real nl[3] = {Real(0), Real(0), Real(0)};
+    nl[b.axis] = b.pos_dir ? Real(-1) : Real(1);
+    for (int k = 0; k < 3; ++k) n[k] = in.R[3 * k] * nl[0] + in.R[3 * k + 1] * nl[1] + in.R[3 * k + 2] * nl[2];
+}
 
 template <typename Real> struct SphereRes {
     bool hit;
@@ -51,55 +69,117 @@ __device__ __forceinline__ SphereRes<Real> sphere_test(const DevInstance<Real>& 
         s.tc = in.L[0] * d[0] + in.L[1] * d[1] + in.L[2] * d[2];
         const float px = in.L[0] - s.tc * d[0], py = in.L[1] - s.tc * d[1], pz = in.L[2] - s.tc * d[2];
         const float d2 = px * px + py * py + pz * pz;
-        const float slack = 1e-5f * in.r2 + 1e-12f;
-        s.hit = (d2 < in.r2 + slack) && (s.tc + in.r * 1.00001f >= 0.0f);
+        s.hit = (d2 < in.r2 * 1.00001f + 1e-12f) && (s.tc + in.r * 1.00001f >= 0.0f);
         const float tb = s.tc - sqrtf(fmaxf(in.r2 - d2, 0.0f)) - 1e-5f * (fabsf(s.tc) + in.r);
         s.tb = fmaxf(tb, 0.0f);
     }
     return s;
 }
 
-// Local direction of instance i for the pixel's camera-space direction.
-template <typename Real>
-__device__ __forceinline__ void local_dir(const DevInstance<Real>& in, const Real dw[3], const Real dc[3], Real rn,
-                                          Real out[3]) {
-    if constexpr (sizeof(Real) == 8) {
-        // d' = R^T d  (math.hpp:221-224, Mat3*Vec3 row order)
-        for (int k = 0; k < 3; ++k) out[k] = in.M[3 * k] * dw[0] + in.M[3 * k + 1] * dw[1] + in.M[3 * k + 2] * dw[2];
-    } else {
-        // d' = (R^T C) d_cam / |d_cam|
-        for (int k = 0; k < 3; ++k)
-            out[k] = (in.M[3 * k] * dc[0] + in.M[3 * k + 1] * dc[1] + in.M[3 * k + 2] * dc[2]) * rn;
+// Per-pixel primary ray. FP32 kernel: the camera-space direction and its norm
+// are also kept in FP64 (dcd, rnd) so each instance's local direction is formed
+// in FP64 and rounded once: a plane entry t = (A + i s) / d_a is only as
+// accurate as the small component d_a.
+struct RayD {
+    int px, py;
+    double rnd;
+};
+
+// ---- FP32 tile culling --------------------------------------------------------
+// All rays of an 8x4 tile leave the camera inside one cone (axis: the tile's
+// centre direction; half-angle: the widest corner). A bounding sphere that
+// misses the (margin-inflated) cone misses every ray of the tile, so each warp
+// tests the instances once per tile (lane i takes instances i, i+32, ...) and
+// the per-ray sphere pass only visits the ballot-compacted survivors.
+struct TileCone {
+    float a[3];       // world axis (unit)
+    float cos_a, sin_a;
+};
+
+__device__ __forceinline__ TileCone tile_cone(const FrameParams<float>& p, int x0, int y0) {
+    const float cxs = fmaf(static_cast<float>(x0) + 4.0f, p.inv_w2, -1.0f) * p.sx;
+    const float cys = fmaf(-(static_cast<float>(y0) + 2.0f), p.inv_h2, 1.0f) * p.sy;
+    const float cn = rsqrtf(cxs * cxs + cys * cys + 1.0f);
+    const float ax = cxs * cn, ay = cys * cn, az = -cn;
+    float smax = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float xs = fmaf(static_cast<float>(x0) + ((k & 1) ? 7.5f : 0.5f), p.inv_w2, -1.0f) * p.sx;
+        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2) ? 3.5f : 0.5f)), p.inv_h2, 1.0f) * p.sy;
+        const float n = rsqrtf(xs * xs + ys * ys + 1.0f);
+        const float bx = xs * n, by = ys * n, bz = -n;
+        // |a x b| = sin of the angle (accurate for small angles, unlike 1 - cos)
+        const float cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+        smax = fmaxf(smax, sqrtf(cx * cx + cy * cy + cz * cz));
     }
+    TileCone c;
+    c.sin_a = fminf(1.0f, smax * 1.01f + 1e-6f);
+    c.cos_a = sqrtf(fmaxf(0.0f, 1.0f - c.sin_a * c.sin_a));
+    for (int k = 0; k < 3; ++k) c.a[k] = p.C[3 * k] * ax + p.C[3 * k + 1] * ay + p.C[3 * k + 2] * az;
+    return c;
 }
 
-template <typename Real, bool kAov, bool kHbo>
+__device__ __forceinline__ bool cone_candidate(const DevInstance<float>& in, const TileCone& c) {
+    const float lx = in.L[0], ly = in.L[1], lz = in.L[2];
+    const float dist2 = lx * lx + ly * ly + lz * lz;
+    const float r = in.r * 1.001f + 1e-5f * sqrtf(dist2) + 1e-6f;
+    if (dist2 <= r * r) return true; // camera inside the (inflated) sphere
+    const float s = lx * c.a[0] + ly * c.a[1] + lz * c.a[2];
+    const float qx = ly * c.a[2] - lz * c.a[1], qy = lz * c.a[0] - lx * c.a[2], qz = lx * c.a[1] - ly * c.a[0];
+    const float perp = sqrtf(qx * qx + qy * qy + qz * qz);
+    if (perp * c.cos_a - s * c.sin_a > r) return false; // outside the lateral surface
+    return s * c.cos_a + perp * c.sin_a >= 0.0f;        // else only the apex region remains
+}
+
+template <typename Real, bool kAov>
 __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint32_t i, const Real dw[3],
-                                                const Real dc[3], Real rn, Best<Real>& best, uint32_t& traversals,
-                                                uint32_t& fetches) {
+                                                const RayD& rd, Best<Real>& best, uint32_t& traversals,
+                                                uint32_t& fetches, uint2* stack) {
     const DevInstance<Real>& in = p.inst[i];
     if (!in.valid_model) return;
-    LocalRay<Real> lr;
-    local_dir(in, dw, dc, rn, lr.d);
-    setup_root(lr, in.A_lo, in.A_hi, in.zflags, in.zbits);
     ++traversals;
-    TravHit<Real> h;
-    NoLog nolog;
-    const bool hit = traverse_model(in.model, lr, h, nolog);
-    fetches += h.fetches;
-    if (!hit) return;
-    if (!best.have || h.t < best.t || (h.t == best.t && in.id < best.id)) {
+    Real ld[3];
+    Real t;
+    uint32_t axis, attr, parent, level, vox[3];
+    if constexpr (sizeof(Real) == 8) {
+        // d' = R^T d  (math.hpp:221-224, Mat3*Vec3 row order)
+        LocalRay<Real> lr;
+        for (int k = 0; k < 3; ++k) lr.d[k] = in.M[3 * k] * dw[0] + in.M[3 * k + 1] * dw[1] + in.M[3 * k + 2] * dw[2];
+        setup_root(lr, in.A_lo, in.A_hi, in.zflags, in.zbits);
+        TravHit<Real> h;
+        NoLog nolog;
+        const bool hit = traverse_model(in.model, lr, h, nolog);
+        fetches += h.fetches;
+        if (!hit) return;
+        for (int k = 0; k < 3; ++k) ld[k] = lr.d[k];
+        t = h.t, axis = h.axis, attr = h.attr, parent = h.parent, level = h.level;
+        if constexpr (kAov) path_to_voxel(h.path, h.level, vox);
+    } else {
+        const double dcx = fma(static_cast<double>(rd.px) + 0.5, p.d_inv_w2, -1.0) * p.d_sx;
+        const double dcy = fma(-(static_cast<double>(rd.py) + 0.5), p.d_inv_h2, 1.0) * p.d_sy;
+        float d[3];
+        for (int k = 0; k < 3; ++k)
+            d[k] = static_cast<float>((fma(in.Md[3 * k], dcx, in.Md[3 * k + 1] * dcy) - in.Md[3 * k + 2]) * rd.rnd);
+        FastRay fr;
+        if (!fast_setup(fr, d, in.A_lo, in.A_hi, in.Ar_lo, in.Ar_hi, in.h2, in.zflags, in.zbits)) return;
+        FastHit h;
+        const bool hit = traverse_fast<kAov>(in.model, fr, h, stack, kBlock);
+        fetches += h.fetches;
+        if (!hit) return;
+        for (int k = 0; k < 3; ++k) ld[k] = d[k], vox[k] = h.vox[k];
+        t = h.t, axis = h.axis, attr = h.attr, parent = h.parent, level = h.level;
+    }
+    if (!best.have || t < best.t || (t == best.t && in.id < best.id)) {
         best.have = true;
-        best.t = h.t;
+        best.t = t;
         best.id = in.id;
         best.inst = i;
-        best.hit = h;
-        // world normal = R n_local, n_local = sign e_axis opposing the unmirrored local d
-        const int a = static_cast<int>(h.axis);
-        const Real sgn = lr.d[a] > Real(0) ? Real(-1) : Real(1);
-        Real nl[3] = {Real(0), Real(0), Real(0)};
-        nl[a] = sgn;
-        for (int k = 0; k < 3; ++k) best.normal[k] = in.R[3 * k] * nl[0] + in.R[3 * k + 1] * nl[1] + in.R[3 * k + 2] * nl[2];
+        best.attr = attr;
+        best.parent = parent;
+        best.level = level;
+        best.axis = axis;
+        best.pos_dir = ld[axis] > Real(0);
+        if constexpr (kAov) best.vox[0] = vox[0], best.vox[1] = vox[1], best.vox[2] = vox[2];
     }
 }
 
@@ -125,52 +205,83 @@ __device__ __forceinline__ uint32_t shade_rgba(uint32_t color, const Real n[3], 
 }
 
 template <typename Real, bool kAov, bool kHbo>
-__global__ void __launch_bounds__(128) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
+__global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
+    extern __shared__ uint2 smem_stack[]; // FP32 traversal stack: [level][thread]
+    __shared__ uint16_t s_list[kWarps][kListCap];
     const uint32_t lane = threadIdx.x & 31u;
-    unsigned long long n_rays = 0, n_sph = 0, n_trav = 0, n_reuse = 0, n_fetch = 0, n_leaf = 0;
+    const uint32_t warp = threadIdx.x >> 5;
+    // rays and sphere tests per frame are known on the host (pixels x objects)
+    uint32_t n_trav = 0, n_reuse = 0, n_fetch = 0, n_leaf = 0;
     const uint32_t n = p.n_inst;
+    uint2* const stack = smem_stack + threadIdx.x;
+    const uint16_t* const list = s_list[warp];
 
     while (true) {
+        __syncwarp();
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= p.n_tiles) break;
         const uint32_t st = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
-        const int px = static_cast<int>((s % p.n_super_x) * kSuper + (wt % (kSuper / kTileW)) * kTileW + (lane % kTileW));
-        const int py = static_cast<int>((s / p.n_super_x) * kSuper + (wt / (kSuper / kTileW)) * kTileH + (lane / kTileW));
+        const int tx0 = static_cast<int>((s % p.n_super_x) * kSuper + (wt % (kSuper / kTileW)) * kTileW);
+        const int ty0 = static_cast<int>((s / p.n_super_x) * kSuper + (wt / (kSuper / kTileW)) * kTileH);
+        const int px = tx0 + static_cast<int>(lane % kTileW);
+        const int py = ty0 + static_cast<int>(lane / kTileW);
+
+        // ---- tile candidate list (FP32 production kernel with culling)
+        uint32_t list_n = 0xffffffffu; // 0xffffffff: per-ray pass over every instance
+        if constexpr (sizeof(Real) == 4) {
+            if (p.culling && n <= 0xffffu) {
+                const TileCone cone = tile_cone(p, tx0, ty0);
+                uint32_t cnt = 0;
+                for (uint32_t base = 0; base < n; base += 32) {
+                    const uint32_t i = base + lane;
+                    const bool c = i < n && cone_candidate(p.inst[i], cone);
+                    const uint32_t m = __ballot_sync(0xffffffffu, c);
+                    const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
+                    if (c && pos < kListCap) s_list[warp][pos] = static_cast<uint16_t>(i);
+                    cnt += __popc(m);
+                }
+                __syncwarp();
+                if (cnt <= kListCap) list_n = cnt;
+            }
+        }
         if (px >= p.width || py >= p.height) continue;
         const size_t pix = static_cast<size_t>(py) * static_cast<size_t>(p.width) + static_cast<size_t>(px);
 
         // ---- primary ray (renderer.cpp:11-23)
-        Real dw[3], dc[3], rn;
+        Real dw[3];
+        RayD rd;
         if constexpr (sizeof(Real) == 8) {
             const double ndc_x = (px + 0.5) / p.width * 2.0 - 1.0;
             const double ndc_y = 1.0 - (py + 0.5) / p.height * 2.0;
-            dc[0] = ndc_x * p.tan_half * p.aspect;
-            dc[1] = ndc_y * p.tan_half;
-            dc[2] = -1.0;
+            const double dc[3] = {ndc_x * p.tan_half * p.aspect, ndc_y * p.tan_half, -1.0};
             Real w[3];
             for (int k = 0; k < 3; ++k) w[k] = p.C[3 * k] * dc[0] + p.C[3 * k + 1] * dc[1] + p.C[3 * k + 2] * dc[2];
             const double len = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
             for (int k = 0; k < 3; ++k) dw[k] = w[k] / len;
-            rn = 1.0;
         } else {
-            const float ndc_x = fmaf(static_cast<float>(px) + 0.5f, p.inv_w2, -1.0f);
-            const float ndc_y = fmaf(-(static_cast<float>(py) + 0.5f), p.inv_h2, 1.0f);
-            dc[0] = ndc_x * p.sx;
-            dc[1] = ndc_y * p.sy;
-            dc[2] = -1.0f;
-            rn = rsqrtf(fmaf(dc[0], dc[0], fmaf(dc[1], dc[1], 1.0f)));
-            for (int k = 0; k < 3; ++k)
-                dw[k] = (p.C[3 * k] * dc[0] + p.C[3 * k + 1] * dc[1] + p.C[3 * k + 2] * dc[2]) * rn;
+            const float dcx = fmaf(static_cast<float>(px) + 0.5f, p.inv_w2, -1.0f) * p.sx;
+            const float dcy = fmaf(-(static_cast<float>(py) + 0.5f), p.inv_h2, 1.0f) * p.sy;
+            const float rn = rsqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
+            for (int k = 0; k < 3; ++k) dw[k] = (p.C[3 * k] * dcx + p.C[3 * k + 1] * dcy - p.C[3 * k + 2]) * rn;
+            const double ddx = fma(static_cast<double>(px) + 0.5, p.d_inv_w2, -1.0) * p.d_sx;
+            const double ddy = fma(-(static_cast<double>(py) + 0.5), p.d_inv_h2, 1.0) * p.d_sy;
+            rd.px = px;
+            rd.py = py;
+            rd.rnd = rsqrt(fma(ddx, ddx, fma(ddy, ddy, 1.0)));
         }
-        ++n_rays;
 
         // ---- sphere pass: count hits, remember the single hit (HBO rule)
         uint32_t n_hits = 0, only = 0;
-        if (p.sphere_pass) {
-            n_sph += n;
+        unsigned long long hitmask = 0; // list mode: bit k = s_list[warp][k] hit
+        if (list_n != 0xffffffffu) {
+            for (uint32_t k = 0; k < list_n; ++k)
+                if (sphere_test(p.inst[list[k]], dw).hit) hitmask |= 1ull << k;
+            n_hits = __popcll(hitmask);
+            if (n_hits) only = list[__ffsll(hitmask) - 1];
+        } else if (p.sphere_pass) {
             for (uint32_t i = 0; i < n; ++i) {
                 if (sphere_test(p.inst[i], dw).hit) {
                     if (n_hits == 0) only = i;
@@ -183,7 +294,9 @@ __global__ void __launch_bounds__(128) frame_kernel(const __grid_constant__ Fram
         best.have = false;
         best.t = Real(0);
         best.id = -1;
-        best.inst = 0;
+        best.pos_dir = false;
+        best.inst = best.attr = best.parent = best.level = best.axis = 0;
+        best.vox[0] = best.vox[1] = best.vox[2] = 0;
         uint32_t traversals = 0, fetches = 0, kind = kMiss;
         bool reused = false;
         bool single_trace = false;
@@ -201,42 +314,62 @@ __global__ void __launch_bounds__(128) frame_kernel(const __grid_constant__ Fram
         }
 
         if (!reused) {
-            uint32_t n_cand = 0;
+            // One traversal call site; the candidate order comes from a small
+            // state machine (keeps a single inlined copy of the traversal).
+            enum { kOne, kListSorted, kListIdOrder, kAllSorted, kAllIdOrder } mode;
+            uint32_t n_cand;
             if (single_trace) {
-                n_cand = 1;
-                trace_candidate<Real, kAov, kHbo>(p, only, dw, dc, rn, best, traversals, fetches);
+                mode = kOne, n_cand = 1;
+            } else if (list_n != 0xffffffffu) {
+                mode = p.sorting ? kListSorted : kListIdOrder, n_cand = n_hits;
             } else if (p.sorting) {
-                n_cand = p.culling ? n_hits : n;
-                // successive minimum over (t_center, index); index order == id order
-                Real last_tc = -pos_inf<Real>();
-                int last_i = -1;
-                while (true) {
+                mode = kAllSorted, n_cand = p.culling ? n_hits : n;
+            } else {
+                mode = kAllIdOrder, n_cand = p.culling ? n_hits : n;
+            }
+            unsigned long long rem = hitmask; // list modes: hit bits not yet visited
+            Real last_tc = -pos_inf<Real>();  // kAllSorted: last (t_center, index) taken
+            int last_i = -1;
+            uint32_t next_i = 0;              // kAllIdOrder cursor
+            bool one_left = true;
+            while (true) {
+                uint32_t cand = 0;
+                Real cand_tb = Real(0);
+                bool found = false;
+                if (mode == kOne) {
+                    found = one_left, cand = only, one_left = false;
+                } else if (mode == kListSorted) {
+                    // (t_center, index) minimum over the remaining hit bits
+                    int kb = -1;
+                    Real tcb = Real(0);
+                    for (unsigned long long it = rem; it; it &= it - 1) {
+                        const int k = __ffsll(it) - 1;
+                        const SphereRes<Real> sr = sphere_test(p.inst[list[k]], dw);
+                        if (kb < 0 || sr.tc < tcb) kb = k, tcb = sr.tc, cand_tb = sr.tb;
+                    }
+                    if (kb >= 0) found = true, cand = list[kb], rem &= ~(1ull << kb);
+                } else if (mode == kListIdOrder) {
+                    if (rem) found = true, cand = list[__ffsll(rem) - 1], rem &= rem - 1;
+                } else if (mode == kAllSorted) {
                     int k = -1;
-                    Real k_tc = Real(0), k_tb = Real(0);
+                    Real k_tc = Real(0);
                     for (uint32_t i = 0; i < n; ++i) {
                         const SphereRes<Real> sr = sphere_test(p.inst[i], dw);
                         if (p.culling && !sr.hit) continue;
                         const bool after = sr.tc > last_tc || (sr.tc == last_tc && static_cast<int>(i) > last_i);
                         if (!after) continue;
-                        if (k < 0 || sr.tc < k_tc) {
-                            k = static_cast<int>(i);
-                            k_tc = sr.tc;
-                            k_tb = sr.hit ? sr.tb : Real(0);
-                        }
+                        if (k < 0 || sr.tc < k_tc) k = static_cast<int>(i), k_tc = sr.tc, cand_tb = sr.hit ? sr.tb : Real(0);
                     }
-                    if (k < 0) break;
-                    last_tc = k_tc;
-                    last_i = k;
-                    if (best.have && best.t < k_tb) continue; // skip, do not break (renderer.cpp:70-72)
-                    trace_candidate<Real, kAov, kHbo>(p, static_cast<uint32_t>(k), dw, dc, rn, best, traversals, fetches);
+                    if (k >= 0) found = true, cand = static_cast<uint32_t>(k), last_tc = k_tc, last_i = k;
+                } else {
+                    while (next_i < n && p.culling && !sphere_test(p.inst[next_i], dw).hit) ++next_i;
+                    if (next_i < n) found = true, cand = next_i++;
                 }
-            } else {
-                // id order, zero boundaries: every candidate is traversed
-                for (uint32_t i = 0; i < n; ++i) {
-                    if (p.culling && !sphere_test(p.inst[i], dw).hit) continue;
-                    ++n_cand;
-                    trace_candidate<Real, kAov, kHbo>(p, i, dw, dc, rn, best, traversals, fetches);
-                }
+                if (!found) break;
+                // sorted orders: skip (do not break) when the best hit is nearer than the
+                // candidate's sphere (renderer.cpp:70-72); id orders carry t_boundary = 0
+                if ((mode == kListSorted || mode == kAllSorted) && best.have && best.t < cand_tb) continue;
+                trace_candidate<Real, kAov>(p, cand, dw, rd, best, traversals, fetches, stack);
             }
             if (best.have) kind = n_cand > 1 ? kMulti : kSingle;
             if constexpr (kHbo) {
@@ -249,14 +382,16 @@ __global__ void __launch_bounds__(128) frame_kernel(const __grid_constant__ Fram
 
         // ---- shade + store
         uint32_t rgba;
-        HitRec rec;
         if constexpr (kHbo) {
+            HitRec rec;
             if (reused && n_hits == 1) {
                 rec = prev;
             } else {
-                rec.color = best.have ? __ldg(p.inst[best.inst].model.attrs + best.hit.attr) : 0xff000000u;
+                rec.color = best.have ? __ldg(p.inst[best.inst].model.attrs + best.attr) : 0xff000000u;
                 rec.pad0 = 0;
-                for (int k = 0; k < 3; ++k) rec.normal[k] = best.have ? static_cast<double>(best.normal[k]) : 0.0;
+                Real nrm[3] = {Real(0), Real(0), Real(0)};
+                if (best.have) best_normal(p, best, nrm);
+                for (int k = 0; k < 3; ++k) rec.normal[k] = static_cast<double>(nrm[k]);
                 rec.t = best.have ? static_cast<double>(best.t) : 0.0;
                 rec.object_id = best.have ? best.id : -1;
                 rec.kind = static_cast<uint8_t>(kind);
@@ -272,8 +407,10 @@ __global__ void __launch_bounds__(128) frame_kernel(const __grid_constant__ Fram
             reinterpret_cast<HitRec*>(p.hbo)[pix] = rec;
         } else {
             if (best.have) {
-                const uint32_t color = __ldg(p.inst[best.inst].model.attrs + best.hit.attr);
-                rgba = shade_rgba(color, best.normal, dw);
+                const uint32_t color = __ldg(p.inst[best.inst].model.attrs + best.attr);
+                Real nrm[3];
+                best_normal(p, best, nrm);
+                rgba = shade_rgba(color, nrm, dw);
             } else {
                 rgba = p.background;
             }
@@ -285,27 +422,28 @@ __global__ void __launch_bounds__(128) frame_kernel(const __grid_constant__ Fram
             PixelAov a;
             a.t = best.have ? static_cast<double>(best.t) : 0.0;
             a.object_id = best.have ? best.id : (kHbo && reused && n_hits == 1 ? -2 : -1);
-            a.node_index = best.have ? best.hit.parent : 0u;
-            a.attr_index = best.have ? best.hit.attr : 0u;
-            if (best.have)
-                path_to_voxel(best.hit.path, best.hit.level, a.voxel);
-            else
-                a.voxel[0] = a.voxel[1] = a.voxel[2] = 0;
-            a.level = static_cast<uint8_t>(best.have ? best.hit.level : 0);
+            a.node_index = best.parent;
+            a.attr_index = best.attr;
+            a.voxel[0] = best.vox[0];
+            a.voxel[1] = best.vox[1];
+            a.voxel[2] = best.vox[2];
+            a.level = static_cast<uint8_t>(best.level);
             a.kind = static_cast<uint8_t>(kind);
-            a.traversals = static_cast<uint16_t>(traversals);
+            a.entry_axis = static_cast<uint8_t>(best.axis);
+            a.pad0 = 0;
+            a.traversals = traversals;
             a.node_fetches = fetches;
+            a.pad1 = 0;
             reinterpret_cast<PixelAov*>(p.aov)[pix] = a;
         }
     }
 
-    // warp-aggregated counters (rays, sphere tests, traversals, reuse, fetches, leaf hits)
-    unsigned long long vals[6] = {n_rays, n_sph, n_trav, n_reuse, n_fetch, n_leaf};
+    // warp-aggregated counters: traversals, reuse, node fetches, leaf hits
+    const uint32_t vals[4] = {n_trav, n_reuse, n_fetch, n_leaf};
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        unsigned long long v = vals[k];
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-        if (lane == 0 && v) atomicAdd(p.counters + k, v);
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, vals[k]);
+        if (lane == 0 && v) atomicAdd(p.counters + 2 + k, static_cast<unsigned long long>(v));
     }
 }
 

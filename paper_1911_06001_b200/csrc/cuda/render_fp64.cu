@@ -16,12 +16,19 @@ void* pick(bool aov, bool hbo) {
 
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l) {
     void* args[] = {const_cast<FrameParams<double>*>(&p)};
-    return cudaLaunchKernel(pick(aov, hbo), dim3(l.grid), dim3(128), args, 0, l.stream);
+    return cudaLaunchKernel(pick(aov, hbo), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f64(p.max_depth), l.stream);
 }
 
-int frame_blocks_per_sm_f64(bool aov, bool hbo) {
+size_t frame_smem_bytes_f64(uint32_t max_depth) {
+    return 0;
+}
+
+int frame_blocks_per_sm_f64(bool aov, bool hbo, uint32_t max_depth) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, pick(aov, hbo), 128, 0) != cudaSuccess) return 1;
+    void* fn = pick(aov, hbo);
+    const size_t smem = frame_smem_bytes_f64(max_depth);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, smem) != cudaSuccess) return 1;
     return b > 0 ? b : 1;
 }
 

@@ -142,7 +142,15 @@ struct vxa_ctx {
     DevBuf<VisitOut> visits;
 
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, t_a = nullptr, t_b = nullptr;
-    int occ[2][2][2] = {}; // [precision][aov][hbo]
+    int occ[2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][stack height]
+
+    // Frame-kernel timing ring: events recorded tight around every frame
+    // kernel launch; vxa_stats_read sums them (gpu_ms) since the last reset.
+    static constexpr int kRing = 4096;
+    cudaEvent_t k_begin[kRing] = {}, k_end[kRing] = {};
+    int k_count = 0;
+    uint64_t h2d = 0, d2h = 0; // bytes copied since the last reset
+    uint64_t n_rays = 0, n_sphere_tests = 0; // host-counted (pixels rendered x objects tested)
 };
 
 namespace {
@@ -197,6 +205,10 @@ int build_instances(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* i
             d.L[a] = static_cast<Real>(l[a]);
             d.A_lo[a] = static_cast<Real>(-h[a] - ol[a]);
             d.A_hi[a] = static_cast<Real>(h[a] - ol[a]);
+            d.h2[a] = static_cast<Real>(2.0 * h[a]);
+            const double alo = -h[a] - ol[a], ahi = h[a] - ol[a];
+            d.Ar_lo[a] = static_cast<float>(alo - static_cast<double>(static_cast<float>(alo)));
+            d.Ar_hi[a] = static_cast<float>(ahi - static_cast<double>(static_cast<float>(ahi)));
             d.zbits[a] = zero_dir_bits(ol[a], h[a]);
             if (-h[a] > ol[a]) d.zflags |= 1u << a;
             if (h[a] > ol[a]) d.zflags |= 1u << (3 + a);
@@ -205,16 +217,17 @@ int build_instances(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* i
         d.r = static_cast<Real>(r);
         d.r2 = static_cast<Real>(r2);
         for (int i = 0; i < 9; ++i) d.R[i] = static_cast<Real>(R[i]);
+        // camera -> local rotation R^T C in FP64 (FP32 kernel's local direction)
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                double acc = 0.0;
+                for (int k2 = 0; k2 < 3; ++k2) acc += Rt[3 * i + k2] * C[3 * k2 + j];
+                d.Md[3 * i + j] = acc;
+            }
         if constexpr (sizeof(Real) == 8) {
             for (int i = 0; i < 9; ++i) d.M[i] = Rt[i];
         } else {
-            // camera -> local rotation, folded in FP64 and rounded once
-            for (int i = 0; i < 3; ++i)
-                for (int j = 0; j < 3; ++j) {
-                    double acc = 0.0;
-                    for (int k2 = 0; k2 < 3; ++k2) acc += Rt[3 * i + k2] * C[3 * k2 + j];
-                    d.M[3 * i + j] = static_cast<float>(acc);
-                }
+            for (int i = 0; i < 9; ++i) d.M[i] = static_cast<float>(d.Md[i]);
         }
     }
     return VXA_OK;
@@ -233,6 +246,10 @@ template <typename Real> void fill_camera(FrameParams<Real>& p, const vxa_frame_
     p.inv_h2 = static_cast<Real>(2.0 / c.height);
     p.sx = static_cast<Real>(tan_half * aspect);
     p.sy = static_cast<Real>(tan_half);
+    p.d_inv_w2 = 2.0 / c.width;
+    p.d_inv_h2 = 2.0 / c.height;
+    p.d_sx = tan_half * aspect;
+    p.d_sy = tan_half;
     p.width = c.width;
     p.height = c.height;
 }
@@ -296,32 +313,55 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.camera_dirty = f->camera_dirty ? 1u : 0u;
     p.rank = f->tile_rank;
     p.world = f->tile_world;
-    p.n_super_x = static_cast<uint32_t>((W + kSuper - 1) / kSuper);
+    p.n_super_x = super_tiles_x(W);
     const uint32_t n_super = p.n_super_x * static_cast<uint32_t>((H + kSuper - 1) / kSuper);
     const uint32_t mine = (n_super + static_cast<uint32_t>(f->tile_world - f->tile_rank) - 1) / static_cast<uint32_t>(f->tile_world);
     p.n_tiles = mine * static_cast<uint32_t>(kTilesPerSuper);
+    // FrameStats::rays / sphere_tests (renderer.cpp:149-151,253): pixels of this
+    // rank's super-tiles, times every object when the sphere pass runs
+    uint64_t my_pixels = 0;
+    const uint32_t nsy = static_cast<uint32_t>((H + kSuper - 1) / kSuper);
+    for (uint32_t sy = 0; sy < nsy; ++sy)
+        for (uint32_t sx = 0; sx < p.n_super_x; ++sx)
+            if ((sy * p.n_super_x + sx) % static_cast<uint32_t>(f->tile_world) == static_cast<uint32_t>(f->tile_rank))
+                my_pixels += static_cast<uint64_t>(std::min<int32_t>(kSuper, W - static_cast<int32_t>(sx) * kSuper)) *
+                             static_cast<uint64_t>(std::min<int32_t>(kSuper, H - static_cast<int32_t>(sy) * kSuper));
+    ctx->n_rays += my_pixels;
+    if (p.sphere_pass) ctx->n_sphere_tests += my_pixels * n;
     p.fb = target;
+    p.max_depth = 1;
+    for (const auto& di : tab)
+        if (di.valid_model) p.max_depth = std::max(p.max_depth, std::min(di.model.depth, kMaxDepth));
     p.tile_counter = ctx->tile_counter.ptr;
     p.counters = ctx->counters.ptr;
     p.aov = aov;
     p.hbo = hbo;
 
     if (bytes) VXA_CUDA(cudaMemcpyAsync(ctx->inst_dev.ptr, ctx->inst_host[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d += bytes;
     VXA_CUDA(cudaEventRecord(ctx->inst_done[slot], ctx->stream));
     VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, sizeof(uint32_t), ctx->stream));
     if (reset_counters) VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
 
     const bool is64 = sizeof(Real) == 8;
     const bool a = aov != nullptr, h = hbo != nullptr;
-    int& occ = ctx->occ[is64][a][h];
-    if (occ == 0) occ = is64 ? frame_blocks_per_sm_f64(a, h) : frame_blocks_per_sm_f32(a, h);
+    int& occ = ctx->occ[is64][a][h][p.max_depth];
+    if (occ == 0) occ = is64 ? frame_blocks_per_sm_f64(a, h, p.max_depth) : frame_blocks_per_sm_f32(a, h, p.max_depth);
     FrameLaunch l{ctx->sm_count * occ, ctx->stream};
+    const int slot_k = ctx->k_count % vxa_ctx::kRing;
+    if (ctx->k_begin[slot_k] == nullptr) {
+        VXA_CUDA(cudaEventCreate(&ctx->k_begin[slot_k]));
+        VXA_CUDA(cudaEventCreate(&ctx->k_end[slot_k]));
+    }
+    VXA_CUDA(cudaEventRecord(ctx->k_begin[slot_k], ctx->stream));
     cudaError_t e;
     if constexpr (sizeof(Real) == 8)
         e = launch_frame_f64(p, a, h, l);
     else
         e = launch_frame_f32(p, a, h, l);
     if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
+    VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
+    ++ctx->k_count;
     return VXA_OK;
 }
 
@@ -335,12 +375,24 @@ int read_counters(vxa_ctx* ctx, vxa_stats* s) {
     unsigned long long c[8] = {};
     VXA_CUDA(cudaMemcpyAsync(c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
-    s->rays = c[0];
-    s->sphere_tests = c[1];
+    s->rays = ctx->n_rays;
+    s->sphere_tests = ctx->n_sphere_tests;
     s->svo_traversals = c[2];
     s->pixels_reused = c[3];
     s->node_fetches = c[4];
     s->leaf_hits = c[5];
+    // kernel time of the frames since the last reset (the ring keeps the last kRing)
+    const int n = std::min(ctx->k_count, vxa_ctx::kRing);
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) {
+        float ms = 0.f;
+        VXA_CUDA(cudaEventElapsedTime(&ms, ctx->k_begin[i], ctx->k_end[i]));
+        total += ms;
+    }
+    s->gpu_ms = total;
+    s->kernel_launches = static_cast<uint64_t>(ctx->k_count);
+    s->h2d_bytes = ctx->h2d;
+    s->d2h_bytes = ctx->d2h + sizeof(c);
     return VXA_OK;
 }
 
@@ -419,6 +471,10 @@ int vxa_destroy(vxa_ctx* ctx) {
     }
     for (cudaEvent_t e : {ctx->ev_a, ctx->ev_b, ctx->t_a, ctx->t_b})
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < vxa_ctx::kRing; ++i) {
+        if (ctx->k_begin[i]) cudaEventDestroy(ctx->k_begin[i]);
+        if (ctx->k_end[i]) cudaEventDestroy(ctx->k_end[i]);
+    }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return VXA_OK;
@@ -531,7 +587,11 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         VXA_CUDA(ctx->hbo.ensure(npix));
         hbo = ctx->hbo.ptr;
         VXA_CUDA(cudaMemcpyAsync(hbo, f->hbo, npix * sizeof(HitRec), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->h2d += npix * sizeof(HitRec);
     }
+    ctx->k_count = 0;
+    ctx->h2d = ctx->d2h = 0;
+    ctx->n_rays = ctx->n_sphere_tests = 0;
     VXA_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
     if (int rc = enqueue_any(ctx, f, in, n, aov, hbo, true); rc != VXA_OK) return rc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
@@ -543,16 +603,19 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         VXA_CUDA(cudaGetLastError());
         ++launches;
         VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->d2h += npix * 3;
     }
-    if (aov_out)
+    if (aov_out) {
         VXA_CUDA(cudaMemcpyAsync(aov_out, aov, npix * sizeof(PixelAov), cudaMemcpyDeviceToHost, ctx->stream));
-    if (f->hbo) VXA_CUDA(cudaMemcpyAsync(f->hbo, hbo, npix * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->d2h += npix * sizeof(PixelAov);
+    }
+    if (f->hbo) {
+        VXA_CUDA(cudaMemcpyAsync(f->hbo, hbo, npix * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->d2h += npix * sizeof(HitRec);
+    }
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
     if (stats) {
         if (int rc = read_counters(ctx, stats); rc != VXA_OK) return rc;
-        float ms = 0.f;
-        VXA_CUDA(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
-        stats->gpu_ms = ms;
         stats->kernel_launches = launches;
     }
     return VXA_OK;
@@ -582,6 +645,9 @@ int vxa_stats_read(vxa_ctx* ctx, vxa_stats* stats) {
 int vxa_stats_reset(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
+    ctx->k_count = 0;
+    ctx->h2d = ctx->d2h = 0;
+    ctx->n_rays = ctx->n_sphere_tests = 0;
     return VXA_OK;
 }
 
@@ -652,6 +718,11 @@ int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_h
     ctx->peer_w = width;
     ctx->peer_h = height;
     return VXA_OK;
+}
+
+int32_t vxa_tile_owner(int32_t x, int32_t y, int32_t width, int32_t height, int32_t world) {
+    if (world < 1 || x < 0 || y < 0 || x >= width || y >= height) return -1;
+    return tile_owner(x, y, width, world);
 }
 
 int vxa_traverse(vxa_ctx* ctx, uint32_t model, const vxa_local_ray* rays, uint32_t n, uint32_t precision,

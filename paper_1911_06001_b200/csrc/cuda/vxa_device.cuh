@@ -38,6 +38,15 @@ constexpr int kTileW = 8, kTileH = 4;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
 
+// Screen partition: 64x64 super-tile s = (y / 64) * n_super_x + x / 64 belongs
+// to rank s % world. The frame kernel enumerates a rank's super-tiles as
+// s = j * world + rank, which is this map inverted.
+__host__ __device__ inline uint32_t super_tiles_x(int32_t width) { return static_cast<uint32_t>((width + kSuper - 1) / kSuper); }
+__host__ __device__ inline int32_t tile_owner(int32_t x, int32_t y, int32_t width, int32_t world) {
+    const uint32_t s = static_cast<uint32_t>(y / kSuper) * super_tiles_x(width) + static_cast<uint32_t>(x / kSuper);
+    return static_cast<int32_t>(s % static_cast<uint32_t>(world));
+}
+
 struct DevModel {
     const uint2* words;
     const uint32_t* side;
@@ -57,6 +66,9 @@ template <typename Real> struct DevInstance {
     Real R[9];    // world rotation (FP64 normal = R n_local)
     Real A_lo[3]; // -h - o_local  (o_local = R^T (cam - t), FP64)
     Real A_hi[3]; //  h - o_local
+    Real h2[3];   // 2h (root cell size)
+    float Ar_lo[3], Ar_hi[3]; // FP32 kernel: FP64 rounding residuals of A_lo / A_hi
+    double Md[9]; // FP64 R^T C (camera -> local), FP32 kernel's local direction
     uint32_t zbits[3]; // zero-direction path: bit L set iff o >= centre at level L
     uint32_t zflags;   // bit a: (-h > o); bit 3+a: (h > o)   (zero-direction slab signs)
     int32_t id;
@@ -76,6 +88,7 @@ template <typename Real> struct FrameParams {
     Real aspect;       // (double)W / H
     Real inv_w2, inv_h2; // FP32 ray setup: 2/W, 2/H
     Real sx, sy;       // FP32 ray setup: tan_half * aspect, tan_half
+    double d_inv_w2, d_inv_h2, d_sx, d_sy; // the same in FP64 (FP32 kernel's local directions)
     uint32_t background; // RGBA8
     uint32_t culling, sorting, sphere_pass;
     uint32_t camera_dirty;
@@ -83,6 +96,7 @@ template <typename Real> struct FrameParams {
     int32_t rank, world;
     uint32_t n_super_x;
     uint32_t n_tiles; // warp tiles owned by this rank
+    uint32_t max_depth; // deepest model of the frame (FP32 shared-memory stack height)
     // outputs
     uint32_t* fb;                 // RGBA8 framebuffer (local or peer-mapped)
     uint32_t* tile_counter;       // persistent-thread work counter
@@ -100,10 +114,13 @@ struct PixelAov {
     uint32_t voxel[3];
     uint8_t level;
     uint8_t kind;
-    uint16_t traversals;
+    uint8_t entry_axis;
+    uint8_t pad0;
+    uint32_t traversals;
     uint32_t node_fetches;
+    uint32_t pad1;
 };
-static_assert(sizeof(PixelAov) == 40, "vxa_pixel_aov layout");
+static_assert(sizeof(PixelAov) == 48, "vxa_pixel_aov layout");
 
 struct HitRec {
     uint32_t color;
@@ -337,6 +354,208 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
 #pragma unroll
         for (int a = 0; a < 3; ++a) tm[a] = midplane(r, a, f0[a], f1[a], level);
         fcur = first_child(f0, tm);
+    }
+    out.fetches = fetches;
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+// Production FP32 core: the same Revelles decision structure (mirror mask,
+// first_node / next_node with strict comparisons, front-to-back children,
+// cull rule, leaf/push rules) but the node's slab planes are derived in
+// position space, as the paper does by halving the parent's edge vectors:
+// node (c, L) spans [c s_L, (c+1) s_L) of the mirrored axis (s_L = 2h / 2^L,
+// halving is exact), and a plane's parameter is t = fma(i, s_L, A) * inv_d
+// with A = -h - o (FP64-folded, rounded once). Every plane therefore has one
+// t value at every level (siblings share their planes bit for bit: the
+// traversal is watertight), the error stays ~2 ulp at any depth, and the
+// stack only holds node words: t0/t1/tm are recomputed from the cell
+// coordinates on a pop instead of being stored.
+
+struct FastRay {
+    float A[3];     // -h - o_m (mirrored frame), rounded
+    float Ar[3];    // its FP64 rounding residual (A + Ar == -h - o_m to ~2^-48)
+    float inv_d[3]; // 1 / |d|
+    float s0[3];    // root cell size 2h
+    float d[3];     // unmirrored local direction (normal sign)
+    uint32_t mirror, zero;
+    uint32_t zbits[3];
+};
+
+struct FastHit {
+    float t;
+    uint32_t attr, parent, level, axis;
+    uint32_t vox[3]; // leaf voxel, unmirrored (leaf_path_to_voxel)
+    uint32_t fetches;
+};
+
+// t of the plane at integer position i (cell size s) of one mirrored axis.
+// (i s + A) is exact inside the FMA; adding the residual keeps the plane
+// offset accurate when it cancels against A (a plane close to the origin).
+__device__ __forceinline__ float plane_t(float i, float s, float A, float Ar, float inv) {
+    return __fmul_rn(__fadd_rn(__fmaf_rn(i, s, A), Ar), inv);
+}
+
+__device__ __forceinline__ float zero_mid(const FastRay& r, int a, int level) {
+    return ((r.zbits[a] >> level) & 1u) ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+}
+
+// t0 / tm / t1 of the node with (float, exact) cell coordinates c at size s.
+__device__ __forceinline__ void node_planes(const FastRay& r, const float c[3], const float s[3], int level,
+                                            float t0[3], float tm[3], float t1[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        t0[a] = plane_t(c[a], s[a], r.A[a], r.Ar[a], r.inv_d[a]);
+        t1[a] = plane_t(c[a] + 1.0f, s[a], r.A[a], r.Ar[a], r.inv_d[a]);
+        tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * s[a], r.A[a], r.Ar[a], r.inv_d[a]);
+    }
+    if (r.zero) {
+        const float inf = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            if (r.zero & axis_bit(a)) {
+                t0[a] = -inf;
+                t1[a] = inf;
+                tm[a] = zero_mid(r, a, level);
+            }
+    }
+}
+
+// Root setup from the FP32-rounded local direction and host-folded offsets
+// (A_* rounded, Ar_* residuals). Returns false when the ray misses the root
+// box (traversal.cpp:56-60).
+__device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const float A_lo[3], const float A_hi[3],
+                                           const float Ar_lo[3], const float Ar_hi[3], const float h2[3],
+                                           uint32_t zflags, const uint32_t zbits[3]) {
+    r.mirror = 0;
+    r.zero = 0;
+    const float inf = __int_as_float(0x7f800000);
+    float te = -inf, tx = inf;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r.d[a] = d[a];
+        r.zbits[a] = zbits[a];
+        r.s0[a] = h2[a];
+        if (d[a] == 0.0f) {
+            r.zero |= axis_bit(a);
+            r.A[a] = 0.0f;
+            r.Ar[a] = 0.0f;
+            r.inv_d[a] = 0.0f;
+            // zero-direction slab convention: inside iff -h <= o < h
+            if ((zflags >> a) & 1u) te = inf;
+            if (!((zflags >> (3 + a)) & 1u)) tx = -inf;
+        } else {
+            const bool m = d[a] < 0.0f;
+            if (m) r.mirror |= axis_bit(a);
+            r.A[a] = m ? -A_hi[a] : A_lo[a];
+            r.Ar[a] = m ? -Ar_hi[a] : Ar_lo[a];
+            r.inv_d[a] = __frcp_rn(fabsf(d[a]));
+            te = fmaxf(te, plane_t(0.0f, h2[a], r.A[a], r.Ar[a], r.inv_d[a]));
+            tx = fminf(tx, plane_t(1.0f, h2[a], r.A[a], r.Ar[a], r.inv_d[a]));
+        }
+    }
+    return !(te >= tx || tx < 0.0f);
+}
+
+// Stack of ancestor node words (bits 24..27 of .x: the saved next octant).
+// kSmemStack: one column per thread in shared memory ([level][thread]:
+// conflict-free whatever the per-lane levels); else a local array.
+template <bool kTrackIdx>
+__device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out, uint2* __restrict__ stack,
+                              uint32_t stride) {
+    uint32_t sidx[kMaxDepth]; // ancestor indices, kept only for AOVs / models with mixed nodes
+    float c[3] = {0.0f, 0.0f, 0.0f};
+    float s[3] = {r.s0[0], r.s0[1], r.s0[2]};
+    float t0[3], tm[3], t1[3];
+    node_planes(r, c, s, 0, t0, tm, t1);
+    uint2 fw = load_node(m, 0);
+    uint32_t fidx = 0, fetches = 1;
+    uint32_t fcur = first_child(t0, tm);
+    int level = 0;
+    const int depth = min(static_cast<int>(m.depth), static_cast<int>(kMaxDepth));
+
+    while (true) {
+        if (fcur == kExit) {
+            if (level == 0) break;
+            --level;
+            fw = stack[level * stride];
+            fcur = (fw.x >> 24) & 0xfu;
+            fw.x &= 0x00ffffffu;
+            if (kTrackIdx || m.side != nullptr) fidx = sidx[level];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                c[a] = floorf(0.5f * c[a]);
+                s[a] = 2.0f * s[a];
+            }
+            node_planes(r, c, s, level, t0, tm, t1);
+            continue;
+        }
+        const uint32_t q = fcur;
+        float c0[3], c1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const bool up = (q & axis_bit(a)) != 0;
+            c0[a] = up ? tm[a] : t0[a];
+            c1[a] = up ? t1[a] : tm[a];
+        }
+        fcur = next_child(c1, q);
+        int entry = 0;
+        float t_enter = c0[0];
+        if (c0[1] > t_enter) {
+            entry = 1;
+            t_enter = c0[1];
+        }
+        if (c0[2] > t_enter) {
+            entry = 2;
+            t_enter = c0[2];
+        }
+        const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
+        if (!(t_enter < t_exit) || t_exit < 0.0f) continue;
+
+        const uint32_t oct = q ^ r.mirror;
+        const uint32_t bit = 1u << oct;
+        const uint32_t valid = fw.x & 0xffu;
+        const uint32_t leafm = (fw.x >> 8) & 0xffu;
+        if (!(valid & bit)) continue;
+        if (leafm & bit) {
+            uint32_t abase = fw.y;
+            if (fw.x & kMixed) abase = __ldg(m.side + fidx);
+            out.attr = abase + popc8_below(valid & leafm, bit);
+            out.t = fmaxf(t_enter, 0.0f);
+            out.parent = fidx;
+            out.level = static_cast<uint32_t>(level + 1);
+            out.axis = static_cast<uint32_t>(entry);
+            out.fetches = fetches;
+            const uint32_t top = (2u << level) - 1u; // 2^(level+1) - 1
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const uint32_t v = 2u * static_cast<uint32_t>(c[a]) + ((q >> (2 - a)) & 1u);
+                out.vox[a] = (r.mirror & axis_bit(a)) ? top - v : v;
+            }
+            return true;
+        }
+        if (level + 1 >= depth) continue;
+        const uint32_t child = fw.y + popc8_below(valid & ~leafm, bit);
+        stack[level * stride] = make_uint2(fw.x | (fcur << 24), fw.y);
+        if (kTrackIdx || m.side != nullptr) sidx[level] = fidx;
+        ++level;
+        fidx = child; // kept for mixed nodes (side array) and AOVs
+        fw = load_node(m, child);
+        ++fetches;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            c[a] = __fmaf_rn(2.0f, c[a], static_cast<float>((q >> (2 - a)) & 1u));
+            s[a] = 0.5f * s[a];
+            t0[a] = c0[a];
+            t1[a] = c1[a];
+            tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * s[a], r.A[a], r.Ar[a], r.inv_d[a]);
+        }
+        if (r.zero) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (r.zero & axis_bit(a)) tm[a] = zero_mid(r, a, level);
+        }
+        fcur = first_child(t0, tm);
     }
     out.fetches = fetches;
     return false;

@@ -149,12 +149,18 @@ Scene make_config_scene(int config, const std::vector<std::shared_ptr<const SvoM
         w = 64, h = 48;
         break;
     }
-    case kTwoObjects: {
+    case kTwoObjects:
+    case kHboScene: {
         for (int i = 0; i < 2; ++i) {
             RigidTransform tf;
             tf.translation = {i == 0 ? -2.0 : 2.0, 0, 0};
             tf.scale = {1.5, 1.5, 1.5};
             s.objects.push_back(object(i, models[0], tf));
+        }
+        if (config == kHboScene) {
+            RigidTransform tf;
+            tf.translation = {0, 1.5, 1};
+            s.objects.push_back(object(2, models.size() > 1 ? models[1] : models[0], tf));
         }
         s.camera = make_look_at_camera({0, 0, 8}, {0, 0, 0}, {0, 1, 0}, 50, 96, 64);
         s.background = {10, 20, 30};

@@ -22,6 +22,7 @@ enum SceneConfig : int {
     kRandomScene = 5,      // one object per model, seeded random rigid transforms (parity tests)
     kSortedTracing = 6,    // reference test_renderer.cpp:166-179 layout (D, B, A, C along +x)
     kTwoObjects = 7,       // reference test_renderer.cpp:285-293 layout
+    kHboScene = 8,         // kTwoObjects + models[1] at (0, 1.5, 1) (test_renderer.cpp:371-374)
 };
 
 // models: C1-C4 use models[0]; kRandomScene uses every model; kSortedTracing

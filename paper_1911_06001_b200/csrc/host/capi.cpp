@@ -170,40 +170,79 @@ int vxn_scene_set_object(vxn_scene* s, int index, const double* tf, int dirty) {
     return 0;
 }
 
+namespace {
+
+void export_frame(const voxanim::Scene& sc, vxa_frame_desc* f) {
+    *f = vxa_frame_desc{};
+    for (int k = 0; k < 3; ++k) f->camera.position[k] = sc.camera.position[k];
+    std::memcpy(f->camera.orientation, sc.camera.orientation.m.data(), 9 * sizeof(double));
+    f->camera.vertical_fov_deg = sc.camera.vertical_fov_deg;
+    f->camera.width = sc.camera.width;
+    f->camera.height = sc.camera.height;
+    std::memcpy(f->background, sc.background.data(), 3);
+    f->culling = 1;
+    f->sorting = 1;
+    f->camera_dirty = sc.camera.dirty ? 1 : 0;
+    f->tile_rank = 0;
+    f->tile_world = 1;
+}
+
+// Instances with model handles (one cache lookup per distinct model).
+void export_instances(const voxanim::Scene& sc, vxa_instance* inst) {
+    const voxanim::SvoModel* last = nullptr;
+    std::uint32_t last_handle = 0;
+    for (std::size_t i = 0; i < sc.objects.size(); ++i) {
+        const voxanim::SceneObject& o = sc.objects[i];
+        vxa_instance& v = inst[i];
+        v = vxa_instance{};
+        v.id = o.id;
+        if (o.model) {
+            if (o.model.get() != last) {
+                last = o.model.get();
+                last_handle = voxanim::gpu::model_handle(*o.model);
+            }
+            v.model = last_handle;
+        }
+        std::memcpy(v.rotation, o.transform.rotation.m.data(), 9 * sizeof(double));
+        for (int k = 0; k < 3; ++k) {
+            v.translation[k] = o.transform.translation[k];
+            v.scale[k] = o.transform.scale[k];
+        }
+        v.dirty = o.dirty ? 1 : 0;
+    }
+}
+
+} // namespace
+
+int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int world) {
+    return guard(
+        [&] {
+            if (time >= 0.0) voxanim::evaluate_animation(s->s, time);
+            thread_local std::vector<vxa_instance> inst;
+            inst.resize(s->s.objects.size());
+            vxa_frame_desc f;
+            export_frame(s->s, &f);
+            export_instances(s->s, inst.data());
+            f.precision = static_cast<std::uint8_t>(precision);
+            f.tile_rank = rank;
+            f.tile_world = world;
+            voxanim::gpu::check(vxa_submit(voxanim::gpu::context(), &f, inst.data(),
+                                           static_cast<std::uint32_t>(inst.size())),
+                                "vxa_submit");
+            return 0;
+        },
+        -1);
+}
+
 int vxn_scene_export(vxn_scene* s, vxa_frame_desc* f, vxa_instance* inst, uint32_t cap, uint32_t* count) {
     return guard(
         [&] {
             const voxanim::Scene& sc = s->s;
             if (count) *count = static_cast<uint32_t>(sc.objects.size());
-            if (f) {
-                *f = vxa_frame_desc{};
-                for (int k = 0; k < 3; ++k) f->camera.position[k] = sc.camera.position[k];
-                std::memcpy(f->camera.orientation, sc.camera.orientation.m.data(), 9 * sizeof(double));
-                f->camera.vertical_fov_deg = sc.camera.vertical_fov_deg;
-                f->camera.width = sc.camera.width;
-                f->camera.height = sc.camera.height;
-                std::memcpy(f->background, sc.background.data(), 3);
-                f->culling = 1;
-                f->sorting = 1;
-                f->camera_dirty = sc.camera.dirty ? 1 : 0;
-                f->tile_rank = 0;
-                f->tile_world = 1;
-            }
+            if (f) export_frame(sc, f);
             if (inst) {
                 if (cap < sc.objects.size()) throw voxanim::ValidationError("export: instance buffer too small");
-                for (std::size_t i = 0; i < sc.objects.size(); ++i) {
-                    const voxanim::SceneObject& o = sc.objects[i];
-                    vxa_instance& v = inst[i];
-                    v = vxa_instance{};
-                    v.id = o.id;
-                    v.model = o.model ? voxanim::gpu::model_handle(*o.model) : 0u;
-                    std::memcpy(v.rotation, o.transform.rotation.m.data(), 9 * sizeof(double));
-                    for (int k = 0; k < 3; ++k) {
-                        v.translation[k] = o.transform.translation[k];
-                        v.scale[k] = o.transform.scale[k];
-                    }
-                    v.dirty = o.dirty ? 1 : 0;
-                }
+                export_instances(sc, inst);
             }
             return 0;
         },

@@ -1,0 +1,85 @@
+"""CPU: the host C++ model path against the reference (oracle/_ref).
+
+* build_from_grid (ours) == build_from_grid (reference), byte for byte, on the
+  reference's own random-grid generator (tests/support/oracles.hpp:265-279);
+* the sparse procedural builder == the reference's dense route
+  (gen_primitive(Sphere) -> build_from_grid) for depth <= 8, solid and shell;
+* node / leaf counts of the benchmark models;
+* the .svo stream: our serialize is accepted by the reference deserialize and
+  re-serialises identically; corrupted streams are rejected with the same
+  error class and message as the reference (svo.cpp:231-291).
+"""
+import struct
+
+import pytest
+
+import paper_1911_06001_b200 as vx
+from oracle import ref
+
+
+@pytest.mark.parametrize("depth", range(1, 9))
+def test_procedural_solid_matches_reference_dense_build(depth):
+    assert vx.Model.procedural(depth, shell=False).serialize() == ref.RefModel.dense_sphere(depth).serialize()
+
+
+@pytest.mark.parametrize("depth", range(1, 9))
+def test_procedural_shell_matches_reference_dense_build(depth):
+    assert vx.Model.procedural(depth, shell=True).serialize() == ref.RefModel.shell_grid(depth).serialize()
+
+
+@pytest.mark.parametrize("depth", [1, 3, 6])
+def test_dense_build_matches_reference(depth):
+    assert vx.Model.dense_sphere(depth).serialize() == ref.RefModel.dense_sphere(depth).serialize()
+
+
+@pytest.mark.parametrize("seed,depth,fill", [(1, 1, 0.5), (2, 2, 0.3), (3, 3, 0.1), (4, 4, 0.45), (5, 5, 0.02),
+                                             (6, 5, 0.3), (7, 6, 0.05)])
+def test_random_grid_build_matches_reference(seed, depth, fill):
+    assert vx.Model.random(seed, depth, fill).serialize() == ref.RefModel.random(seed, depth, fill).serialize()
+
+
+def test_benchmark_model_counts():
+    # C1 depth-8 solid; C2/C3 depth-10 shell; C4 depth-11 shell
+    assert vx.Model.procedural(8, shell=False).info() == {"depth": 8, "nodes": 1284089, "attributes": 8783848}
+    assert vx.Model.procedural(10, shell=True).info() == {"depth": 10, "nodes": 1333345, "attributes": 2734640}
+    m11 = vx.Model.procedural(11, shell=True)
+    assert m11.info() == {"depth": 11, "nodes": 5328225, "attributes": 10945296}
+    assert len(m11.serialize()) == 107719904
+    assert m11.violations() == 0
+
+
+def test_serialize_roundtrip_through_reference():
+    m = vx.Model.procedural(6, shell=True)
+    b = m.serialize()
+    assert ref.RefModel.from_bytes(b).serialize() == b
+    assert vx.Model.from_bytes(b).serialize() == b
+
+
+def _corruptions(b):
+    n_nodes = struct.unpack_from("<I", b, 12)[0]
+    out = {
+        "bad_magic": b"XVOA" + b[4:],
+        "bad_version": b[:4] + struct.pack("<I", 2) + b[8:],
+        "bad_header": b[:8] + struct.pack("<I", 17) + b[12:],
+        "truncated_header": b[:10],
+        "truncated": b[:-1],
+        "trailing": b + b"\0",
+    }
+    nb = bytearray(b)
+    struct.pack_into("<I", nb, 20, n_nodes + 5)  # root child_base out of range
+    out["node_index"] = bytes(nb)
+    ab = bytearray(b)
+    last = 20 + 12 * (n_nodes - 1)
+    struct.pack_into("<I", ab, last + 4, 1 << 30)  # a leaf parent's attr_base out of range
+    out["attr_index"] = bytes(ab)
+    return out
+
+
+def test_corrupted_streams_rejected_like_the_reference():
+    b = vx.Model.procedural(3, shell=True).serialize()
+    for name, data in _corruptions(b).items():
+        with pytest.raises(vx.VoxanimError) as ours:
+            vx.Model.from_bytes(data)
+        with pytest.raises(RuntimeError) as theirs:
+            ref.RefModel.from_bytes(data)
+        assert str(ours.value) == str(theirs.value), name

@@ -1,0 +1,115 @@
+"""GPU: render_frame semantics beyond the image — the hit buffer (HBO,
+renderer.cpp:143-169,207-213,254-263), FrameStats, the multi-device screen
+partition, and the error contract of the drop-in API."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_1911_06001_b200 as vx
+from paper_1911_06001_b200 import _abi
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+
+def hbo_pair(seed=414):
+    models = [vx.Model.full_cube(), vx.Model.random(seed, 3, 0.3)]
+    s = vx.Scene(vx.config.HBO, models)
+    o = ref.RefScene(vx.config.HBO, [ref.RefModel.from_bytes(m.serialize()) for m in models])
+    return s, o
+
+
+def mutate(scene, frame, rng_t):
+    """The reference HBO-transparency recipe (test_renderer.cpp:376-408)."""
+    if frame % 3 == 1:
+        oid, tf, _ = scene.get_object(2)
+        tf[9:12] = [rng_t[0], 1.5 + rng_t[1], 1.0]
+        scene.set_object(2, tf, True)
+    if frame == 7:
+        scene.set_object(0, scene.get_object(0)[1], True)
+    if frame == 13:
+        scene.set_camera_dirty(True)
+
+
+@pytest.mark.parametrize("precision", [vx.VXA_FP64, vx.VXA_FP32])
+def test_hbo_transparency_and_reference_stats(gpu, precision):
+    s_hbo, o = hbo_pair()
+    s_plain, _ = hbo_pair()
+    hbo = vx.HitBuffer(96, 64)
+    rhbo = ref.RefHitBuffer(96, 64)
+    rng = np.random.default_rng(5)
+    reused_total = 0
+    for frame in range(25):
+        jit = rng.uniform(-0.05, 0.05, 2)
+        for sc in (s_hbo, s_plain, o):
+            mutate(sc, frame, jit)
+        a, _, sa = s_hbo.render(precision=precision, hbo=hbo)
+        b, _, sb = s_plain.render(precision=precision)
+        assert (a == b).all(), f"frame {frame}: hit buffer changed the image"
+        assert sa["rays"] == 96 * 64
+        reused_total += sa["pixels_reused"]
+        if precision == vx.VXA_FP64:
+            r_img, r_st = o.render(hbo=rhbo)
+            assert (a == r_img).all(), f"frame {frame}: differs from the reference"
+            for k in ("pixels_reused", "svo_traversals", "sphere_tests", "rays"):
+                assert sa[k] == r_st[k], (frame, k, sa[k], r_st[k])
+        for sc in (s_hbo, s_plain, o):
+            sc.mark_clean()
+    assert reused_total > 0
+
+
+def test_hbo_dimension_mismatch_raises(gpu):
+    s, _ = hbo_pair()
+    with pytest.raises(vx.VoxanimError, match="hit buffer dimensions"):
+        s.render(hbo=vx.HitBuffer(10, 10))
+
+
+def test_screen_partition_composes_the_same_frame(gpu):
+    """Ranks 0..world-1 rendering their super-tiles into one framebuffer (as the
+    NVLink peer-store path does across GPUs) reproduce the single-device frame."""
+    lib = vx.vxa()
+    model = vx.Model.procedural(8, shell=True)
+    s = vx.Scene(vx.config.C4, [model], 0, 1000, 600)
+    s.evaluate(0.7)
+    ctx = vx.context()
+    f, inst, n = s.export()
+    full = np.zeros((600, 1000, 3), np.uint8)
+    assert lib.vxa_render(ctx, C.byref(f), inst, n, full.ctypes.data, None, None) == 0
+    for world in (2, 3, 4, 8):
+        for rank in range(world):
+            f.tile_rank, f.tile_world = rank, world
+            assert lib.vxa_submit(ctx, C.byref(f), inst, n) == 0, lib.vxa_last_error()
+        part = np.zeros_like(full)
+        assert lib.vxa_read_framebuffer(ctx, part.ctypes.data, 1000, 600) == 0
+        assert (part == full).all(), f"world {world}"
+
+
+def test_stats_and_launch_counts(gpu):
+    model = vx.Model.procedural(8, shell=False)
+    s = vx.Scene(vx.config.C1, [model])
+    o = ref.RefScene(vx.config.C1, [ref.RefModel.from_bytes(model.serialize())])
+    _, _, st = s.render(precision=vx.VXA_FP64)
+    _, rst = o.render()
+    for k in ("rays", "sphere_tests", "svo_traversals", "pixels_reused"):
+        assert st[k] == rst[k], k
+    assert st["kernel_launches"] == 2  # frame kernel + RGB8 pack
+    assert st["gpu_ms"] > 0
+
+
+def test_invalid_arguments(gpu):
+    lib = vx.vxa()
+    ctx = vx.context()
+    f = _abi.vxa_frame_desc()
+    f.camera.width, f.camera.height, f.tile_world = 0, 10, 1
+    assert lib.vxa_render(ctx, C.byref(f), None, 0, None, None, None) == _abi.VXA_ERR_INVALID
+    f.camera.width, f.tile_world, f.tile_rank = 10, 2, 2
+    assert lib.vxa_render(ctx, C.byref(f), None, 0, None, None, None) == _abi.VXA_ERR_INVALID
+    # a model violating the SVO invariants (child_base <= parent) is refused
+    bad = (C.c_uint8 * 12)(0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0)
+    h = C.c_uint32()
+    assert lib.vxa_upload_model(ctx, bad, 1, None, 0, 1, C.byref(h)) == _abi.VXA_ERR_MODEL
+    # empty scene renders the background
+    s = vx.Scene(vx.config.TWO_OBJECTS, [vx.Model.random(3, 2, 0.0)])
+    img, _, st = s.render()
+    assert (img == np.array([10, 20, 30], np.uint8)).all()

@@ -1,0 +1,104 @@
+"""GPU parity: the CUDA frame against the reference CPU renderer (oracle/_ref).
+
+FP64 parity kernel: bit-exact image, hit object, leaf-parent node, attribute
+index, level, voxel and t for every pixel.
+FP32 production kernel: every pixel whose hit differs from the oracle must be
+a documented slab-test tie (oracle/ref_harness.cpp classify_pixel); where the
+hit agrees, t must be within 1e-6 relative (floor 1e-6 absolute) and RGB
+within +-1 LSB per channel.
+"""
+import numpy as np
+import pytest
+
+import paper_1911_06001_b200 as vx
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+T_REL = 1e-6
+
+
+def pair(cfg, models, seed=0, w=0, h=0):
+    """(product scene, oracle scene) built from the same models (oracle side via .svo bytes)."""
+    rmodels = [ref.RefModel.from_bytes(m.serialize()) for m in models]
+    s = vx.Scene(cfg, models, seed, w, h)
+    o = ref.RefScene(cfg, rmodels, seed, s.width, s.height)
+    return s, o
+
+
+def check_fp64(s, o, culling=True, sorting=True):
+    o_aov, o_rgb = o.dump(culling, sorting)
+    o_img, o_st = o.render(culling, sorting)
+    assert (o_rgb == o_img).all()
+    rgb, aov, st = s.render(culling, sorting, precision=vx.VXA_FP64, aov=True)
+    assert (rgb == o_img).all(), f"{int((rgb != o_img).any(axis=2).sum())} pixels differ"
+    for f in ("object_id", "node_index", "attr_index", "level", "entry_axis", "t", "kind", "traversals",
+              "node_fetches"):
+        bad = aov[f] != o_aov[f]
+        assert not bad.any(), f"{f}: {int(bad.sum())} pixels differ"
+    assert (aov["voxel"] == o_aov["voxel"]).all()
+    for k in ("rays", "sphere_tests", "svo_traversals", "pixels_reused"):
+        assert st[k] == o_st[k], k
+    return o_aov, o_img
+
+
+def check_fp32(s, o, o_aov, o_img, culling=True, sorting=True, max_tie_frac=5e-3):
+    rgb, aov, st = s.render(culling, sorting, precision=vx.VXA_FP32, aov=True)
+    cls = o.classify(o_aov, aov, T_REL)
+    n_hit = max(1, int((o_aov["object_id"] >= 0).sum()))
+    bugs = int((cls == ref.BUG).sum())
+    t_bad = int((cls == ref.T_OUT_OF_TOL).sum())
+    assert bugs == 0, f"{bugs} unexplained FP32 mismatches"
+    assert t_bad == 0, f"{t_bad} pixels with t outside {T_REL}"
+    ties = int((cls == ref.TIE).sum())
+    assert ties <= max_tie_frac * n_hit + 2, f"{ties} ties of {n_hit} hits"
+    same = cls == ref.MATCH
+    diff = np.abs(rgb.astype(int) - o_img.astype(int)).max(axis=2)
+    assert (diff[same] <= 1).all(), "RGB outside +-1 LSB on matching pixels"
+    return ties, n_hit
+
+
+def test_sorted_tracing_scene(gpu):
+    s, o = pair(vx.config.SORTED_TRACING, [vx.Model.full_cube()])
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img)
+
+
+def test_two_objects(gpu):
+    s, o = pair(vx.config.TWO_OBJECTS, [vx.Model.full_cube()])
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+def test_random_scenes_all_option_combinations(gpu, seed):
+    models = [vx.Model.random(100 * seed + k, 2 + (k % 3), 0.3) for k in range(6)]
+    s, o = pair(vx.config.RANDOM, models, seed)
+    for culling in (True, False):
+        for sorting in (True, False):
+            o_aov, o_img = check_fp64(s, o, culling, sorting)
+            check_fp32(s, o, o_aov, o_img, culling, sorting)
+
+
+def test_c1_full_size(gpu):
+    s, o = pair(vx.config.C1, [vx.Model.procedural(8, shell=False)])
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img)
+
+
+@pytest.mark.parametrize("t", [0.0, 0.5, 1.3, 2.9])
+def test_c2_animated_frames_reduced(gpu, t):
+    s, o = pair(vx.config.C2, [vx.Model.procedural(10, shell=True)], w=480, h=270)
+    s.evaluate(t)
+    o.evaluate(t)
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img)
+
+
+def test_c4_reduced(gpu):
+    s, o = pair(vx.config.C4, [vx.Model.procedural(11, shell=True)], w=640, h=360)
+    for t in (0.0, 1.7):
+        s.evaluate(t)
+        o.evaluate(t)
+        o_aov, o_img = check_fp64(s, o)
+        check_fp32(s, o, o_aov, o_img)
