@@ -170,6 +170,12 @@ int vxa_stats_reset(vxa_ctx* ctx);
 /* Copies the resident RGBA8 framebuffer to host RGB8 (width*height*3). */
 int vxa_read_framebuffer(vxa_ctx* ctx, uint8_t* rgb_out, int32_t width, int32_t height);
 
+/* Page-locks a caller-owned host buffer (cudaHostRegister) so image / AOV
+ * reads into it run as asynchronous DMA at full PCIe rate; unregister before
+ * freeing the memory. */
+int vxa_host_register(vxa_ctx* ctx, void* ptr, size_t bytes);
+int vxa_host_unregister(vxa_ctx* ctx, void* ptr);
+
 /* Timing helpers on the context stream (CUDA events). */
 int vxa_timer_begin(vxa_ctx* ctx);
 int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms);

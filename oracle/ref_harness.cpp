@@ -311,11 +311,19 @@ int classify_pixel(const Scene& scene, const Ray& ray, const AovRec& o, const Ao
     if (!ho && !hg) return 0;
     if (ho && hg && o.object_id == g.object_id && o.voxel[0] == g.voxel[0] && o.voxel[1] == g.voxel[1] &&
         o.voxel[2] == g.voxel[2] && o.level == g.level && o.node_index == g.node_index && o.attr_index == g.attr_index) {
-        const double tol = t_rel * std::max(1.0, std::abs(o.t));
+        // FP32 t tolerance: t_rel relative, plus the FP32 resolution of the entry
+        // plane's position (cell size and origin rounded to 2^-24 relative)
+        // divided by the incidence |d_a| -- a grazing entry is ill-conditioned.
+        const SceneObject* obj = scene.find_object(o.object_id);
+        const Ray loc = transform_ray_world_to_local(ray, obj->transform);
+        const int ax = o.entry_axis;
+        const double da = std::abs(loc.direction[ax]);
+        const double ha = bounds_from_scale(obj->transform.scale).half_extent[ax];
+        double tol = t_rel * std::max(1.0, std::abs(o.t));
+        if (da > 0.0) tol += std::ldexp(std::abs(loc.origin[ax]) + 2.0 * ha, -22) / da;
         if (std::abs(o.t - g.t) > tol) return 3;
         if (o.entry_axis == g.entry_axis) return 0;
         // same voxel entered through a different face: an edge/corner entry tie
-        const SceneObject* obj = scene.find_object(o.object_id);
         const Interval iv = voxel_interval(*obj, ray, o.voxel, o.level);
         return std::abs(iv.axis_in[o.entry_axis] - iv.axis_in[g.entry_axis]) <= tau(o.t) ? 1 : 2;
     }

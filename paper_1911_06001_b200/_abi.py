@@ -161,7 +161,7 @@ VXA_SYMBOLS = [
     "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
     "vxa_upload_model", "vxa_release_model", "vxa_model_info",
     "vxa_render", "vxa_submit", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
-    "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
+    "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
     "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_traverse",
 ]
 VXN_SYMBOLS = [
@@ -202,6 +202,8 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_stats_read", i, P, C.POINTER(vxa_stats))
     _declare(lib, "vxa_stats_reset", i, P)
     _declare(lib, "vxa_read_framebuffer", i, P, P, C.c_int32, C.c_int32)
+    _declare(lib, "vxa_host_register", i, P, P, C.c_size_t)
+    _declare(lib, "vxa_host_unregister", i, P, P)
     _declare(lib, "vxa_timer_begin", i, P)
     _declare(lib, "vxa_timer_end", i, P, C.POINTER(d))
     _declare(lib, "vxa_flush_l2", i, P)

@@ -664,6 +664,20 @@ int vxa_read_framebuffer(vxa_ctx* ctx, uint8_t* rgb_out, int32_t width, int32_t 
     return VXA_OK;
 }
 
+int vxa_host_register(vxa_ctx* ctx, void* ptr, size_t bytes) {
+    if (ctx == nullptr || ptr == nullptr || bytes == 0) return fail(VXA_ERR_INVALID, "null argument");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    VXA_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+    return VXA_OK;
+}
+
+int vxa_host_unregister(vxa_ctx* ctx, void* ptr) {
+    if (ctx == nullptr || ptr == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    VXA_CUDA(cudaHostUnregister(ptr));
+    return VXA_OK;
+}
+
 int vxa_timer_begin(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     VXA_CUDA(cudaEventRecord(ctx->t_a, ctx->stream));
