@@ -23,7 +23,7 @@ constexpr int kBlock = 128;
 // Minimum resident blocks per SM requested from ptxas for the FP32 kernel
 // (register budget 65536 / (128 * n)); tuned by measurement.
 #ifndef VXA_MIN_BLOCKS
-#define VXA_MIN_BLOCKS 1
+#define VXA_MIN_BLOCKS 8
 #endif
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
@@ -161,7 +161,7 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         for (int k = 0; k < 3; ++k)
             d[k] = static_cast<float>((fma(in.Md[3 * k], dcx, in.Md[3 * k + 1] * dcy) - in.Md[3 * k + 2]) * rd.rnd);
         FastRay fr;
-        if (!fast_setup(fr, d, in.A_lo, in.A_hi, in.Ar_lo, in.Ar_hi, in.h2, in.zflags, in.zbits)) return;
+        if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits)) return;
         FastHit h;
         const bool hit = traverse_fast<kAov>(in.model, fr, h, stack, kBlock);
         fetches += h.fetches;

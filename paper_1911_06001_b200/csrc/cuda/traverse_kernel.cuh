@@ -66,14 +66,17 @@ __global__ void __launch_bounds__(128) traverse_kernel(DevModel m, const Travers
         FastRay r;
         hit = false;
         o.node_fetches = 0;
-        float Ar_lo[3], Ar_hi[3];
+        float U_lo[3], U_hi[3], Ur_lo[3], Ur_hi[3];
         for (int a = 0; a < 3; ++a) {
             const double o = in.origin[a], h = in.half_extent[a];
-            Ar_lo[a] = static_cast<float>((-h - o) - static_cast<double>(A_lo[a]));
-            Ar_hi[a] = static_cast<float>((h - o) - static_cast<double>(A_hi[a]));
+            const double ulo = (-h - o) / (2.0 * h), uhi = (h - o) / (2.0 * h);
+            U_lo[a] = static_cast<float>(ulo);
+            U_hi[a] = static_cast<float>(uhi);
+            Ur_lo[a] = static_cast<float>(ulo - static_cast<double>(U_lo[a]));
+            Ur_hi[a] = static_cast<float>(uhi - static_cast<double>(U_hi[a]));
         }
         uint2 lstack[kMaxDepth];
-        if (fast_setup(r, d, A_lo, A_hi, Ar_lo, Ar_hi, h2, zf, zb)) {
+        if (fast_setup(r, d, U_lo, U_hi, Ur_lo, Ur_hi, h2, zf, zb)) {
             FastHit h;
             hit = traverse_fast<true>(m, r, h, lstack, 1);
             o.node_fetches = h.fetches;

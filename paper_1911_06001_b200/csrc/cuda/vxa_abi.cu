@@ -56,7 +56,8 @@ __global__ void repack_nodes(const uint32_t* __restrict__ raw, uint32_t n, uint2
     w.x = valid | (leaf << 8) | ((internal && leaves) ? kMixed : 0u);
     w.y = internal ? child_base : attr_base;
     words[i] = w;
-    if (side != nullptr) side[i] = attr_base;
+    // child_base is unique among nodes with internal children
+    if (side != nullptr && internal && leaves) side[child_base] = attr_base;
 }
 
 // RGBA8 framebuffer -> RGB8 (four pixels per thread: 16 B in, 12 B out).
@@ -206,9 +207,12 @@ int build_instances(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* i
             d.A_lo[a] = static_cast<Real>(-h[a] - ol[a]);
             d.A_hi[a] = static_cast<Real>(h[a] - ol[a]);
             d.h2[a] = static_cast<Real>(2.0 * h[a]);
-            const double alo = -h[a] - ol[a], ahi = h[a] - ol[a];
-            d.Ar_lo[a] = static_cast<float>(alo - static_cast<double>(static_cast<float>(alo)));
-            d.Ar_hi[a] = static_cast<float>(ahi - static_cast<double>(static_cast<float>(ahi)));
+            // FP32 kernel: unit-cube plane offsets (-h - o) / 2h, (h - o) / 2h + residuals
+            const double ulo = (-h[a] - ol[a]) / (2.0 * h[a]), uhi = (h[a] - ol[a]) / (2.0 * h[a]);
+            d.U_lo[a] = static_cast<float>(ulo);
+            d.U_hi[a] = static_cast<float>(uhi);
+            d.Ur_lo[a] = static_cast<float>(ulo - static_cast<double>(d.U_lo[a]));
+            d.Ur_hi[a] = static_cast<float>(uhi - static_cast<double>(d.U_hi[a]));
             d.zbits[a] = zero_dir_bits(ol[a], h[a]);
             if (-h[a] > ol[a]) d.zflags |= 1u << a;
             if (h[a] > ol[a]) d.zflags |= 1u << (3 + a);

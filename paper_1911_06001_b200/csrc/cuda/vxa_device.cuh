@@ -19,7 +19,8 @@
 //   words : uint2 per node  {x = valid | leaf << 8 | kMixed, y = base}
 //           base = child_base when the node has internal children, else
 //           attr_base; kMixed marks the rare node with both kinds, whose
-//           attr_base then lives in side[node].
+//           attr_base then lives in side[child_base] (child_base is unique
+//           among nodes with internal children).
 //   attrs : uint32 RGBA8 per attribute.
 #pragma once
 
@@ -67,7 +68,8 @@ template <typename Real> struct DevInstance {
     Real A_lo[3]; // -h - o_local  (o_local = R^T (cam - t), FP64)
     Real A_hi[3]; //  h - o_local
     Real h2[3];   // 2h (root cell size)
-    float Ar_lo[3], Ar_hi[3]; // FP32 kernel: FP64 rounding residuals of A_lo / A_hi
+    float U_lo[3], U_hi[3];   // FP32 kernel: (-h - o) / 2h, (h - o) / 2h (unit-cube plane offsets)
+    float Ur_lo[3], Ur_hi[3]; // and their FP64 rounding residuals
     double Md[9]; // FP64 R^T C (camera -> local), FP32 kernel's local direction
     uint32_t zbits[3]; // zero-direction path: bit L set iff o >= centre at level L
     uint32_t zflags;   // bit a: (-h > o); bit 3+a: (h > o)   (zero-direction slab signs)
@@ -323,7 +325,7 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
         log.visit(static_cast<double>(t_enter), static_cast<uint32_t>(level + 1), is_leaf);
         path = (path & ~(0xfull << (4 * level))) | (static_cast<unsigned long long>(oct) << (4 * level));
         if (is_leaf) {
-            const uint32_t abase = (fw.x & kMixed) ? __ldg(m.side + fidx) : fw.y;
+            const uint32_t abase = (fw.x & kMixed) ? __ldg(m.side + fw.y) : fw.y;
             out.attr = abase + popc8_below(valid & leafm, bit);
             out.t = t_enter < Real(0) ? Real(0) : t_enter;
             out.parent = fidx;
@@ -373,11 +375,12 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
 // coordinates on a pop instead of being stored.
 
 struct FastRay {
-    float A[3];     // -h - o_m (mirrored frame), rounded
-    float Ar[3];    // its FP64 rounding residual (A + Ar == -h - o_m to ~2^-48)
-    float inv_d[3]; // 1 / |d|
-    float s0[3];    // root cell size 2h
-    float d[3];     // unmirrored local direction (normal sign)
+    // Unit-cube form of each mirrored axis: positions are measured in root
+    // cells (x' = (x + h) / 2h), so node planes sit at exact dyadic positions
+    // c * 2^-L and the scale 2h only multiplies t (folded into inv).
+    float A[3];   // (-h - o_m) / 2h, rounded
+    float Ar[3];  // its FP64 rounding residual
+    float inv[3]; // 2h / |d|
     uint32_t mirror, zero;
     uint32_t zbits[3];
 };
@@ -389,41 +392,33 @@ struct FastHit {
     uint32_t fetches;
 };
 
-// t of the plane at integer position i (cell size s) of one mirrored axis.
-// (i s + A) is exact inside the FMA; adding the residual keeps the plane
-// offset accurate when it cancels against A (a plane close to the origin).
-__device__ __forceinline__ float plane_t(float i, float s, float A, float Ar, float inv) {
-    return __fmul_rn(__fadd_rn(__fmaf_rn(i, s, A), Ar), inv);
+// t of the plane at position i * sz (i integer-valued, sz = 2^-L) of one
+// mirrored axis: i * sz + A is exact inside the FMA up to one rounding; the
+// residual keeps it accurate when it cancels (a plane close to the origin).
+// Every plane gets one value whatever the level that computes it, so sibling
+// cells share planes bit for bit (the traversal is watertight).
+__device__ __forceinline__ float plane_t(float i, float sz, float A, float Ar, float inv) {
+    return __fmul_rn(__fadd_rn(__fmaf_rn(i, sz, A), Ar), inv);
 }
 
 __device__ __forceinline__ float zero_mid(const FastRay& r, int a, int level) {
     return ((r.zbits[a] >> level) & 1u) ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
 }
 
-// t0 / tm / t1 of the node with (float, exact) cell coordinates c at size s.
-__device__ __forceinline__ void node_planes(const FastRay& r, const float c[3], const float s[3], int level,
-                                            float t0[3], float tm[3], float t1[3]) {
+__device__ __forceinline__ void fix_zero_axes(const FastRay& r, int level, float t0[3], float tm[3], float t1[3]) {
+    const float inf = __int_as_float(0x7f800000);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        t0[a] = plane_t(c[a], s[a], r.A[a], r.Ar[a], r.inv_d[a]);
-        t1[a] = plane_t(c[a] + 1.0f, s[a], r.A[a], r.Ar[a], r.inv_d[a]);
-        tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * s[a], r.A[a], r.Ar[a], r.inv_d[a]);
-    }
-    if (r.zero) {
-        const float inf = __int_as_float(0x7f800000);
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-            if (r.zero & axis_bit(a)) {
-                t0[a] = -inf;
-                t1[a] = inf;
-                tm[a] = zero_mid(r, a, level);
-            }
-    }
+    for (int a = 0; a < 3; ++a)
+        if (r.zero & axis_bit(a)) {
+            t0[a] = -inf;
+            t1[a] = inf;
+            tm[a] = zero_mid(r, a, level);
+        }
 }
 
-// Root setup from the FP32-rounded local direction and host-folded offsets
-// (A_* rounded, Ar_* residuals). Returns false when the ray misses the root
-// box (traversal.cpp:56-60).
+// Root setup. d: FP32-rounded local direction; A_lo/A_hi (+ residuals):
+// (-h - o) / 2h and (h - o) / 2h folded on the host in FP64; h2 = 2h.
+// Returns false when the ray misses the root box (traversal.cpp:56-60).
 __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const float A_lo[3], const float A_hi[3],
                                            const float Ar_lo[3], const float Ar_hi[3], const float h2[3],
                                            uint32_t zflags, const uint32_t zbits[3]) {
@@ -433,14 +428,12 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
     float te = -inf, tx = inf;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        r.d[a] = d[a];
         r.zbits[a] = zbits[a];
-        r.s0[a] = h2[a];
         if (d[a] == 0.0f) {
             r.zero |= axis_bit(a);
             r.A[a] = 0.0f;
             r.Ar[a] = 0.0f;
-            r.inv_d[a] = 0.0f;
+            r.inv[a] = 0.0f;
             // zero-direction slab convention: inside iff -h <= o < h
             if ((zflags >> a) & 1u) te = inf;
             if (!((zflags >> (3 + a)) & 1u)) tx = -inf;
@@ -449,25 +442,32 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
             if (m) r.mirror |= axis_bit(a);
             r.A[a] = m ? -A_hi[a] : A_lo[a];
             r.Ar[a] = m ? -Ar_hi[a] : Ar_lo[a];
-            r.inv_d[a] = __frcp_rn(fabsf(d[a]));
-            te = fmaxf(te, plane_t(0.0f, h2[a], r.A[a], r.Ar[a], r.inv_d[a]));
-            tx = fminf(tx, plane_t(1.0f, h2[a], r.A[a], r.Ar[a], r.inv_d[a]));
+            r.inv[a] = __fdiv_rn(h2[a], fabsf(d[a]));
+            te = fmaxf(te, plane_t(0.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
+            tx = fminf(tx, plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
         }
     }
     return !(te >= tx || tx < 0.0f);
 }
 
-// Stack of ancestor node words (bits 24..27 of .x: the saved next octant).
-// kSmemStack: one column per thread in shared memory ([level][thread]:
-// conflict-free whatever the per-lane levels); else a local array.
+// Iterative traversal. The explicit stack holds only ancestor node words
+// (bits 24..27 of .x: the saved next octant) in the caller's stack column
+// (shared memory, [level][thread]); t0/tm/t1 of a parent are rebuilt on a
+// pop from the child's interval plus one plane per axis.
 template <bool kTrackIdx>
 __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out, uint2* __restrict__ stack,
                               uint32_t stride) {
-    uint32_t sidx[kMaxDepth]; // ancestor indices, kept only for AOVs / models with mixed nodes
-    float c[3] = {0.0f, 0.0f, 0.0f};
-    float s[3] = {r.s0[0], r.s0[1], r.s0[2]};
+    uint32_t sidx[kTrackIdx ? kMaxDepth : 1]; // ancestor indices (AOV: leaf parent)
+    float c[3] = {0.0f, 0.0f, 0.0f};          // cell coordinates (exact integers)
+    float sz = 1.0f;                          // cell size 2^-level
     float t0[3], tm[3], t1[3];
-    node_planes(r, c, s, 0, t0, tm, t1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        t0[a] = plane_t(0.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]);
+        t1[a] = plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]);
+        tm[a] = plane_t(1.0f, 0.5f, r.A[a], r.Ar[a], r.inv[a]);
+    }
+    if (r.zero) fix_zero_axes(r, 0, t0, tm, t1);
     uint2 fw = load_node(m, 0);
     uint32_t fidx = 0, fetches = 1;
     uint32_t fcur = first_child(t0, tm);
@@ -481,13 +481,22 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
             fw = stack[level * stride];
             fcur = (fw.x >> 24) & 0xfu;
             fw.x &= 0x00ffffffu;
-            if (kTrackIdx || m.side != nullptr) fidx = sidx[level];
+            if constexpr (kTrackIdx) fidx = sidx[level];
+            sz = 2.0f * sz;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                c[a] = floorf(0.5f * c[a]);
-                s[a] = 2.0f * s[a];
+                const float cp = floorf(0.5f * c[a]);
+                const bool upper = c[a] != 2.0f * cp; // the child was the upper half
+                c[a] = cp;
+                if (upper) {
+                    tm[a] = t0[a];
+                    t0[a] = plane_t(cp, sz, r.A[a], r.Ar[a], r.inv[a]);
+                } else {
+                    tm[a] = t1[a];
+                    t1[a] = plane_t(cp + 1.0f, sz, r.A[a], r.Ar[a], r.inv[a]);
+                }
             }
-            node_planes(r, c, s, level, t0, tm, t1);
+            if (r.zero) fix_zero_axes(r, level, t0, tm, t1);
             continue;
         }
         const uint32_t q = fcur;
@@ -518,8 +527,8 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         const uint32_t leafm = (fw.x >> 8) & 0xffu;
         if (!(valid & bit)) continue;
         if (leafm & bit) {
-            uint32_t abase = fw.y;
-            if (fw.x & kMixed) abase = __ldg(m.side + fidx);
+            // mixed nodes keep attr_base in side[child_base] (vxa_abi.cu repack)
+            const uint32_t abase = (fw.x & kMixed) ? __ldg(m.side + fw.y) : fw.y;
             out.attr = abase + popc8_below(valid & leafm, bit);
             out.t = fmaxf(t_enter, 0.0f);
             out.parent = fidx;
@@ -537,18 +546,20 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         if (level + 1 >= depth) continue;
         const uint32_t child = fw.y + popc8_below(valid & ~leafm, bit);
         stack[level * stride] = make_uint2(fw.x | (fcur << 24), fw.y);
-        if (kTrackIdx || m.side != nullptr) sidx[level] = fidx;
+        if constexpr (kTrackIdx) {
+            sidx[level] = fidx;
+            fidx = child;
+        }
         ++level;
-        fidx = child; // kept for mixed nodes (side array) and AOVs
         fw = load_node(m, child);
         ++fetches;
+        sz = 0.5f * sz;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             c[a] = __fmaf_rn(2.0f, c[a], static_cast<float>((q >> (2 - a)) & 1u));
-            s[a] = 0.5f * s[a];
             t0[a] = c0[a];
             t1[a] = c1[a];
-            tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * s[a], r.A[a], r.Ar[a], r.inv_d[a]);
+            tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
         }
         if (r.zero) {
 #pragma unroll
