@@ -105,6 +105,10 @@ template <typename Real> struct FrameParams {
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
     void* aov;                    // vxa_pixel_aov* or null
     void* hbo;                    // vxa_hit_record* (device copy) or null
+    // overflow list: pixels the fast kernel hands to the generic kernel
+    uint32_t* ovf_list;
+    uint32_t* ovf_count;
+    uint32_t ovf_mode; // generic kernel: 1 = render only the listed pixels
 };
 
 // Host-layout records written by the kernel (match include/vxa.h).
