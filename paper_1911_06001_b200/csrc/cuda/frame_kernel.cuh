@@ -221,29 +221,18 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
-        int tx0 = 0, ty0 = 0, px, py;
-        if (p.ovf_mode) {
-            // second pass over the pixels the fast kernel deferred (frame_fast.cuh)
-            const uint32_t count = *p.ovf_count;
-            if (tile * 32u >= count) break;
-            const uint32_t k = tile * 32u + lane;
-            const uint32_t pixel = k < count ? p.ovf_list[k] : 0xffffffffu;
-            px = pixel == 0xffffffffu ? p.width : static_cast<int>(pixel % static_cast<uint32_t>(p.width));
-            py = pixel == 0xffffffffu ? p.height : static_cast<int>(pixel / static_cast<uint32_t>(p.width));
-        } else {
-            if (tile >= p.n_tiles) break;
-            const uint32_t st = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
-            const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
-            tx0 = static_cast<int>((s % p.n_super_x) * kSuper + (wt % (kSuper / kTileW)) * kTileW);
-            ty0 = static_cast<int>((s / p.n_super_x) * kSuper + (wt / (kSuper / kTileW)) * kTileH);
-            px = tx0 + static_cast<int>(lane % kTileW);
-            py = ty0 + static_cast<int>(lane / kTileW);
-        }
+        if (tile >= p.n_tiles) break;
+        const uint32_t st = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
+        const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
+        const int tx0 = static_cast<int>((s % p.n_super_x) * kSuper + (wt % (kSuper / kTileW)) * kTileW);
+        const int ty0 = static_cast<int>((s / p.n_super_x) * kSuper + (wt / (kSuper / kTileW)) * kTileH);
+        const int px = tx0 + static_cast<int>(lane % kTileW);
+        const int py = ty0 + static_cast<int>(lane / kTileW);
 
         // ---- tile candidate list (FP32 production kernel with culling)
         uint32_t list_n = 0xffffffffu; // 0xffffffff: per-ray pass over every instance
         if constexpr (sizeof(Real) == 4) {
-            if (p.culling && n <= 0xffffu && !p.ovf_mode) {
+            if (p.culling && n <= 0xffffu) {
                 const TileCone cone = tile_cone(p, tx0, ty0);
                 uint32_t cnt = 0;
                 for (uint32_t base = 0; base < n; base += 32) {

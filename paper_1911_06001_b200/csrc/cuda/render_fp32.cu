@@ -1,6 +1,6 @@
 // Production FP32 instantiation of the frame and traversal kernels
 // (compiled with FMA contraction enabled: -fmad=true).
-#include "frame_fast.cuh"
+#include "frame_kernel.cuh"
 #include "traverse_kernel.cuh"
 
 namespace vxa {
@@ -20,26 +20,6 @@ cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, co
 
 size_t frame_smem_bytes_f32(uint32_t max_depth) {
     return sizeof(uint2) * kBlock * (max_depth > 0 ? max_depth : 1);
-}
-
-namespace {
-void* fast_fn(bool aov) {
-    return aov ? reinterpret_cast<void*>(&frame_kernel_fast<true>) : reinterpret_cast<void*>(&frame_kernel_fast<false>);
-}
-} // namespace
-
-cudaError_t launch_frame_fast_f32(const FrameParams<float>& p, bool aov, const FrameLaunch& l) {
-    void* args[] = {const_cast<FrameParams<float>*>(&p)};
-    return cudaLaunchKernel(fast_fn(aov), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f32(p.max_depth), l.stream);
-}
-
-int frame_fast_blocks_per_sm_f32(bool aov, uint32_t max_depth) {
-    int b = 0;
-    void* fn = fast_fn(aov);
-    const size_t smem = frame_smem_bytes_f32(max_depth);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, smem) != cudaSuccess) return 1;
-    return b > 0 ? b : 1;
 }
 
 int frame_blocks_per_sm_f32(bool aov, bool hbo, uint32_t max_depth) {

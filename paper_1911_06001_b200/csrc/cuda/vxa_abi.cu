@@ -126,9 +126,7 @@ struct vxa_ctx {
     uint32_t* peer_fb = nullptr; // rank 0's framebuffer mapped via CUDA IPC
     int32_t peer_w = 0, peer_h = 0;
 
-    DevBuf<uint32_t> tile_counter; // [0] frame tiles, [1] overflow tiles, [2] overflow pixel count
-    DevBuf<uint32_t> ovf_list;
-    int fast_kernel = -1;          // production kernel enabled (VOXANIM_KERNEL=generic disables)
+    DevBuf<uint32_t> tile_counter;
     DevBuf<unsigned long long> counters;
     DevBuf<unsigned char> inst_dev;
     unsigned char* inst_host[2] = {nullptr, nullptr};
@@ -146,7 +144,6 @@ struct vxa_ctx {
 
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, t_a = nullptr, t_b = nullptr;
     int occ[2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][stack height]
-    int occ_fast[2][kMaxDepth + 1] = {};  // production kernel [aov][stack height]
 
     // Frame-kernel timing ring: events recorded tight around every frame
     // kernel launch; vxa_stats_read sums them (gpu_ms) since the last reset.
@@ -154,7 +151,6 @@ struct vxa_ctx {
     cudaEvent_t k_begin[kRing] = {}, k_end[kRing] = {};
     int k_count = 0;
     uint64_t h2d = 0, d2h = 0; // bytes copied since the last reset
-    uint64_t extra_kernels = 0;  // overflow passes launched since the last reset
     uint64_t n_rays = 0, n_sphere_tests = 0; // host-counted (pixels rendered x objects tested)
 };
 
@@ -348,22 +344,12 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     if (bytes) VXA_CUDA(cudaMemcpyAsync(ctx->inst_dev.ptr, ctx->inst_host[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
     ctx->h2d += bytes;
     VXA_CUDA(cudaEventRecord(ctx->inst_done[slot], ctx->stream));
-    VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, 3 * sizeof(uint32_t), ctx->stream));
+    VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, sizeof(uint32_t), ctx->stream));
     if (reset_counters) VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
 
     const bool is64 = sizeof(Real) == 8;
     const bool a = aov != nullptr, h = hbo != nullptr;
-    if (ctx->fast_kernel < 0) {
-        const char* env = std::getenv("VOXANIM_KERNEL");
-        ctx->fast_kernel = (env && std::strcmp(env, "generic") == 0) ? 0 : 1;
-    }
-    // production FP32 path: persistent lane-refill kernel + overflow pass
-    const bool fast = !is64 && p.culling && !h && ctx->fast_kernel == 1;
-    p.ovf_count = ctx->tile_counter.ptr + 2;
-    if (fast) {
-        VXA_CUDA(ctx->ovf_list.ensure(static_cast<size_t>(W) * H));
-        p.ovf_list = ctx->ovf_list.ptr;
-    }
+
     int& occ = ctx->occ[is64][a][h][p.max_depth];
     if (occ == 0) occ = is64 ? frame_blocks_per_sm_f64(a, h, p.max_depth) : frame_blocks_per_sm_f32(a, h, p.max_depth);
     FrameLaunch l{ctx->sm_count * occ, ctx->stream};
@@ -374,22 +360,10 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     }
     VXA_CUDA(cudaEventRecord(ctx->k_begin[slot_k], ctx->stream));
     cudaError_t e;
-    if constexpr (sizeof(Real) == 8) {
+    if constexpr (sizeof(Real) == 8)
         e = launch_frame_f64(p, a, h, l);
-    } else if (fast) {
-        int& occ_fast = ctx->occ_fast[a][p.max_depth];
-        if (occ_fast == 0) occ_fast = frame_fast_blocks_per_sm_f32(a, p.max_depth);
-        e = launch_frame_fast_f32(p, a, FrameLaunch{ctx->sm_count * occ_fast, ctx->stream});
-        if (e == cudaSuccess) {
-            FrameParams<Real> q = p; // overflow pass: generic kernel over the deferred pixels
-            q.ovf_mode = 1;
-            q.tile_counter = ctx->tile_counter.ptr + 1;
-            e = launch_frame_f32(q, a, h, l);
-            ++ctx->extra_kernels;
-        }
-    } else {
+    else
         e = launch_frame_f32(p, a, h, l);
-    }
     if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
     VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
     ++ctx->k_count;
@@ -421,7 +395,7 @@ int read_counters(vxa_ctx* ctx, vxa_stats* s) {
         total += ms;
     }
     s->gpu_ms = total;
-    s->kernel_launches = static_cast<uint64_t>(ctx->k_count) + ctx->extra_kernels;
+    s->kernel_launches = static_cast<uint64_t>(ctx->k_count);
     s->h2d_bytes = ctx->h2d;
     s->d2h_bytes = ctx->d2h + sizeof(c);
     return VXA_OK;
@@ -460,7 +434,7 @@ int vxa_create(int device, vxa_ctx** out) {
     ctx->sm_count = prop.multiProcessorCount;
     std::snprintf(ctx->name, sizeof(ctx->name), "%s", prop.name);
     VXA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    VXA_CUDA(ctx->tile_counter.ensure(4));
+    VXA_CUDA(ctx->tile_counter.ensure(1));
     VXA_CUDA(ctx->counters.ensure(8));
     VXA_CUDA(cudaMemset(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long)));
     for (int s = 0; s < 2; ++s) {
@@ -487,7 +461,6 @@ int vxa_destroy(vxa_ctx* ctx) {
     if (ctx->peer_fb) cudaIpcCloseMemHandle(ctx->peer_fb);
     ctx->fb.release();
     ctx->tile_counter.release();
-    ctx->ovf_list.release();
     ctx->counters.release();
     ctx->inst_dev.release();
     ctx->aov.release();
@@ -623,12 +596,11 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     }
     ctx->k_count = 0;
     ctx->h2d = ctx->d2h = 0;
-    ctx->extra_kernels = 0;
     ctx->n_rays = ctx->n_sphere_tests = 0;
     VXA_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
     if (int rc = enqueue_any(ctx, f, in, n, aov, hbo, true); rc != VXA_OK) return rc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
-    uint64_t launches = 1 + ctx->extra_kernels;
+    uint64_t launches = 1;
     if (rgb_out) {
         VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
         const size_t quads = (npix + 3) / 4;
@@ -680,7 +652,6 @@ int vxa_stats_reset(vxa_ctx* ctx) {
     VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
     ctx->k_count = 0;
     ctx->h2d = ctx->d2h = 0;
-    ctx->extra_kernels = 0;
     ctx->n_rays = ctx->n_sphere_tests = 0;
     return VXA_OK;
 }

@@ -105,10 +105,6 @@ template <typename Real> struct FrameParams {
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
     void* aov;                    // vxa_pixel_aov* or null
     void* hbo;                    // vxa_hit_record* (device copy) or null
-    // overflow list: pixels the fast kernel hands to the generic kernel
-    uint32_t* ovf_list;
-    uint32_t* ovf_count;
-    uint32_t ovf_mode; // generic kernel: 1 = render only the listed pixels
 };
 
 // Host-layout records written by the kernel (match include/vxa.h).
@@ -479,8 +475,14 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
     const int depth = min(static_cast<int>(m.depth), static_cast<int>(kMaxDepth));
 
     while (true) {
-        if (fcur == kExit) {
-            if (level == 0) break;
+        // Pops run in the same iteration as the next child step (instead of an
+        // iteration of their own), so lanes that pop and lanes that step do not
+        // serialise two loop bodies.
+        while (fcur == kExit) {
+            if (level == 0) {
+                out.fetches = fetches;
+                return false;
+            }
             --level;
             fw = stack[level * stride];
             fcur = (fw.x >> 24) & 0xfu;
@@ -501,7 +503,6 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
                 }
             }
             if (r.zero) fix_zero_axes(r, level, t0, tm, t1);
-            continue;
         }
         const uint32_t q = fcur;
         float c0[3], c1[3];
@@ -572,8 +573,6 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         }
         fcur = first_child(t0, tm);
     }
-    out.fetches = fetches;
-    return false;
 }
 
 // Voxel coordinates of a hit path (leaf_path_to_voxel, traversal.cpp:260-268).

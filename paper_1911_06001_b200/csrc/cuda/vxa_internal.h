@@ -38,9 +38,7 @@ cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, c
 int frame_blocks_per_sm_f32(bool aov, bool hbo, uint32_t max_depth);
 int frame_blocks_per_sm_f64(bool aov, bool hbo, uint32_t max_depth);
 size_t frame_smem_bytes_f32(uint32_t max_depth);
-// production FP32 kernel (culling on, no hit buffer) + its overflow pass
-cudaError_t launch_frame_fast_f32(const FrameParams<float>& p, bool aov, const FrameLaunch& l);
-int frame_fast_blocks_per_sm_f32(bool aov, uint32_t max_depth);
+
 size_t frame_smem_bytes_f64(uint32_t max_depth);
 
 struct TraverseRayIn {

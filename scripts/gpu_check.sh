@@ -6,7 +6,7 @@ set -x
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 900 python -m pytest tests -m gpu -q --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
 timeout 300 python bench.py --steps 200 --warmup 10 > gpurun_out/bench.log 2>&1; echo bench=$?
-for v in paper_1911_06001_b200/lib_[vf]*; do
+for v in paper_1911_06001_b200/lib_v*; do
   [ -d "$v" ] || continue
   VOXANIM_LIB_DIR=$PWD/$v timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_$(basename $v).log 2>&1
 done
