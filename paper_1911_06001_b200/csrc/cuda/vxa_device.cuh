@@ -475,14 +475,8 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
     const int depth = min(static_cast<int>(m.depth), static_cast<int>(kMaxDepth));
 
     while (true) {
-        // Pops run in the same iteration as the next child step (instead of an
-        // iteration of their own), so lanes that pop and lanes that step do not
-        // serialise two loop bodies.
-        while (fcur == kExit) {
-            if (level == 0) {
-                out.fetches = fetches;
-                return false;
-            }
+        if (fcur == kExit) {
+            if (level == 0) break;
             --level;
             fw = stack[level * stride];
             fcur = (fw.x >> 24) & 0xfu;
@@ -503,6 +497,7 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
                 }
             }
             if (r.zero) fix_zero_axes(r, level, t0, tm, t1);
+            continue;
         }
         const uint32_t q = fcur;
         float c0[3], c1[3];
@@ -573,6 +568,8 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         }
         fcur = first_child(t0, tm);
     }
+    out.fetches = fetches;
+    return false;
 }
 
 // Voxel coordinates of a hit path (leaf_path_to_voxel, traversal.cpp:260-268).
