@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3 animated-vs-static side measurements")
     return ap.parse_args()
 
 
@@ -347,6 +348,32 @@ def run_ours(args):
                "path": "evaluate_animation + voxanim::gpu::render_frame_into -> vxa_render: instance table "
                        "H2D from pinned staging, frame kernel, RGB8 pack, D2H into a page-locked host image"}
 
+    # side measurements: animated vs static at 1080p (configs C2 / C3)
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = {}
+        m10 = vx.Model.procedural(10, shell=True)
+        for name, cfg, anim in (("c2_animated_1080p", 2, True), ("c3_static_1080p", 3, False)):
+            sc = vx.Scene(cfg, [m10])
+            for k in range(5):
+                vxl.vxn_scene_submit(sc._h, frame_time(k, anim), prec, 0, 1)
+            lib.vxa_synchronize(ctx)
+            tot = 0.0
+            steps_x = 60
+            for k in range(steps_x):
+                lib.vxa_flush_l2(ctx)
+                lib.vxa_timer_begin(ctx)
+                if vxl.vxn_scene_submit(sc._h, frame_time(5 + k, anim) if anim else -1.0, prec, 0, 1) != 0:
+                    raise RuntimeError(vxl.vxn_last_error().decode())
+                msx = C.c_double()
+                lib.vxa_timer_end(ctx, C.byref(msx))
+                tot += msx.value
+            msf = tot / steps_x
+            extras[name] = {"ms_per_frame": round(msf, 4), "fps": round(1000 / msf, 1),
+                            "mrays_per_s": round(1920 * 1080 / msf / 1e3, 1), "frames": steps_x}
+        extras["animated_vs_static"] = round(extras["c2_animated_1080p"]["ms_per_frame"] /
+                                             extras["c3_static_1080p"]["ms_per_frame"], 4)
+
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -378,6 +405,7 @@ def run_ours(args):
                                      "bytes": round(alg_bytes / pixels_mine, 3)}},
             "cpu_baseline": base,
             "e2e": e2e,
+            "extras": extras,
             "gpu_launches": int(st.kernel_launches),
             "clocks": clocks.summary(),
         }
