@@ -161,6 +161,12 @@ class Scene:
         tf = (C.c_double * 15)(*transform15)
         _check(voxanim().vxn_scene_set_object(self._h, i, tf, 1 if dirty else 0), "set_object")
 
+    def frame_desc(self) -> vxa_frame_desc:
+        """Camera + background as a vxa_frame_desc (host only, no device needed)."""
+        f = vxa_frame_desc()
+        _check(voxanim().vxn_scene_export(self._h, C.byref(f), None, 0, None), "export")
+        return f
+
     def export(self):
         """(vxa_frame_desc, vxa_instance array) — the C-ABI view of the scene."""
         n = self.object_count()

@@ -26,7 +26,8 @@ constexpr int kBlock = 128;
 #define VXA_MIN_BLOCKS 8
 #endif
 constexpr int kWarps = kBlock / 32;
-constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
+constexpr uint32_t kListCap = 64;
+using BlockStack = SmemStack<kBlock * sizeof(uint2)>; // per-warp tile candidate list (bit positions of a u64 mask)
 
 template <typename Real> struct Best {
     bool have;
@@ -134,7 +135,7 @@ __device__ __forceinline__ bool cone_candidate(const DevInstance<float>& in, con
 template <typename Real, bool kAov>
 __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint32_t i, const Real dw[3],
                                                 const RayD& rd, Best<Real>& best, uint32_t& traversals,
-                                                uint32_t& fetches, uint2* stack) {
+                                                uint32_t& fetches, BlockStack& stack) {
     const DevInstance<Real>& in = p.inst[i];
     if (!in.valid_model) return;
     ++traversals;
@@ -163,7 +164,7 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         FastRay fr;
         if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits)) return;
         FastHit h;
-        const bool hit = traverse_fast<kAov>(in.model, fr, h, stack, kBlock);
+        const bool hit = traverse_fast<kAov>(in.model, fr, h, stack);
         fetches += h.fetches;
         if (!hit) return;
         for (int k = 0; k < 3; ++k) ld[k] = d[k], vox[k] = h.vox[k];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
     // rays and sphere tests per frame are known on the host (pixels x objects)
     uint32_t n_trav = 0, n_reuse = 0, n_fetch = 0, n_leaf = 0;
     const uint32_t n = p.n_inst;
-    uint2* const stack = smem_stack + threadIdx.x;
+    BlockStack stack{static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack + threadIdx.x))};
     const uint16_t* const list = s_list[warp];
 
     while (true) {

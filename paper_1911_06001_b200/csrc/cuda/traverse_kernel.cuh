@@ -75,10 +75,10 @@ __global__ void __launch_bounds__(128) traverse_kernel(DevModel m, const Travers
             Ur_lo[a] = static_cast<float>(ulo - static_cast<double>(U_lo[a]));
             Ur_hi[a] = static_cast<float>(uhi - static_cast<double>(U_hi[a]));
         }
-        uint2 lstack[kMaxDepth];
+        LocalStack lstack;
         if (fast_setup(r, d, U_lo, U_hi, Ur_lo, Ur_hi, h2, zf, zb)) {
             FastHit h;
-            hit = traverse_fast<true>(m, r, h, lstack, 1);
+            hit = traverse_fast<true>(m, r, h, lstack);
             o.node_fetches = h.fetches;
             if (hit) {
                 t = h.t, axis = h.axis, attr = h.attr, parent = h.parent, level = h.level;

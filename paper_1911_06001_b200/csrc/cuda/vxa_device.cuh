@@ -450,13 +450,35 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
     return !(te >= tx || tx < 0.0f);
 }
 
+// Traversal stacks. SmemStack: one column per thread of a [level][thread]
+// shared-memory array, addressed through a 32-bit shared-window base kept in
+// one register (the compiler otherwise re-derives the generic pointer from
+// threadIdx on every push/pop); LocalStack: a private array (API kernel).
+template <uint32_t kStride> struct SmemStack {
+    uint32_t base; // shared address of this thread's level-0 slot; levels kStride bytes apart
+    __device__ __forceinline__ uint2 load(int level) const {
+        uint2 v;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(base + level * kStride));
+        return v;
+    }
+    __device__ __forceinline__ void store(int level, uint2 v) const {
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(base + level * kStride), "r"(v.x), "r"(v.y));
+    }
+};
+
+struct LocalStack {
+    uint2 a[kMaxDepth];
+    __device__ __forceinline__ uint2 load(int level) const { return a[level]; }
+    __device__ __forceinline__ void store(int level, uint2 v) { a[level] = v; }
+};
+
 // Iterative traversal. The explicit stack holds only ancestor node words
 // (bits 24..27 of .x: the saved next octant) in the caller's stack column
 // (shared memory, [level][thread]); t0/tm/t1 of a parent are rebuilt on a
 // pop from the child's interval plus one plane per axis.
-template <bool kTrackIdx>
-__device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out, uint2* __restrict__ stack,
-                              uint32_t stride) {
+template <bool kTrackIdx, class Stack>
+__device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out, Stack& stack) {
+    const uint2* __restrict__ words = m.words; // kept in registers across the loop
     uint32_t sidx[kTrackIdx ? kMaxDepth : 1]; // ancestor indices (AOV: leaf parent)
     float c[3] = {0.0f, 0.0f, 0.0f};          // cell coordinates (exact integers)
     float sz = 1.0f;                          // cell size 2^-level
@@ -468,7 +490,7 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         tm[a] = plane_t(1.0f, 0.5f, r.A[a], r.Ar[a], r.inv[a]);
     }
     if (r.zero) fix_zero_axes(r, 0, t0, tm, t1);
-    uint2 fw = load_node(m, 0);
+    uint2 fw = __ldg(words);
     uint32_t fidx = 0, fetches = 1;
     uint32_t fcur = first_child(t0, tm);
     int level = 0;
@@ -478,7 +500,7 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         if (fcur == kExit) {
             if (level == 0) break;
             --level;
-            fw = stack[level * stride];
+            fw = stack.load(level);
             fcur = (fw.x >> 24) & 0xfu;
             fw.x &= 0x00ffffffu;
             if constexpr (kTrackIdx) fidx = sidx[level];
@@ -545,13 +567,13 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         }
         if (level + 1 >= depth) continue;
         const uint32_t child = fw.y + popc8_below(valid & ~leafm, bit);
-        stack[level * stride] = make_uint2(fw.x | (fcur << 24), fw.y);
+        stack.store(level, make_uint2(fw.x | (fcur << 24), fw.y));
         if constexpr (kTrackIdx) {
             sidx[level] = fidx;
             fidx = child;
         }
         ++level;
-        fw = load_node(m, child);
+        fw = __ldg(words + child);
         ++fetches;
         sz = 0.5f * sz;
 #pragma unroll
