@@ -507,16 +507,15 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
             sz = 2.0f * sz;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
+                // the child shares tm and one outer plane with the parent; only the
+                // other outer plane is recomputed (branch-free: one plane per axis)
                 const float cp = floorf(0.5f * c[a]);
                 const bool upper = c[a] != 2.0f * cp; // the child was the upper half
                 c[a] = cp;
-                if (upper) {
-                    tm[a] = t0[a];
-                    t0[a] = plane_t(cp, sz, r.A[a], r.Ar[a], r.inv[a]);
-                } else {
-                    tm[a] = t1[a];
-                    t1[a] = plane_t(cp + 1.0f, sz, r.A[a], r.Ar[a], r.inv[a]);
-                }
+                const float outer = plane_t(upper ? cp : cp + 1.0f, sz, r.A[a], r.Ar[a], r.inv[a]);
+                tm[a] = upper ? t0[a] : t1[a];
+                t0[a] = upper ? outer : t0[a];
+                t1[a] = upper ? t1[a] : outer;
             }
             if (r.zero) fix_zero_axes(r, level, t0, tm, t1);
             continue;
@@ -578,7 +577,7 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         sz = 0.5f * sz;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            c[a] = __fmaf_rn(2.0f, c[a], static_cast<float>((q >> (2 - a)) & 1u));
+            c[a] = __fmaf_rn(2.0f, c[a], (q & axis_bit(a)) ? 1.0f : 0.0f);
             t0[a] = c0[a];
             t1[a] = c1[a];
             tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
