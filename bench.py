@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3 animated-vs-static side measurements")
+    ap.add_argument("--same-device", action="store_true",
+                    help="testing aid: every rank uses GPU 0 (CUDA IPC between processes on one device, gloo "
+                         "barriers) to exercise the multi-rank path on a one-GPU box; not a scaling measurement")
     return ap.parse_args()
 
 
@@ -235,7 +238,8 @@ def run_reference(args):
 
 def run_ours(args):
     rank, world, local = dist_env()
-    os.environ["VOXANIM_DEVICE"] = str(local)
+    device = 0 if args.same_device else local
+    os.environ["VOXANIM_DEVICE"] = str(device)
     import paper_1911_06001_b200 as vx
     from paper_1911_06001_b200 import _abi
 
@@ -244,8 +248,11 @@ def run_ours(args):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     lib = vx.vxa()
     model, scene, W, H, animated = build_scene(vx, args.workload)
@@ -300,12 +307,17 @@ def run_ours(args):
     st = _abi.vxa_stats()
     check(lib.vxa_stats_read(ctx, C.byref(st)), "stats")
     total_ms = sum(step_ms)
-    if dist is not None:
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
         import torch
 
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.same_device else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        return float(t.item())
+
+    total_ms = max_over_ranks(total_ms)
 
     ms_per_step = total_ms / args.steps
     rays = W * H
@@ -320,8 +332,56 @@ def run_ours(args):
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.workload)
 
+    # N > 1: the frame composed in rank 0's framebuffer by peer stores must equal
+    # the single-device frame (same pixels, same arithmetic)
+    multi_ok = None
+    if world > 1:
+        import numpy as np
+
+        k_chk = args.warmup + args.steps + 1
+        submit(k_chk)
+        check(lib.vxa_synchronize(ctx), "sync")
+        barrier()
+        if rank == 0:
+            composed = np.empty((H, W, 3), np.uint8)
+            check(lib.vxa_read_framebuffer(ctx, composed.ctypes.data, W, H), "read_framebuffer")
+            if vxl.vxn_scene_submit(scene._h, frame_time(k_chk, animated), prec, 0, 1) != 0:
+                raise RuntimeError(vxl.vxn_last_error().decode())
+            alone = np.empty((H, W, 3), np.uint8)
+            check(lib.vxa_read_framebuffer(ctx, alone.ctypes.data, W, H), "read_framebuffer")
+            multi_ok = bool((composed == alone).all())
+        barrier()
+
     # end to end through the public API (voxanim::render_frame with host buffers)
     e2e = None
+    if not args.no_e2e and world > 1:
+        # every rank: host update + its super-tiles (peer stores into rank 0); rank 0
+        # then reads the composed RGB8 frame into page-locked host memory
+        import numpy as np
+
+        host_img = np.empty((H, W, 3), np.uint8)
+        if rank == 0:
+            check(lib.vxa_host_register(ctx, host_img.ctypes.data, host_img.nbytes), "host_register")
+        lib.vxa_stats_reset(ctx)
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(args.e2e_steps):
+            submit(k)
+            check(lib.vxa_synchronize(ctx), "sync")
+            barrier()
+            if rank == 0:
+                check(lib.vxa_read_framebuffer(ctx, host_img.ctypes.data, W, H), "read_framebuffer")
+            barrier()
+        el = max_over_ranks(time.perf_counter() - t0)
+        st2 = _abi.vxa_stats()
+        lib.vxa_stats_read(ctx, C.byref(st2))
+        if rank == 0:
+            lib.vxa_host_unregister(ctx, host_img.ctypes.data)
+        e2e = {"value": round(rays * args.e2e_steps / el / 1e6, 3), "unit": "Mrays/s",
+               "h2d_bytes_per_step": int(st2.h2d_bytes // args.e2e_steps) * world,
+               "d2h_bytes_per_step": W * H * 3, "ms_per_step": round(el * 1e3 / args.e2e_steps, 3),
+               "path": "every rank: evaluate_animation + vxa_submit of its super-tiles (NVLink peer stores into "
+                       "rank 0); rank 0: RGB8 pack + D2H into a page-locked host image"}
     if not args.no_e2e and world == 1:
         import numpy as np
 
@@ -407,6 +467,7 @@ def run_ours(args):
             "e2e": e2e,
             "extras": extras,
             "gpu_launches": int(st.kernel_launches),
+            "multi_gpu_frame_identical": multi_ok,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
