@@ -278,7 +278,7 @@ def run_ours(args):
 
     def submit(k):
         # host update (evaluate_animation) + instance table + frame submission, in C++
-        if vxl.vxn_scene_submit(scene._h, frame_time(k, animated), prec, rank, world) != 0:
+        if vxl.vxn_scene_submit(scene._h, frame_time(k, animated), prec, rank, world, 0) != 0:
             raise RuntimeError(vxl.vxn_last_error().decode())
 
     def barrier():
@@ -345,7 +345,7 @@ def run_ours(args):
         if rank == 0:
             composed = np.empty((H, W, 3), np.uint8)
             check(lib.vxa_read_framebuffer(ctx, composed.ctypes.data, W, H), "read_framebuffer")
-            if vxl.vxn_scene_submit(scene._h, frame_time(k_chk, animated), prec, 0, 1) != 0:
+            if vxl.vxn_scene_submit(scene._h, frame_time(k_chk, animated), prec, 0, 1, 0) != 0:
                 raise RuntimeError(vxl.vxn_last_error().decode())
             alone = np.empty((H, W, 3), np.uint8)
             check(lib.vxa_read_framebuffer(ctx, alone.ctypes.data, W, H), "read_framebuffer")
@@ -413,24 +413,37 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_extras:
         extras = {}
         m10 = vx.Model.procedural(10, shell=True)
-        for name, cfg, anim in (("c2_animated_1080p", 2, True), ("c3_static_1080p", 3, False)):
+        # "opt" = culling + sorting + the device-resident hit buffer (paper Fig. 6 "w/opt")
+        runs = (("c2_animated_1080p", 2, True, False), ("c3_static_1080p", 3, False, False),
+                ("c2_animated_opt_1080p", 2, True, True), ("c3_static_opt_1080p", 3, False, True))
+        for name, cfg, anim, opt in runs:
             sc = vx.Scene(cfg, [m10])
+            hbo = C.c_uint32(0)
+            if opt:
+                check(lib.vxa_hbo_create(ctx, 1920, 1080, C.byref(hbo)), "hbo_create")
             for k in range(5):
-                vxl.vxn_scene_submit(sc._h, frame_time(k, anim), prec, 0, 1)
+                vxl.vxn_scene_submit(sc._h, frame_time(k, anim), prec, 0, 1, hbo.value)
             lib.vxa_synchronize(ctx)
+            lib.vxa_stats_reset(ctx)
             tot = 0.0
             steps_x = 60
             for k in range(steps_x):
                 lib.vxa_flush_l2(ctx)
                 lib.vxa_timer_begin(ctx)
-                if vxl.vxn_scene_submit(sc._h, frame_time(5 + k, anim) if anim else -1.0, prec, 0, 1) != 0:
+                if vxl.vxn_scene_submit(sc._h, frame_time(5 + k, anim) if anim else -1.0, prec, 0, 1, hbo.value) != 0:
                     raise RuntimeError(vxl.vxn_last_error().decode())
                 msx = C.c_double()
                 lib.vxa_timer_end(ctx, C.byref(msx))
                 tot += msx.value
+            stx = _abi.vxa_stats()
+            lib.vxa_stats_read(ctx, C.byref(stx))
+            if opt:
+                lib.vxa_hbo_release(ctx, hbo.value)
             msf = tot / steps_x
             extras[name] = {"ms_per_frame": round(msf, 4), "fps": round(1000 / msf, 1),
-                            "mrays_per_s": round(1920 * 1080 / msf / 1e3, 1), "frames": steps_x}
+                            "mrays_per_s": round(1920 * 1080 / msf / 1e3, 1), "frames": steps_x,
+                            "pixels_reused_per_frame": int(stx.pixels_reused // steps_x),
+                            "traversals_per_frame": int(stx.svo_traversals // steps_x)}
         extras["animated_vs_static"] = round(extras["c2_animated_1080p"]["ms_per_frame"] /
                                              extras["c3_static_1080p"]["ms_per_frame"], 4)
 

@@ -52,10 +52,11 @@ int vxn_scene_set_object(vxn_scene* s, int index, const double* transform15, int
 int vxn_scene_export(vxn_scene* s, vxa_frame_desc* frame, vxa_instance* instances, uint32_t cap, uint32_t* count);
 void vxn_scene_free(vxn_scene* s);
 
-/* One benchmark step without Python in the loop: evaluate_animation(time)
- * (skipped when time < 0), build the instance table and vxa_submit the frame
- * (precision, screen-tile rank/world) on the global context. */
-int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int world);
+/* One benchmark step without Python in the loop, the reference bench loop
+ * (cli.cpp:265-270): evaluate_animation(time) (skipped when time < 0), build
+ * the instance table, vxa_submit the frame (precision, screen-tile
+ * rank/world, optional device hit buffer) on the global context, mark_clean. */
+int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int world, uint32_t hbo_device);
 
 vxn_hbo* vxn_hbo_create(int width, int height);
 void vxn_hbo_free(vxn_hbo* h);

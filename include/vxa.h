@@ -121,6 +121,11 @@ typedef struct vxa_frame_desc {
     /* Host hit buffer (width*height records) or NULL (RenderOptions::hbo).
      * Read before and written after the frame, in place. */
     vxa_hit_record* hbo;
+    /* Device-resident hit buffer (vxa_hbo_create handle) or 0: same reuse rule,
+     * records stay in HBM between frames (the paper's frame-coherence buffer
+     * without host round trips). Mutually exclusive with hbo. */
+    uint32_t hbo_device;
+    uint32_t pad1;
 } vxa_frame_desc;
 
 /* voxanim::FrameStats (renderer.hpp:62-68) plus device evidence. */
@@ -159,8 +164,16 @@ typedef struct vxa_pixel_aov {
 int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* instances,
                uint32_t instance_count, uint8_t* rgb_out, vxa_pixel_aov* aov_out, vxa_stats* stats);
 
+/* Device-resident hit buffers (HBO) for width x height frames, initialised
+ * to Miss records (a fresh voxanim::HitBuffer). */
+int vxa_hbo_create(vxa_ctx* ctx, int32_t width, int32_t height, uint32_t* handle_out);
+int vxa_hbo_release(vxa_ctx* ctx, uint32_t handle);
+/* Copies a device hit buffer to host records (width*height). */
+int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out);
+
 /* Asynchronous form for benchmarking: enqueues the frame on the context
- * stream (framebuffer stays in HBM), no host outputs, no HBO. */
+ * stream (framebuffer stays in HBM), no host outputs; a device hit buffer
+ * (hbo_device) is allowed, a host one is not. */
 int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* instances,
                uint32_t instance_count);
 int vxa_synchronize(vxa_ctx* ctx);

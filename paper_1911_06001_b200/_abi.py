@@ -63,6 +63,8 @@ class vxa_frame_desc(C.Structure):
         ("tile_rank", C.c_int32),
         ("tile_world", C.c_int32),
         ("hbo", C.POINTER(vxa_hit_record)),
+        ("hbo_device", C.c_uint32),
+        ("pad1", C.c_uint32),
     ]
 
 
@@ -160,7 +162,7 @@ except ImportError:  # pragma: no cover
 VXA_SYMBOLS = [
     "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
     "vxa_upload_model", "vxa_release_model", "vxa_model_info",
-    "vxa_render", "vxa_submit", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
+    "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_render", "vxa_submit", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
     "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_traverse",
 ]
@@ -198,6 +200,9 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_render", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32, P, P,
              C.POINTER(vxa_stats))
     _declare(lib, "vxa_submit", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32)
+    _declare(lib, "vxa_hbo_create", i, P, C.c_int32, C.c_int32, C.POINTER(u32))
+    _declare(lib, "vxa_hbo_release", i, P, u32)
+    _declare(lib, "vxa_hbo_download", i, P, u32, P)
     _declare(lib, "vxa_synchronize", i, P)
     _declare(lib, "vxa_stats_read", i, P, C.POINTER(vxa_stats))
     _declare(lib, "vxa_stats_reset", i, P)
@@ -242,7 +247,7 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_scene_export", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32,
              C.POINTER(u32))
     _declare(lib, "vxn_scene_free", None, P)
-    _declare(lib, "vxn_scene_submit", i, P, d, i, i, i)
+    _declare(lib, "vxn_scene_submit", i, P, d, i, i, i, u32)
     _declare(lib, "vxn_hbo_create", P, i, i)
     _declare(lib, "vxn_hbo_free", None, P)
     _declare(lib, "vxn_render", i, P, i, i, i, P, P, P, C.POINTER(u64), C.POINTER(d), C.POINTER(vxa_stats))

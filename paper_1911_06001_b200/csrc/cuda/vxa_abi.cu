@@ -60,6 +60,21 @@ __global__ void repack_nodes(const uint32_t* __restrict__ raw, uint32_t n, uint2
     if (side != nullptr && internal && leaves) side[child_base] = attr_base;
 }
 
+// Fresh hit records: HitRecord{} (colour {0,0,0,255}, normal 0, t 0, id -1, Miss).
+__global__ void init_hit_records(HitRec* r, size_t n) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    HitRec h;
+    h.color = 0xff000000u;
+    h.pad0 = 0;
+    h.normal[0] = h.normal[1] = h.normal[2] = 0.0;
+    h.t = 0.0;
+    h.object_id = -1;
+    h.kind = 0;
+    h.pad1[0] = h.pad1[1] = h.pad1[2] = 0;
+    r[i] = h;
+}
+
 // RGBA8 framebuffer -> RGB8 (four pixels per thread: 16 B in, 12 B out).
 __global__ void pack_rgb(const uint32_t* __restrict__ fb, uint8_t* __restrict__ rgb, size_t n_pix) {
     const size_t q = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -134,6 +149,12 @@ struct vxa_ctx {
     cudaEvent_t inst_done[2] = {nullptr, nullptr};
     int inst_slot = 0;
 
+    struct DeviceHbo {
+        HitRec* rec = nullptr;
+        int32_t w = 0, h = 0;
+    };
+    std::map<uint32_t, DeviceHbo> hbos;
+    uint32_t next_hbo = 1;
     DevBuf<PixelAov> aov;
     DevBuf<HitRec> hbo;
     DevBuf<uint8_t> rgb;
@@ -459,6 +480,7 @@ int vxa_destroy(vxa_ctx* ctx) {
         cudaFree(m.attrs);
     }
     if (ctx->peer_fb) cudaIpcCloseMemHandle(ctx->peer_fb);
+    for (auto& [h, b] : ctx->hbos) cudaFree(b.rec);
     ctx->fb.release();
     ctx->tile_counter.release();
     ctx->counters.release();
@@ -588,6 +610,14 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         aov = ctx->aov.ptr;
         VXA_CUDA(cudaMemsetAsync(aov, 0, npix * sizeof(PixelAov), ctx->stream));
     }
+    if (f->hbo && f->hbo_device) return fail(VXA_ERR_INVALID, "host and device hit buffers are exclusive");
+    if (f->hbo_device) {
+        const auto it = ctx->hbos.find(f->hbo_device);
+        if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
+        if (it->second.w != f->camera.width || it->second.h != f->camera.height)
+            return fail(VXA_ERR_INVALID, "hit buffer dimensions do not match the camera");
+        hbo = it->second.rec;
+    }
     if (f->hbo) {
         VXA_CUDA(ctx->hbo.ensure(npix));
         hbo = ctx->hbo.ptr;
@@ -626,13 +656,64 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     return VXA_OK;
 }
 
+int vxa_hbo_create(vxa_ctx* ctx, int32_t width, int32_t height, uint32_t* handle_out) {
+    if (ctx == nullptr || handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    if (width < 1 || height < 1) return fail(VXA_ERR_INVALID, "bad hit buffer size");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = static_cast<size_t>(width) * height;
+    vxa_ctx::DeviceHbo b;
+    VXA_CUDA(cudaMalloc(&b.rec, n * sizeof(HitRec)));
+    b.w = width;
+    b.h = height;
+    init_hit_records<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(b.rec, n);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFree(b.rec);
+        return fail(VXA_ERR_CUDA, std::string("hbo init: ") + cudaGetErrorString(e));
+    }
+    const uint32_t h = ctx->next_hbo++;
+    ctx->hbos[h] = b;
+    *handle_out = h;
+    return VXA_OK;
+}
+
+int vxa_hbo_release(vxa_ctx* ctx, uint32_t handle) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    const auto it = ctx->hbos.find(handle);
+    if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(it->second.rec);
+    ctx->hbos.erase(it);
+    return VXA_OK;
+}
+
+int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out) {
+    if (ctx == nullptr || out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    const auto it = ctx->hbos.find(handle);
+    if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = static_cast<size_t>(it->second.w) * it->second.h;
+    VXA_CUDA(cudaMemcpyAsync(out, it->second.rec, n * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VXA_OK;
+}
+
 int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     if (int rc = check_frame(f); rc != VXA_OK) return rc;
-    if (f->hbo) return fail(VXA_ERR_INVALID, "vxa_submit does not take a hit buffer");
+    if (f->hbo) return fail(VXA_ERR_INVALID, "vxa_submit does not take a host hit buffer");
     if (n > 0 && in == nullptr) return fail(VXA_ERR_INVALID, "null instance array");
     VXA_CUDA(cudaSetDevice(ctx->device));
-    return enqueue_any(ctx, f, in, n, nullptr, nullptr, false);
+    HitRec* hbo = nullptr;
+    if (f->hbo_device) {
+        const auto it = ctx->hbos.find(f->hbo_device);
+        if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
+        if (it->second.w != f->camera.width || it->second.h != f->camera.height)
+            return fail(VXA_ERR_INVALID, "hit buffer dimensions do not match the camera");
+        hbo = it->second.rec;
+    }
+    return enqueue_any(ctx, f, in, n, nullptr, hbo, false);
 }
 
 int vxa_synchronize(vxa_ctx* ctx) {

@@ -214,7 +214,7 @@ void export_instances(const voxanim::Scene& sc, vxa_instance* inst) {
 
 } // namespace
 
-int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int world) {
+int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int world, uint32_t hbo_device) {
     return guard(
         [&] {
             if (time >= 0.0) voxanim::evaluate_animation(s->s, time);
@@ -226,9 +226,11 @@ int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int wor
             f.precision = static_cast<std::uint8_t>(precision);
             f.tile_rank = rank;
             f.tile_world = world;
+            f.hbo_device = hbo_device;
             voxanim::gpu::check(vxa_submit(voxanim::gpu::context(), &f, inst.data(),
                                            static_cast<std::uint32_t>(inst.size())),
                                 "vxa_submit");
+            voxanim::mark_clean(s->s); // the caller's per-frame mark_clean (reference cli.cpp:270)
             return 0;
         },
         -1);

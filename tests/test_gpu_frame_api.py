@@ -113,3 +113,43 @@ def test_invalid_arguments(gpu):
     s = vx.Scene(vx.config.TWO_OBJECTS, [vx.Model.random(3, 2, 0.0)])
     img, _, st = s.render()
     assert (img == np.array([10, 20, 30], np.uint8)).all()
+
+
+@pytest.mark.parametrize("precision", [vx.VXA_FP64, vx.VXA_FP32])
+def test_device_hit_buffer_matches_host_hit_buffer(gpu, precision):
+    """The device-resident HBO (vxa_hbo_create) follows the same reuse rule as the
+    host HitBuffer: identical images and FrameStats over a mutating sequence, and
+    (FP64) identical to the reference renderer with its HitBuffer."""
+    lib = vx.vxa()
+    ctx = vx.context()
+    s_dev, o = hbo_pair(77)
+    s_host, _ = hbo_pair(77)
+    hbo_host = vx.HitBuffer(96, 64)
+    rhbo = ref.RefHitBuffer(96, 64)
+    handle = C.c_uint32()
+    assert lib.vxa_hbo_create(ctx, 96, 64, C.byref(handle)) == 0
+    rng = np.random.default_rng(9)
+    for frame in range(20):
+        jit = rng.uniform(-0.05, 0.05, 2)
+        for sc in (s_dev, s_host, o):
+            mutate(sc, frame, jit)
+        f, inst, n = s_dev.export()
+        f.precision = precision
+        f.hbo_device = handle.value
+        img = np.zeros((64, 96, 3), np.uint8)
+        st = _abi.vxa_stats()
+        assert lib.vxa_render(ctx, C.byref(f), inst, n, img.ctypes.data, None, C.byref(st)) == 0, \
+            lib.vxa_last_error()
+        b, _, sb = s_host.render(precision=precision, hbo=hbo_host)
+        assert (img == b).all(), frame
+        assert st.pixels_reused == sb["pixels_reused"] and st.svo_traversals == sb["svo_traversals"]
+        if precision == vx.VXA_FP64:
+            r_img, r_st = o.render(hbo=rhbo)
+            assert (img == r_img).all()
+            assert st.pixels_reused == r_st["pixels_reused"]
+        for sc in (s_dev, s_host, o):
+            sc.mark_clean()
+    recs = (_abi.vxa_hit_record * (96 * 64))()
+    assert lib.vxa_hbo_download(ctx, handle.value, recs) == 0
+    assert any(r.kind != 0 for r in recs)
+    assert lib.vxa_hbo_release(ctx, handle.value) == 0
