@@ -132,7 +132,7 @@ __device__ __forceinline__ bool cone_candidate(const DevInstance<float>& in, con
     return s * c.cos_a + perp * c.sin_a >= 0.0f;        // else only the apex region remains
 }
 
-template <typename Real, bool kAov>
+template <typename Real, bool kAov, bool kCompact>
 __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint32_t i, const Real dw[3],
                                                 const RayD& rd, Best<Real>& best, uint32_t& traversals,
                                                 uint32_t& fetches, BlockStack& stack) {
@@ -164,7 +164,12 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         FastRay fr;
         if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits)) return;
         FastHit h;
-        const bool hit = traverse_fast<kAov>(in.model, fr, h, stack);
+        bool hit;
+        if constexpr (kCompact)
+            hit = traverse_fast<kAov>(CompactNodes{in.model.cwords}, static_cast<int>(in.model.depth), fr, h, stack);
+        else
+            hit = traverse_fast<kAov>(WideNodes{in.model.words, in.model.side}, static_cast<int>(in.model.depth), fr, h,
+                                      stack);
         fetches += h.fetches;
         if (!hit) return;
         for (int k = 0; k < 3; ++k) ld[k] = d[k], vox[k] = h.vox[k];
@@ -205,7 +210,7 @@ __device__ __forceinline__ uint32_t shade_rgba(uint32_t color, const Real n[3], 
     return out;
 }
 
-template <typename Real, bool kAov, bool kHbo>
+template <typename Real, bool kAov, bool kHbo, bool kCompact>
 __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
     extern __shared__ uint2 smem_stack[]; // FP32 traversal stack: [level][thread]
     __shared__ uint16_t s_list[kWarps][kListCap];
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
                 // sorted orders: skip (do not break) when the best hit is nearer than the
                 // candidate's sphere (renderer.cpp:70-72); id orders carry t_boundary = 0
                 if ((mode == kListSorted || mode == kAllSorted) && best.have && best.t < cand_tb) continue;
-                trace_candidate<Real, kAov>(p, cand, dw, rd, best, traversals, fetches, stack);
+                trace_candidate<Real, kAov, kCompact>(p, cand, dw, rd, best, traversals, fetches, stack);
             }
             if (best.have) kind = n_cand > 1 ? kMulti : kSingle;
             if constexpr (kHbo) {

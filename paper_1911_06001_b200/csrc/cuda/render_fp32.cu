@@ -6,25 +6,26 @@
 namespace vxa {
 
 namespace {
-template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<float, A, H>); }
-void* pick(bool aov, bool hbo) {
-    if (aov) return hbo ? frame_fn<true, true>() : frame_fn<true, false>();
-    return hbo ? frame_fn<false, true>() : frame_fn<false, false>();
+template <bool A, bool H, bool K> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<float, A, H, K>); }
+template <bool K> void* pick_k(bool aov, bool hbo) {
+    if (aov) return hbo ? frame_fn<true, true, K>() : frame_fn<true, false, K>();
+    return hbo ? frame_fn<false, true, K>() : frame_fn<false, false, K>();
 }
+void* pick(bool aov, bool hbo, bool compact) { return compact ? pick_k<true>(aov, hbo) : pick_k<false>(aov, hbo); }
 } // namespace
 
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l) {
     void* args[] = {const_cast<FrameParams<float>*>(&p)};
-    return cudaLaunchKernel(pick(aov, hbo), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f32(p.max_depth), l.stream);
+    return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f32(p.max_depth), l.stream);
 }
 
 size_t frame_smem_bytes_f32(uint32_t max_depth) {
     return sizeof(uint2) * kBlock * (max_depth > 0 ? max_depth : 1);
 }
 
-int frame_blocks_per_sm_f32(bool aov, bool hbo, uint32_t max_depth) {
+int frame_blocks_per_sm_f32(bool aov, bool hbo, bool compact, uint32_t max_depth) {
     int b = 0;
-    void* fn = pick(aov, hbo);
+    void* fn = pick(aov, hbo, compact);
     const size_t smem = frame_smem_bytes_f32(max_depth);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, smem) != cudaSuccess) return 1;

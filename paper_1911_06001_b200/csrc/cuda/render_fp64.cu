@@ -7,8 +7,8 @@
 namespace vxa {
 
 namespace {
-template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<double, A, H>); }
-void* pick(bool aov, bool hbo) {
+template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<double, A, H, false>); }
+void* pick(bool aov, bool hbo, bool /*compact: FP64 keeps the general words*/) {
     if (aov) return hbo ? frame_fn<true, true>() : frame_fn<true, false>();
     return hbo ? frame_fn<false, true>() : frame_fn<false, false>();
 }
@@ -16,16 +16,16 @@ void* pick(bool aov, bool hbo) {
 
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l) {
     void* args[] = {const_cast<FrameParams<double>*>(&p)};
-    return cudaLaunchKernel(pick(aov, hbo), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f64(p.max_depth), l.stream);
+    return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f64(p.max_depth), l.stream);
 }
 
 size_t frame_smem_bytes_f64(uint32_t max_depth) {
     return 0;
 }
 
-int frame_blocks_per_sm_f64(bool aov, bool hbo, uint32_t max_depth) {
+int frame_blocks_per_sm_f64(bool aov, bool hbo, bool compact, uint32_t max_depth) {
     int b = 0;
-    void* fn = pick(aov, hbo);
+    void* fn = pick(aov, hbo, compact);
     const size_t smem = frame_smem_bytes_f64(max_depth);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, smem) != cudaSuccess) return 1;

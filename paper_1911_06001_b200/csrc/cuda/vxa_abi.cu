@@ -102,6 +102,7 @@ __global__ void pack_rgb(const uint32_t* __restrict__ fb, uint8_t* __restrict__ 
 struct ModelEntry {
     DevModel dev{};
     uint2* words = nullptr;
+    uint32_t* cwords = nullptr; // compact words when the model is canonical
     uint32_t* side = nullptr;
     uint32_t* attrs = nullptr;
     uint64_t bytes = 0;
@@ -164,7 +165,7 @@ struct vxa_ctx {
     DevBuf<VisitOut> visits;
 
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, t_a = nullptr, t_b = nullptr;
-    int occ[2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][stack height]
+    int occ[2][2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][compact][stack height]
 
     // Frame-kernel timing ring: events recorded tight around every frame
     // kernel launch; vxa_stats_read sums them (gpu_ms) since the last reset.
@@ -355,8 +356,14 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     if (p.sphere_pass) ctx->n_sphere_tests += my_pixels * n;
     p.fb = target;
     p.max_depth = 1;
+    p.compact = sizeof(Real) == 4 ? 1u : 0u;
     for (const auto& di : tab)
-        if (di.valid_model) p.max_depth = std::max(p.max_depth, std::min(di.model.depth, kMaxDepth));
+        if (di.valid_model) {
+            p.max_depth = std::max(p.max_depth, std::min(di.model.depth, kMaxDepth));
+            if (di.model.cwords == nullptr) p.compact = 0;
+        }
+    // VOXANIM_NODE_WORDS=wide forces the general words (tests, A/B timing); read per frame
+    if (const char* env = std::getenv("VOXANIM_NODE_WORDS"); env && std::strcmp(env, "wide") == 0) p.compact = 0;
     p.tile_counter = ctx->tile_counter.ptr;
     p.counters = ctx->counters.ptr;
     p.aov = aov;
@@ -371,8 +378,9 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     const bool is64 = sizeof(Real) == 8;
     const bool a = aov != nullptr, h = hbo != nullptr;
 
-    int& occ = ctx->occ[is64][a][h][p.max_depth];
-    if (occ == 0) occ = is64 ? frame_blocks_per_sm_f64(a, h, p.max_depth) : frame_blocks_per_sm_f32(a, h, p.max_depth);
+    int& occ = ctx->occ[is64][a][h][p.compact][p.max_depth];
+    if (occ == 0)
+        occ = is64 ? frame_blocks_per_sm_f64(a, h, false, p.max_depth) : frame_blocks_per_sm_f32(a, h, p.compact, p.max_depth);
     FrameLaunch l{ctx->sm_count * occ, ctx->stream};
     const int slot_k = ctx->k_count % vxa_ctx::kRing;
     if (ctx->k_begin[slot_k] == nullptr) {
@@ -475,6 +483,7 @@ int vxa_destroy(vxa_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& [h, m] : ctx->models) {
+        cudaFree(m.cwords);
         cudaFree(m.words);
         cudaFree(m.side);
         cudaFree(m.attrs);
@@ -539,6 +548,34 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
             return fail(VXA_ERR_MODEL, "node " + std::to_string(i) + ": attr_base out of range");
         any_mixed |= ni > 0 && nl > 0;
     }
+    // Canonical models (leaves exactly at the last level, bases < 2^24) also get
+    // compact 4-byte words: valid | base << 8. Levels follow from the BFS-free
+    // rule "children come after their parent" (validated above).
+    std::vector<uint32_t> compact;
+    {
+        std::vector<uint8_t> lvl(node_count, 0);
+        bool ok = node_count < (1u << 24) && attr_count <= (1u << 24);
+        for (uint32_t i = 0; i < node_count && ok; ++i) {
+            const uint8_t* r = raw + 12 * size_t{i};
+            uint32_t cb, ab;
+            std::memcpy(&cb, r, 4);
+            std::memcpy(&ab, r + 4, 4);
+            const uint32_t valid = r[8], leaf = r[9];
+            const uint32_t internal = valid & ~leaf & 0xffu;
+            const bool last = lvl[i] + 1u == depth;
+            if (last ? (leaf != valid) : (leaf != 0)) ok = false;
+            if (internal) {
+                const int ni = __builtin_popcount(internal);
+                for (int k = 0; k < ni; ++k) lvl[cb + k] = static_cast<uint8_t>(lvl[i] + 1);
+            }
+            if (ok) {
+                const uint32_t base = last ? ab : cb;
+                if (base >= (1u << 24)) ok = false;
+                compact.push_back(valid | ((valid ? base : 0u) << 8));
+            }
+        }
+        if (!ok) compact.clear();
+    }
     ModelEntry m;
     uint32_t* raw_dev = nullptr;
     const size_t raw_bytes = 12 * size_t{node_count};
@@ -546,6 +583,9 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
     cudaError_t e = cudaMalloc(&m.words, sizeof(uint2) * node_count);
     if (e == cudaSuccess && any_mixed) e = cudaMalloc(&m.side, sizeof(uint32_t) * node_count);
     if (e == cudaSuccess) e = cudaMalloc(&m.attrs, sizeof(uint32_t) * std::max<uint32_t>(attr_count, 1));
+    if (e == cudaSuccess && !compact.empty()) e = cudaMalloc(&m.cwords, sizeof(uint32_t) * node_count);
+    if (e == cudaSuccess && !compact.empty())
+        e = cudaMemcpyAsync(m.cwords, compact.data(), sizeof(uint32_t) * node_count, cudaMemcpyHostToDevice, ctx->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(raw_dev, nodes, raw_bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (e == cudaSuccess && attr_count)
         e = cudaMemcpyAsync(m.attrs, attrs, sizeof(uint32_t) * attr_count, cudaMemcpyHostToDevice, ctx->stream);
@@ -557,17 +597,20 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
     cudaFree(raw_dev);
     if (e != cudaSuccess) {
         cudaFree(m.words);
+        cudaFree(m.cwords);
         cudaFree(m.side);
         cudaFree(m.attrs);
         return fail(e == cudaErrorMemoryAllocation ? VXA_ERR_OOM : VXA_ERR_CUDA,
                     std::string("model upload: ") + cudaGetErrorString(e));
     }
     m.dev.words = m.words;
+    m.dev.cwords = m.cwords;
     m.dev.side = m.side;
     m.dev.attrs = m.attrs;
     m.dev.depth = depth;
     m.dev.node_count = node_count;
-    m.bytes = sizeof(uint2) * uint64_t{node_count} + (any_mixed ? 4ull * node_count : 0) + 4ull * attr_count;
+    m.bytes = sizeof(uint2) * uint64_t{node_count} + (any_mixed ? 4ull * node_count : 0) + 4ull * attr_count +
+              (m.cwords ? 4ull * node_count : 0);
     const uint32_t handle = ctx->next_handle++;
     ctx->models[handle] = m;
     *handle_out = handle;
@@ -581,6 +624,7 @@ int vxa_release_model(vxa_ctx* ctx, uint32_t handle) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaFree(it->second.words);
+    cudaFree(it->second.cwords);
     cudaFree(it->second.side);
     cudaFree(it->second.attrs);
     ctx->models.erase(it);
@@ -592,7 +636,7 @@ int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32
     const auto it = ctx->models.find(handle);
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     if (device_bytes) *device_bytes = it->second.bytes;
-    if (node_format) *node_format = 2;
+    if (node_format) *node_format = it->second.cwords ? 1 : 2;
     return VXA_OK;
 }
 

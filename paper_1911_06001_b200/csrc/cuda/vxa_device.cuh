@@ -49,11 +49,51 @@ __host__ __device__ inline int32_t tile_owner(int32_t x, int32_t y, int32_t widt
 }
 
 struct DevModel {
-    const uint2* words;
-    const uint32_t* side;
+    const uint2* words;     // general 8-byte node words
+    const uint32_t* side;   // attr_base of mixed nodes, indexed by child_base
+    const uint32_t* cwords; // compact 4-byte words (canonical models only) or null
     const uint32_t* attrs;
     uint32_t depth;
     uint32_t node_count;
+};
+
+// Node word policies of the FP32 core.
+// WideNodes: {valid | leaf << 8 | mixed, base} for any valid model.
+// CompactNodes: valid | base << 8 (base < 2^24), for canonical models -- leaves
+// exactly at the last level, none above it (every model build_from_grid or the
+// procedural builder produces): the leaf mask is implied by the level, halving
+// the node bytes the traversal touches.
+struct WideNodes {
+    const uint2* w;
+    const uint32_t* side;
+    using Word = uint2;
+    __device__ __forceinline__ Word load(uint32_t i) const { return __ldg(w + i); }
+    __device__ __forceinline__ static uint32_t valid(Word x) { return x.x & 0xffu; }
+    __device__ __forceinline__ static uint32_t leaves(Word x, int /*level*/, int /*depth*/) { return (x.x >> 8) & 0xffu; }
+    __device__ __forceinline__ static uint32_t child_base(Word x) { return x.y; }
+    __device__ __forceinline__ uint32_t attr_base(Word x) const { return (x.x & kMixed) ? __ldg(side + x.y) : x.y; }
+    __device__ __forceinline__ static uint2 pack(Word x, uint32_t cur) { return make_uint2(x.x | (cur << 24), x.y); }
+    __device__ __forceinline__ static Word unpack(uint2 v, uint32_t& cur) {
+        cur = (v.x >> 24) & 0xfu;
+        return make_uint2(v.x & 0x00ffffffu, v.y);
+    }
+};
+
+struct CompactNodes {
+    const uint32_t* w;
+    using Word = uint32_t;
+    __device__ __forceinline__ Word load(uint32_t i) const { return __ldg(w + i); }
+    __device__ __forceinline__ static uint32_t valid(Word x) { return x & 0xffu; }
+    __device__ __forceinline__ static uint32_t leaves(Word x, int level, int depth) {
+        return level + 1 == depth ? (x & 0xffu) : 0u;
+    }
+    __device__ __forceinline__ static uint32_t child_base(Word x) { return x >> 8; }
+    __device__ __forceinline__ uint32_t attr_base(Word x) const { return x >> 8; }
+    __device__ __forceinline__ static uint2 pack(Word x, uint32_t cur) { return make_uint2(x, cur); }
+    __device__ __forceinline__ static Word unpack(uint2 v, uint32_t& cur) {
+        cur = v.y;
+        return v.x;
+    }
 };
 
 // Per-instance frame constants, rebuilt on the host every frame from the FP64
@@ -99,6 +139,7 @@ template <typename Real> struct FrameParams {
     uint32_t n_super_x;
     uint32_t n_tiles; // warp tiles owned by this rank
     uint32_t max_depth; // deepest model of the frame (FP32 shared-memory stack height)
+    uint32_t compact;   // every model has compact 4-byte words (FP32 kernel)
     // outputs
     uint32_t* fb;                 // RGBA8 framebuffer (local or peer-mapped)
     uint32_t* tile_counter;       // persistent-thread work counter
@@ -476,9 +517,8 @@ struct LocalStack {
 // (bits 24..27 of .x: the saved next octant) in the caller's stack column
 // (shared memory, [level][thread]); t0/tm/t1 of a parent are rebuilt on a
 // pop from the child's interval plus one plane per axis.
-template <bool kTrackIdx, class Stack>
-__device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out, Stack& stack) {
-    const uint2* __restrict__ words = m.words; // kept in registers across the loop
+template <bool kTrackIdx, class Nodes, class Stack>
+__device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay& r, FastHit& out, Stack& stack) {
     uint32_t sidx[kTrackIdx ? kMaxDepth : 1]; // ancestor indices (AOV: leaf parent)
     float c[3] = {0.0f, 0.0f, 0.0f};          // cell coordinates (exact integers)
     float sz = 1.0f;                          // cell size 2^-level
@@ -490,19 +530,17 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
         tm[a] = plane_t(1.0f, 0.5f, r.A[a], r.Ar[a], r.inv[a]);
     }
     if (r.zero) fix_zero_axes(r, 0, t0, tm, t1);
-    uint2 fw = __ldg(words);
+    typename Nodes::Word fw = nodes.load(0);
     uint32_t fidx = 0, fetches = 1;
     uint32_t fcur = first_child(t0, tm);
     int level = 0;
-    const int depth = min(static_cast<int>(m.depth), static_cast<int>(kMaxDepth));
+    const int depth = min(model_depth, static_cast<int>(kMaxDepth));
 
     while (true) {
         if (fcur == kExit) {
             if (level == 0) break;
             --level;
-            fw = stack.load(level);
-            fcur = (fw.x >> 24) & 0xfu;
-            fw.x &= 0x00ffffffu;
+            fw = Nodes::unpack(stack.load(level), fcur);
             if constexpr (kTrackIdx) fidx = sidx[level];
             sz = 2.0f * sz;
 #pragma unroll
@@ -544,13 +582,11 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
 
         const uint32_t oct = q ^ r.mirror;
         const uint32_t bit = 1u << oct;
-        const uint32_t valid = fw.x & 0xffu;
-        const uint32_t leafm = (fw.x >> 8) & 0xffu;
+        const uint32_t valid = Nodes::valid(fw);
         if (!(valid & bit)) continue;
+        const uint32_t leafm = Nodes::leaves(fw, level, depth);
         if (leafm & bit) {
-            // mixed nodes keep attr_base in side[child_base] (vxa_abi.cu repack)
-            const uint32_t abase = (fw.x & kMixed) ? __ldg(m.side + fw.y) : fw.y;
-            out.attr = abase + popc8_below(valid & leafm, bit);
+            out.attr = nodes.attr_base(fw) + popc8_below(valid & leafm, bit);
             out.t = fmaxf(t_enter, 0.0f);
             out.parent = fidx;
             out.level = static_cast<uint32_t>(level + 1);
@@ -565,14 +601,14 @@ __device__ bool traverse_fast(const DevModel& m, const FastRay& r, FastHit& out,
             return true;
         }
         if (level + 1 >= depth) continue;
-        const uint32_t child = fw.y + popc8_below(valid & ~leafm, bit);
-        stack.store(level, make_uint2(fw.x | (fcur << 24), fw.y));
+        const uint32_t child = Nodes::child_base(fw) + popc8_below(valid & ~leafm, bit);
+        stack.store(level, Nodes::pack(fw, fcur));
         if constexpr (kTrackIdx) {
             sidx[level] = fidx;
             fidx = child;
         }
         ++level;
-        fw = __ldg(words + child);
+        fw = nodes.load(child);
         ++fetches;
         sz = 0.5f * sz;
 #pragma unroll

@@ -35,8 +35,8 @@ struct FrameLaunch {
 
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l);
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l);
-int frame_blocks_per_sm_f32(bool aov, bool hbo, uint32_t max_depth);
-int frame_blocks_per_sm_f64(bool aov, bool hbo, uint32_t max_depth);
+int frame_blocks_per_sm_f32(bool aov, bool hbo, bool compact, uint32_t max_depth);
+int frame_blocks_per_sm_f64(bool aov, bool hbo, bool compact, uint32_t max_depth);
 size_t frame_smem_bytes_f32(uint32_t max_depth);
 
 size_t frame_smem_bytes_f64(uint32_t max_depth);

@@ -102,3 +102,39 @@ def test_c4_reduced(gpu):
         o.evaluate(t)
         o_aov, o_img = check_fp64(s, o)
         check_fp32(s, o, o_aov, o_img)
+
+
+def mixed_node_model():
+    """A hand-built (non-canonical) model: the root holds a leaf voxel next to an
+    internal child -- valid for the reference (svo.cpp validate) but not for the
+    compact node words, so the general words + side array are exercised."""
+    import struct
+
+    nodes = [(1, 0, 0b00000011, 0b00000001), (0, 1, 0xFF, 0xFF)]
+    attrs = [(200, 40, 40, 255)] + [(40 + 20 * k, 200 - 10 * k, 90, 255) for k in range(8)]
+    data = b"SVOA" + struct.pack("<IIII", 1, 2, len(nodes), len(attrs))
+    for cb, ab, v, l in nodes:
+        data += struct.pack("<IIBBH", cb, ab, v, l, 0)
+    for a in attrs:
+        data += bytes(a)
+    return vx.Model.from_bytes(data)
+
+
+def test_mixed_node_model(gpu):
+    m = mixed_node_model()
+    s, o = pair(vx.config.TWO_OBJECTS, [m])
+    o_aov, o_img = check_fp64(s, o)
+    assert (o_aov["object_id"] >= 0).sum() > 100
+    check_fp32(s, o, o_aov, o_img)
+
+
+@pytest.mark.parametrize("words", ["wide", "compact"])
+def test_node_word_formats_agree(gpu, words, monkeypatch):
+    """C4 reduced with the general 8-byte words forced (VOXANIM_NODE_WORDS=wide)
+    and with the compact words: both parity-clean against the oracle."""
+    monkeypatch.setenv("VOXANIM_NODE_WORDS", words)
+    s, o = pair(vx.config.C4, [vx.Model.procedural(9, shell=True)], w=320, h=180)
+    s.evaluate(0.9)
+    o.evaluate(0.9)
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img)
