@@ -559,14 +559,20 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             continue;
         }
         const uint32_t q = fcur;
-        float c0[3], c1[3];
+        float c1[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const bool up = (q & axis_bit(a)) != 0;
-            c0[a] = up ? tm[a] : t0[a];
-            c1[a] = up ? t1[a] : tm[a];
-        }
+        for (int a = 0; a < 3; ++a) c1[a] = (q & axis_bit(a)) ? t1[a] : tm[a];
         fcur = next_child(c1, q);
+        // An absent child is skipped before its interval is evaluated: the
+        // reference culls first and checks node_child second, but both only
+        // `continue`, so the order of the two tests is not observable.
+        const uint32_t oct = q ^ r.mirror;
+        const uint32_t bit = 1u << oct;
+        const uint32_t valid = Nodes::valid(fw);
+        if (!(valid & bit)) continue;
+        float c0[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) c0[a] = (q & axis_bit(a)) ? tm[a] : t0[a];
         int entry = 0;
         float t_enter = c0[0];
         if (c0[1] > t_enter) {
@@ -579,11 +585,6 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         }
         const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
         if (!(t_enter < t_exit) || t_exit < 0.0f) continue;
-
-        const uint32_t oct = q ^ r.mirror;
-        const uint32_t bit = 1u << oct;
-        const uint32_t valid = Nodes::valid(fw);
-        if (!(valid & bit)) continue;
         const uint32_t leafm = Nodes::leaves(fw, level, depth);
         if (leafm & bit) {
             out.attr = nodes.attr_base(fw) + popc8_below(valid & leafm, bit);
