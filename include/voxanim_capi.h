@@ -58,6 +58,10 @@ void vxn_scene_free(vxn_scene* s);
  * rank/world, optional device hit buffer) on the global context, mark_clean. */
 int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int world, uint32_t hbo_device);
 
+/* Streaming step: evaluate_animation(time), frame + asynchronous RGB8 readback
+ * into rgb_out (vxa_submit_readback); wait with vxa_wait_readback(ticket). */
+int vxn_scene_stream(vxn_scene* s, double time, int precision, uint8_t* rgb_out, uint64_t* ticket);
+
 vxn_hbo* vxn_hbo_create(int width, int height);
 void vxn_hbo_free(vxn_hbo* h);
 

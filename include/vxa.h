@@ -177,6 +177,15 @@ int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out);
 int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* instances,
                uint32_t instance_count);
 int vxa_synchronize(vxa_ctx* ctx);
+
+/* Streaming form: enqueues the frame, its RGB8 pack and an asynchronous D2H into
+ * rgb_out (host, width*height*3; page-lock it with vxa_host_register) on a copy
+ * stream, so frame k's readback overlaps frame k+1's kernel. Returns a ticket;
+ * rgb_out is valid once vxa_wait_readback(ticket) returns. Two readbacks can be
+ * in flight; a third waits for the oldest. */
+int vxa_submit_readback(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* instances,
+                        uint32_t instance_count, uint8_t* rgb_out, uint64_t* ticket);
+int vxa_wait_readback(vxa_ctx* ctx, uint64_t ticket);
 /* Device counters accumulated since the last vxa_stats_reset. */
 int vxa_stats_read(vxa_ctx* ctx, vxa_stats* stats);
 int vxa_stats_reset(vxa_ctx* ctx);

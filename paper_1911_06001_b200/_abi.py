@@ -162,7 +162,8 @@ except ImportError:  # pragma: no cover
 VXA_SYMBOLS = [
     "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
     "vxa_upload_model", "vxa_release_model", "vxa_model_info",
-    "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_render", "vxa_submit", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
+    "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_render", "vxa_submit", "vxa_submit_readback",
+    "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
     "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_traverse",
 ]
@@ -170,7 +171,7 @@ VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
     "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
-    "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit",
+    "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit", "vxn_scene_stream",
     "vxn_hbo_create", "vxn_hbo_free", "vxn_render", "vxn_traverse", "vxn_context",
 ]
 
@@ -200,6 +201,9 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_render", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32, P, P,
              C.POINTER(vxa_stats))
     _declare(lib, "vxa_submit", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32)
+    _declare(lib, "vxa_submit_readback", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32, P,
+             C.POINTER(u64))
+    _declare(lib, "vxa_wait_readback", i, P, u64)
     _declare(lib, "vxa_hbo_create", i, P, C.c_int32, C.c_int32, C.POINTER(u32))
     _declare(lib, "vxa_hbo_release", i, P, u32)
     _declare(lib, "vxa_hbo_download", i, P, u32, P)
@@ -248,6 +252,7 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
              C.POINTER(u32))
     _declare(lib, "vxn_scene_free", None, P)
     _declare(lib, "vxn_scene_submit", i, P, d, i, i, i, u32)
+    _declare(lib, "vxn_scene_stream", i, P, d, i, P, C.POINTER(u64))
     _declare(lib, "vxn_hbo_create", P, i, i)
     _declare(lib, "vxn_hbo_free", None, P)
     _declare(lib, "vxn_render", i, P, i, i, i, P, P, P, C.POINTER(u64), C.POINTER(d), C.POINTER(vxa_stats))

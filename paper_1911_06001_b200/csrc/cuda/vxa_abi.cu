@@ -165,6 +165,11 @@ struct vxa_ctx {
     DevBuf<VisitOut> visits;
 
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, t_a = nullptr, t_b = nullptr;
+    // streaming readback: RGB8 staging ring on a copy stream
+    cudaStream_t copy_stream = nullptr;
+    DevBuf<uint8_t> rb_rgb[2];
+    cudaEvent_t rb_packed[2] = {nullptr, nullptr}, rb_done[2] = {nullptr, nullptr};
+    uint64_t rb_next = 0; // next ticket
     int occ[2][2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][compact][stack height]
 
     // Frame-kernel timing ring: events recorded tight around every frame
@@ -470,6 +475,12 @@ int vxa_create(int device, vxa_ctx** out) {
         VXA_CUDA(cudaEventCreateWithFlags(&ctx->inst_done[s], cudaEventDisableTiming));
         VXA_CUDA(cudaEventRecord(ctx->inst_done[s], ctx->stream));
     }
+    VXA_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        VXA_CUDA(cudaEventCreateWithFlags(&ctx->rb_packed[k], cudaEventDisableTiming));
+        VXA_CUDA(cudaEventCreateWithFlags(&ctx->rb_done[k], cudaEventDisableTiming));
+        VXA_CUDA(cudaEventRecord(ctx->rb_done[k], ctx->copy_stream));
+    }
     VXA_CUDA(cudaEventCreate(&ctx->ev_a));
     VXA_CUDA(cudaEventCreate(&ctx->ev_b));
     VXA_CUDA(cudaEventCreate(&ctx->t_a));
@@ -511,6 +522,13 @@ int vxa_destroy(vxa_ctx* ctx) {
         if (ctx->k_begin[i]) cudaEventDestroy(ctx->k_begin[i]);
         if (ctx->k_end[i]) cudaEventDestroy(ctx->k_end[i]);
     }
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    for (int k = 0; k < 2; ++k) {
+        ctx->rb_rgb[k].release();
+        if (ctx->rb_packed[k]) cudaEventDestroy(ctx->rb_packed[k]);
+        if (ctx->rb_done[k]) cudaEventDestroy(ctx->rb_done[k]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return VXA_OK;
@@ -758,6 +776,35 @@ int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         hbo = it->second.rec;
     }
     return enqueue_any(ctx, f, in, n, nullptr, hbo, false);
+}
+
+int vxa_submit_readback(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n,
+                        uint8_t* rgb_out, uint64_t* ticket) {
+    if (ctx == nullptr || rgb_out == nullptr || ticket == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    if (int rc = vxa_submit(ctx, f, in, n); rc != VXA_OK) return rc;
+    const size_t npix = static_cast<size_t>(f->camera.width) * f->camera.height;
+    const int slot = static_cast<int>(ctx->rb_next & 1u);
+    VXA_CUDA(ctx->rb_rgb[slot].ensure(npix * 3 + 16));
+    // the slot's previous D2H must be done before the pack overwrites it
+    VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->rb_done[slot], 0));
+    const size_t quads = (npix + 3) / 4;
+    pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rb_rgb[slot].ptr, npix);
+    VXA_CUDA(cudaGetLastError());
+    VXA_CUDA(cudaEventRecord(ctx->rb_packed[slot], ctx->stream));
+    VXA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->rb_packed[slot], 0));
+    VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rb_rgb[slot].ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    VXA_CUDA(cudaEventRecord(ctx->rb_done[slot], ctx->copy_stream));
+    ctx->d2h += npix * 3;
+    *ticket = ctx->rb_next++;
+    return VXA_OK;
+}
+
+int vxa_wait_readback(vxa_ctx* ctx, uint64_t ticket) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    if (ticket >= ctx->rb_next) return fail(VXA_ERR_INVALID, "unknown readback ticket");
+    if (ticket + 2 < ctx->rb_next) return VXA_OK; // its slot has been reused: already complete
+    VXA_CUDA(cudaEventSynchronize(ctx->rb_done[ticket & 1u]));
+    return VXA_OK;
 }
 
 int vxa_synchronize(vxa_ctx* ctx) {

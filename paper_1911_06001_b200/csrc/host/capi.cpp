@@ -236,6 +236,25 @@ int vxn_scene_submit(vxn_scene* s, double time, int precision, int rank, int wor
         -1);
 }
 
+int vxn_scene_stream(vxn_scene* s, double time, int precision, uint8_t* rgb_out, uint64_t* ticket) {
+    return guard(
+        [&] {
+            if (time >= 0.0) voxanim::evaluate_animation(s->s, time);
+            thread_local std::vector<vxa_instance> inst;
+            inst.resize(s->s.objects.size());
+            vxa_frame_desc f;
+            export_frame(s->s, &f);
+            export_instances(s->s, inst.data());
+            f.precision = static_cast<std::uint8_t>(precision);
+            voxanim::gpu::check(vxa_submit_readback(voxanim::gpu::context(), &f, inst.data(),
+                                                    static_cast<std::uint32_t>(inst.size()), rgb_out, ticket),
+                                "vxa_submit_readback");
+            voxanim::mark_clean(s->s);
+            return 0;
+        },
+        -1);
+}
+
 int vxn_scene_export(vxn_scene* s, vxa_frame_desc* f, vxa_instance* inst, uint32_t cap, uint32_t* count) {
     return guard(
         [&] {

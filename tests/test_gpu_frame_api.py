@@ -153,3 +153,32 @@ def test_device_hit_buffer_matches_host_hit_buffer(gpu, precision):
     assert lib.vxa_hbo_download(ctx, handle.value, recs) == 0
     assert any(r.kind != 0 for r in recs)
     assert lib.vxa_hbo_release(ctx, handle.value) == 0
+
+
+def test_streaming_readback_matches_synchronous_frames(gpu):
+    """vxa_submit_readback (frame k's D2H overlapping frame k+1) delivers the same
+    images as synchronous render_frame calls."""
+    lib = vx.vxa()
+    ctx = vx.context()
+    model = vx.Model.procedural(8, shell=True)
+    s_stream = vx.Scene(vx.config.C4, [model], 0, 640, 360)
+    s_sync = vx.Scene(vx.config.C4, [model], 0, 640, 360)
+    vxl = vx.voxanim()
+    bufs = [np.zeros((360, 640, 3), np.uint8) for _ in range(2)]
+    for b in bufs:
+        assert lib.vxa_host_register(ctx, b.ctypes.data, b.nbytes) == 0
+    tickets, frames = [], []
+    t = C.c_uint64()
+    for k in range(6):
+        assert vxl.vxn_scene_stream(s_stream._h, k / 30.0, vx.VXA_FP32, bufs[k % 2].ctypes.data, C.byref(t)) == 0
+        tickets.append(t.value)
+        s_sync.evaluate(k / 30.0)
+        frames.append(s_sync.render(precision=vx.VXA_FP32)[0])
+        s_sync.mark_clean()
+        if k >= 1:
+            assert lib.vxa_wait_readback(ctx, tickets[k - 1]) == 0
+            assert (bufs[(k - 1) % 2] == frames[k - 1]).all(), k - 1
+    assert lib.vxa_wait_readback(ctx, tickets[-1]) == 0
+    assert (bufs[5 % 2] == frames[5]).all()
+    for b in bufs:
+        lib.vxa_host_unregister(ctx, b.ctypes.data)
