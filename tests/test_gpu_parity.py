@@ -138,3 +138,16 @@ def test_node_word_formats_agree(gpu, words, monkeypatch):
     o.evaluate(0.9)
     o_aov, o_img = check_fp64(s, o)
     check_fp32(s, o, o_aov, o_img)
+
+
+@pytest.mark.parametrize("cfg,t", [(vx.config.C2, 1.7), (vx.config.C4, 2.3)])
+def test_full_size_frame(gpu, cfg, t):
+    """BASELINE configurations at their full resolution (C2 1920x1080 depth 10,
+    C4 3840x2160 with 64 depth-11 instances): FP64 bit-exact, FP32 ties only."""
+    depth = 10 if cfg == vx.config.C2 else 11
+    s, o = pair(cfg, [vx.Model.procedural(depth, shell=True)])
+    s.evaluate(t)
+    o.evaluate(t)
+    o_aov, o_img = check_fp64(s, o)
+    ties, n_hit = check_fp32(s, o, o_aov, o_img)
+    print(f"config {cfg}: {n_hit} hit pixels, {ties} FP32 ties ({100.0 * ties / n_hit:.4f} %)")
