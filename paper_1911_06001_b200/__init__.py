@@ -60,6 +60,8 @@ class config:  # bench_scenes.hpp
     SORTED_TRACING = 6
     TWO_OBJECTS = 7
     HBO = 8
+    AXIS_ALIGNED = 9
+    MANY = 10
 
 
 class Model:

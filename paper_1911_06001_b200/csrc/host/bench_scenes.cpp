@@ -167,6 +167,32 @@ Scene make_config_scene(int config, const std::vector<std::shared_ptr<const SvoM
         w = 96, h = 64;
         break;
     }
+    case kAxisAligned: {
+        s.objects.push_back(object(0, models[0], RigidTransform{}));
+        RigidTransform tf;
+        tf.translation = {0.75, -0.25, -1.0};
+        tf.scale = {0.5, 1.0, 0.75};
+        s.objects.push_back(object(1, models.size() > 1 ? models[1] : models[0], tf));
+        s.camera = make_look_at_camera({0, 0, 3}, {0, 0, 0}, {0, 1, 0}, 60, 101, 101);
+        s.background = {5, 5, 5};
+        w = 101, h = 101;
+        break;
+    }
+    case kManyInstances: {
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> jitter(-0.2, 0.2), scl(0.3, 0.6);
+        for (int i = 0; i < 200; ++i) {
+            RigidTransform tf;
+            tf.translation = {(i % 20 - 9.5) * 0.45 + jitter(rng), (i / 20 - 4.5) * 0.45 + jitter(rng),
+                              -0.6 * (i % 7) + jitter(rng)};
+            tf.scale = {scl(rng), scl(rng), scl(rng)};
+            tf.rotation = rotation_from_quaternion(unit_quaternion(rng));
+            s.objects.push_back(object(i, models[static_cast<std::size_t>(i) % models.size()], tf));
+        }
+        s.camera = make_look_at_camera({0, 0, 6}, {0, 0, -1}, {0, 1, 0}, 70, 320, 180);
+        w = 320, h = 180;
+        break;
+    }
     default:
         throw std::invalid_argument("make_config_scene: unknown configuration " + std::to_string(config));
     }

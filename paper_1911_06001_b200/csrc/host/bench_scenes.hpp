@@ -23,6 +23,9 @@ enum SceneConfig : int {
     kSortedTracing = 6,    // reference test_renderer.cpp:166-179 layout (D, B, A, C along +x)
     kTwoObjects = 7,       // reference test_renderer.cpp:285-293 layout
     kHboScene = 8,         // kTwoObjects + models[1] at (0, 1.5, 1) (test_renderer.cpp:371-374)
+    kAxisAligned = 9,      // camera on the z axis, odd resolution: a row and a column of rays with
+                           // exactly zero local direction components (zero-direction convention)
+    kManyInstances = 10,   // 4 x models.size() x 50 instances on a grid (wide candidate lists)
 };
 
 // models: C1-C4 use models[0]; kRandomScene uses every model; kSortedTracing

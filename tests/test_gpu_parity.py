@@ -151,3 +151,46 @@ def test_full_size_frame(gpu, cfg, t):
     o_aov, o_img = check_fp64(s, o)
     ties, n_hit = check_fp32(s, o, o_aov, o_img)
     print(f"config {cfg}: {n_hit} hit pixels, {ties} FP32 ties ({100.0 * ties / n_hit:.4f} %)")
+
+
+def test_axis_aligned_camera_zero_direction_rays(gpu):
+    """Odd resolution on the z axis with identity transforms: the middle row and
+    column carry exactly-zero local direction components (traversal.cpp:19-21,
+    135-140 zero-direction convention)."""
+    s, o = pair(vx.config.AXIS_ALIGNED, [vx.Model.procedural(6, shell=False), vx.Model.random(9, 4, 0.3)])
+    o_aov, o_img = check_fp64(s, o)
+    assert (o_aov["object_id"][50, :] >= 0).sum() > 10  # the zero-direction row hits
+    check_fp32(s, o, o_aov, o_img)
+
+
+def test_many_instances_overflow_the_tile_list(gpu):
+    """200 instances: tiles whose cone meets more than 64 instances fall back to
+    the per-ray pass over every instance; results stay parity-clean."""
+    models = [vx.Model.procedural(6, shell=True), vx.Model.random(4, 4, 0.2)]
+    s, o = pair(vx.config.MANY, models, seed=3)
+    for culling, sorting in ((True, True), (True, False)):
+        o_aov, o_img = check_fp64(s, o, culling, sorting)
+        check_fp32(s, o, o_aov, o_img, culling, sorting)
+
+
+def test_deep_model_depth_12(gpu):
+    """A depth-12 shell (21 M nodes, 44 M attributes -- past the compact words'
+    2^24 range, so the general words run at scale): FP64 per-ray bit-exact vs the
+    reference, and a frame through both kernels."""
+    m = vx.Model.procedural(12, shell=True)
+    rm = ref.RefModel.from_bytes(m.serialize())
+    rng = np.random.default_rng(13)
+    n = 4000
+    rays = np.zeros(n, vx.RAY_DTYPE)
+    rays["origin"] = rng.uniform(-2, 2, (n, 3))
+    tgt = rng.uniform(-0.3, 0.3, (n, 3))
+    d = tgt - rays["origin"]
+    rays["direction"] = d / np.linalg.norm(d, axis=1, keepdims=True)
+    rays["half_extent"] = (0.5, 0.5, 0.5)
+    ours, theirs = vx.traverse(m, rays), ref.traverse(rm, rays, with_fetches=True)
+    assert ours["hit"].mean() > 0.5
+    for k in ("hit", "t_hit", "leaf_path", "path_len", "node_index", "attr_index", "node_fetches"):
+        assert (ours[k] == theirs[k]).all(), k
+    s, o = pair(vx.config.C1, [m], w=128, h=128)
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img)
