@@ -268,6 +268,23 @@ Interval voxel_interval(const SceneObject& obj, const Ray& world, const uint32_t
     return iv;
 }
 
+// A zero-direction axis whose origin lies on (or within FP32 resolution of)
+// one of the voxel's boundary planes: the ray runs along the face between two
+// voxel rows, and which row owns it is the half-open convention's tie.
+bool on_zero_dir_face(const SceneObject& obj, const Ray& world, const uint32_t v[3], uint32_t level) {
+    const Ray r = transform_ray_world_to_local(world, obj.transform);
+    const OctreeBounds b = bounds_from_scale(obj.transform.scale);
+    for (int a = 0; a < 3; ++a) {
+        if (std::abs(r.direction[a]) > 1e-6) continue;
+        const double h = b.half_extent[a];
+        const double cell = 2.0 * h / std::ldexp(1.0, static_cast<int>(level));
+        const double lo = -h + v[a] * cell, hi = lo + cell;
+        const double eps = std::ldexp(std::abs(r.origin[a]) + 2.0 * h, -20);
+        if (std::abs(r.origin[a] - lo) <= eps || std::abs(r.origin[a] - hi) <= eps) return true;
+    }
+    return false;
+}
+
 bool sphere_grazed(const SceneObject& obj, const Ray& ray, double t_ref) {
     const BoundingSphere s = bounding_sphere(obj);
     const Vec3 l = s.center - ray.origin;
@@ -334,6 +351,8 @@ int classify_pixel(const Scene& scene, const Ray& ray, const AovRec& o, const Ao
     // sphere / box grazes of either instance
     for (const SceneObject* obj : {oo, og})
         if (obj && (sphere_grazed(*obj, ray, tref) || box_grazed(*obj, ray, tref))) return 1;
+    if ((oo && on_zero_dir_face(*oo, ray, o.voxel, o.level)) || (og && on_zero_dir_face(*og, ray, g.voxel, g.level)))
+        return 1;
     Interval vo, vg;
     if (oo) {
         vo = voxel_interval(*oo, ray, o.voxel, o.level);

@@ -82,9 +82,21 @@ __device__ __forceinline__ SphereRes<Real> sphere_test(const DevInstance<Real>& 
 // in FP64 and rounded once: a plane entry t = (A + i s) / d_a is only as
 // accurate as the small component d_a.
 struct RayD {
-    int px, py;
-    double rnd;
+    double dcx, dcy; // camera-space direction (z = -1), reference NDC arithmetic
+    double rnd;      // 1 / |(dcx, dcy, -1)|
 };
+
+// FP64 camera-space direction of pixel (px, py) with the reference's NDC
+// arithmetic (renderer.cpp:19-21, divisions included): a centre row/column
+// yields an exact 0 like the reference does, so zero-direction rays stay zero.
+template <typename Real>
+__device__ __forceinline__ void camera_dir_f64(const FrameParams<Real>& p, int px, int py, RayD& rd) {
+    const double ndc_x = (px + 0.5) / p.width * 2.0 - 1.0;
+    const double ndc_y = 1.0 - (py + 0.5) / p.height * 2.0;
+    rd.dcx = ndc_x * p.d_sy * p.d_aspect;
+    rd.dcy = ndc_y * p.d_sy;
+    rd.rnd = rsqrt(fma(rd.dcx, rd.dcx, fma(rd.dcy, rd.dcy, 1.0)));
+}
 
 // ---- FP32 tile culling --------------------------------------------------------
 // All rays of an 8x4 tile leave the camera inside one cone (axis: the tile's
@@ -156,11 +168,9 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         t = h.t, axis = h.axis, attr = h.attr, parent = h.parent, level = h.level;
         if constexpr (kAov) path_to_voxel(h.path, h.level, vox);
     } else {
-        const double dcx = fma(static_cast<double>(rd.px) + 0.5, p.d_inv_w2, -1.0) * p.d_sx;
-        const double dcy = fma(-(static_cast<double>(rd.py) + 0.5), p.d_inv_h2, 1.0) * p.d_sy;
         float d[3];
         for (int k = 0; k < 3; ++k)
-            d[k] = static_cast<float>((fma(in.Md[3 * k], dcx, in.Md[3 * k + 1] * dcy) - in.Md[3 * k + 2]) * rd.rnd);
+            d[k] = static_cast<float>((fma(in.Md[3 * k], rd.dcx, in.Md[3 * k + 1] * rd.dcy) - in.Md[3 * k + 2]) * rd.rnd);
         FastRay fr;
         if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits)) return;
         FastHit h;
@@ -272,11 +282,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
             const float dcy = fmaf(-(static_cast<float>(py) + 0.5f), p.inv_h2, 1.0f) * p.sy;
             const float rn = rsqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
             for (int k = 0; k < 3; ++k) dw[k] = (p.C[3 * k] * dcx + p.C[3 * k + 1] * dcy - p.C[3 * k + 2]) * rn;
-            const double ddx = fma(static_cast<double>(px) + 0.5, p.d_inv_w2, -1.0) * p.d_sx;
-            const double ddy = fma(-(static_cast<double>(py) + 0.5), p.d_inv_h2, 1.0) * p.d_sy;
-            rd.px = px;
-            rd.py = py;
-            rd.rnd = rsqrt(fma(ddx, ddx, fma(ddy, ddy, 1.0)));
+            camera_dir_f64(p, px, py, rd);
         }
 
         // ---- sphere pass: count hits, remember the single hit (HBO rule)

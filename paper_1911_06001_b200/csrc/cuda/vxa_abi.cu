@@ -277,10 +277,8 @@ template <typename Real> void fill_camera(FrameParams<Real>& p, const vxa_frame_
     p.inv_h2 = static_cast<Real>(2.0 / c.height);
     p.sx = static_cast<Real>(tan_half * aspect);
     p.sy = static_cast<Real>(tan_half);
-    p.d_inv_w2 = 2.0 / c.width;
-    p.d_inv_h2 = 2.0 / c.height;
-    p.d_sx = tan_half * aspect;
     p.d_sy = tan_half;
+    p.d_aspect = aspect;
     p.width = c.width;
     p.height = c.height;
 }

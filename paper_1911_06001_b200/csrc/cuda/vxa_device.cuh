@@ -130,7 +130,7 @@ template <typename Real> struct FrameParams {
     Real aspect;       // (double)W / H
     Real inv_w2, inv_h2; // FP32 ray setup: 2/W, 2/H
     Real sx, sy;       // FP32 ray setup: tan_half * aspect, tan_half
-    double d_inv_w2, d_inv_h2, d_sx, d_sy; // the same in FP64 (FP32 kernel's local directions)
+    double d_sy, d_aspect; // tan_half and aspect in FP64 (FP32 kernel's local directions)
     uint32_t background; // RGBA8
     uint32_t culling, sorting, sphere_pass;
     uint32_t camera_dirty;
