@@ -160,7 +160,8 @@ def test_axis_aligned_camera_zero_direction_rays(gpu):
     s, o = pair(vx.config.AXIS_ALIGNED, [vx.Model.procedural(6, shell=False), vx.Model.random(9, 4, 0.3)])
     o_aov, o_img = check_fp64(s, o)
     assert (o_aov["object_id"][50, :] >= 0).sum() > 10  # the zero-direction row hits
-    check_fp32(s, o, o_aov, o_img)
+    # the centre row/column run exactly along cell faces: ties by construction
+    check_fp32(s, o, o_aov, o_img, max_tie_frac=0.02)
 
 
 def test_many_instances_overflow_the_tile_list(gpu):
