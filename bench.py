@@ -85,7 +85,31 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    # NVML clocks-event reason bits (nvml.h: nvmlClocksEventReason*)
+    NVML_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4}
+
+    def _poll_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                bits = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if bits & self.NVML_BITS[n] else "Not Active" for n in self.NAMES])
+                self._stop.wait(0.005)
+        finally:
+            pynvml.nvmlShutdown()
+
     def _poll(self):
+        try:
+            import pynvml  # noqa: F401  (nvidia_ml_py)
+            return self._poll_nvml()
+        except Exception:
+            self.samples = []
         cmd = ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
                "--format=csv,noheader,nounits"]
         while not self._stop.is_set():
@@ -121,6 +145,47 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- helpers
+
+def model_build_bench(lib, ctx, reps: int = 5) -> dict:
+    """build_from_grid on the device (vxa_build_model)
+    for the reference's dense sphere grid at depth 10 (1024^3 bitset, 128 MiB,
+    page-locked host memory; timed: H2D of the grid + every build kernel), next
+    to the product's host builder at depth 10 and the reference's own
+    build_from_grid at depth 8 (C1's model; at depth 10 it needs ~48 s / 15 GB)."""
+    import paper_1911_06001_b200 as vx
+
+    def check(rc, what):
+        if rc != 0:
+            raise RuntimeError(f"{what}: {lib.vxa_last_error().decode()}")
+
+    out = {}
+    for depth in (8, 10):
+        words, gd = vx.grid_primitive("sphere", depth)
+        check(lib.vxa_host_register(ctx, words.ctypes.data, words.nbytes), "host_register")
+        times = []
+        h, nn, na = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        for _ in range(reps + 1):
+            t0 = time.perf_counter()
+            check(lib.vxa_build_model(ctx, words.ctypes.data, gd, 0, 0, C.byref(h), C.byref(nn), C.byref(na)),
+                  "build_model")
+            times.append((time.perf_counter() - t0) * 1e3)
+            lib.vxa_release_model(ctx, h.value)
+        lib.vxa_host_unregister(ctx, words.ctypes.data)
+        row = {"grid_bytes": int(words.nbytes), "nodes": nn.value, "attributes": na.value,
+               "device_ms": round(statistics.median(times[1:]), 3)}
+        t0 = time.perf_counter()
+        vx.Model.from_grid(words, gd, device=False)
+        row["host_builder_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        if depth == 8:
+            from oracle import ref  # CPU baseline of this row: the reference itself
+            t0 = time.perf_counter()
+            ref.RefModel.dense_sphere(8)  # gen_primitive + build_from_grid (gen is ~5% of it)
+            row["reference_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        out[f"sphere_depth{depth}"] = row
+    out["path"] = ("vxa_build_model: grid H2D, Morton leaf masks, mask pyramid, per-level popcount, "
+                   "exclusive scan, emission of 12-byte records + compact words + attributes, wide repack")
+    return out
+
 
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -474,6 +539,7 @@ def run_ours(args):
                             "traversals_per_frame": int(stx.svo_traversals // steps_x)}
         extras["animated_vs_static"] = round(extras["c2_animated_1080p"]["ms_per_frame"] /
                                              extras["c3_static_1080p"]["ms_per_frame"], 4)
+        extras["model_build"] = model_build_bench(lib, ctx)
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

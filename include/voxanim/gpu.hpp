@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "vxa.h"
+#include "voxanim/ingest.hpp"
 #include "voxanim/renderer.hpp"
 
 namespace voxanim::gpu {
@@ -47,6 +48,11 @@ vxa_ctx* context();
 // the model's storage (node/attribute buffers, sizes, depth) plus a content
 // signature, so distinct models never alias.
 std::uint32_t model_handle(const SvoModel& model);
+
+// voxanim::build_from_grid on the device (vxa_build_model): the same SvoModel,
+// byte for byte, built in HBM and copied back; the device copy is kept in the
+// model cache, so rendering the returned model does not upload it again.
+SvoModel build_from_grid(const VoxelGrid& grid, std::uint32_t depth);
 
 // Translates a vxa_status into the API's exception types (throws unless VXA_OK).
 void check(int status, const char* what);

@@ -31,6 +31,14 @@ vxn_model* vxn_model_procedural(int shell, uint32_t depth);      /* sparse build
 vxn_model* vxn_model_dense_sphere(uint32_t depth);               /* build_from_grid(gen_primitive(Sphere)) */
 vxn_model* vxn_model_random(uint64_t seed, uint32_t depth, double fill); /* mt19937_64 random grid */
 vxn_model* vxn_model_full_cube(void);                            /* depth-1 model, all 8 voxels */
+/* build_from_grid of a dense VoxelGrid bitset ((n^3+63)/64 words, n = 2^depth, x-major)
+ * with ColorSpec{color_mode, color_rgba}; device != 0 builds it on the GPU (vxa_build_model). */
+vxn_model* vxn_model_from_grid(const uint64_t* words, uint32_t depth, uint32_t color_mode, uint32_t color_rgba,
+                               int device);
+/* gen_primitive(kind, depth) bitset (kind: 0 Sphere, 1 BoxShell, 2 Menger, 3 Checker) into out
+ * (cap_words words; out may be NULL to query); *grid_depth = log2 of its resolution (Menger:
+ * 3^depth rounded up to a power of two). Returns the word count, or -1. */
+int64_t vxn_grid_primitive(int kind, uint32_t depth, uint64_t* out, size_t cap_words, uint32_t* grid_depth);
 vxn_model* vxn_model_deserialize(const uint8_t* bytes, size_t n);
 int64_t vxn_model_serialize(const vxn_model* m, uint8_t* out, size_t cap); /* returns the size */
 int vxn_model_info(const vxn_model* m, uint32_t* depth, uint64_t* nodes, uint64_t* attrs);

@@ -73,6 +73,25 @@ int vxa_release_model(vxa_ctx* ctx, uint32_t handle);
  * and which packed format was chosen (1 = 4-byte words, 2 = 8-byte words). */
 int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32_t* node_format);
 
+/* Device model build: replaces voxanim::build_from_grid (reference
+ * proj/include/voxanim/svo.hpp:62, proj/src/svo.cpp:52-132) for a dense grid.
+ * grid_words: host copy of a VoxelGrid bitset (proj/include/voxanim/ingest.hpp:34-63:
+ * resolution n = 2^depth, bit (x*n + y)*n + z of 64-bit words, (n^3+63)/64 words);
+ * depth in [1, 10] (the dense-grid cap, ingest.cpp:15). color_mode: the grid's
+ * ColorSpec (0 PositionHash, 1 ByHeight, 2 Constant with color_rgba = r | g<<8 |
+ * b<<16 | a<<24). The model is built in device memory (same node and attribute
+ * numbering as the reference, byte for byte) and registered like an upload;
+ * node_count / attr_count (optional) receive its size. The context keeps its
+ * build scratch (grid staging, occupancy pyramid, level lists; ~1.5 GB after a
+ * depth-10 build) for the next build until vxa_destroy. */
+int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, uint32_t color_mode,
+                    uint32_t color_rgba, uint32_t* handle_out, uint64_t* node_count, uint64_t* attr_count);
+/* Copy a device model's 12-byte SvoNode records and attributes to host memory
+ * (either pointer may be null; capacities in elements). */
+int vxa_model_download(vxa_ctx* ctx, uint32_t handle, void* nodes, uint64_t node_cap, uint32_t* attrs,
+                       uint64_t attr_cap);
+int vxa_model_counts(vxa_ctx* ctx, uint32_t handle, uint32_t* depth, uint64_t* node_count, uint64_t* attr_count);
+
 /* ---- frame -------------------------------------------------------------- */
 
 /* voxanim::Camera (proj/include/voxanim/scene.hpp:35-42). */

@@ -57,6 +57,7 @@ def lib() -> C.CDLL:
             "vref_model_dense_sphere": (P, u32),
             "vref_model_shell_grid": (P, u32),
             "vref_model_random": (P, u64, u32, d),
+            "vref_model_from_grid": (P, P, u32, u32, u32),
             "vref_model_serialize": (C.c_int64, P, P, C.c_size_t),
             "vref_model_free": (None, P),
             "vref_scene_config": (P, i, C.POINTER(P), u32, u64, i, i),
@@ -117,6 +118,13 @@ class RefModel:
     @classmethod
     def random(cls, seed, depth, fill):
         return cls(lib().vref_model_random(seed, depth, fill))
+
+    @classmethod
+    def from_grid(cls, words, depth, color_mode=0, color_rgba=0xFFC8C8C8):
+        """The reference build_from_grid of a VoxelGrid bitset (numpy uint64 words)."""
+        import numpy as np
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        return cls(lib().vref_model_from_grid(w.ctypes.data, depth, color_mode, color_rgba))
 
     def serialize(self) -> bytes:
         n = lib().vref_model_serialize(self._h, None, 0)

@@ -418,6 +418,30 @@ VREF_API vref_model* vref_model_shell_grid(uint32_t depth) {
         (vref_model*)nullptr);
 }
 
+// The reference's own build_from_grid (svo.cpp:80-132) on a caller-supplied
+// VoxelGrid bitset (x-major, (n^3+63)/64 words) and ColorSpec.
+VREF_API vref_model* vref_model_from_grid(const uint64_t* words, uint32_t depth, uint32_t color_mode, uint32_t rgba) {
+    return guard(
+        [&] {
+            ColorSpec cs;
+            cs.mode = static_cast<ColorMode>(color_mode);
+            cs.constant = {static_cast<uint8_t>(rgba), static_cast<uint8_t>(rgba >> 8), static_cast<uint8_t>(rgba >> 16),
+                           static_cast<uint8_t>(rgba >> 24)};
+            const uint32_t n = 1u << depth;
+            VoxelGrid g(n, cs);
+            const uint64_t bits = uint64_t{n} * n * n;
+            for (uint64_t w = 0; w < (bits + 63) / 64; ++w)
+                for (uint64_t v = words[w]; v; v &= v - 1) {
+                    const uint64_t i = 64 * w + static_cast<uint64_t>(__builtin_ctzll(v));
+                    if (i >= bits) break;
+                    g.set(static_cast<uint32_t>(i / (uint64_t{n} * n)), static_cast<uint32_t>((i / n) % n),
+                          static_cast<uint32_t>(i % n));
+                }
+            return wrap(build_from_grid(g, depth));
+        },
+        (vref_model*)nullptr);
+}
+
 VREF_API vref_model* vref_model_random(uint64_t seed, uint32_t depth, double fill) {
     return guard(
         [&] {

@@ -89,6 +89,18 @@ class Model:
         return cls(voxanim().vxn_model_full_cube())
 
     @classmethod
+    def from_grid(cls, words, depth: int, color_mode: int = 0, color_rgba: int = 0xFFC8C8C8,
+                  device: bool = True) -> "Model":
+        """build_from_grid of a VoxelGrid bitset (uint64 words, x-major); on the
+        GPU (vxa_build_model) unless device=False."""
+        import numpy as np
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        n = 1 << depth
+        if w.size != (n ** 3 + 63) // 64:
+            raise VoxanimError(f"grid has {w.size} words, expected {(n ** 3 + 63) // 64}")
+        return cls(voxanim().vxn_model_from_grid(w.ctypes.data, depth, color_mode, color_rgba, 1 if device else 0))
+
+    @classmethod
     def from_bytes(cls, data: bytes) -> "Model":
         buf = C.create_string_buffer(data, len(data))
         return cls(voxanim().vxn_model_deserialize(buf, len(data)))
@@ -113,6 +125,23 @@ class Model:
         if getattr(self, "_h", None) and _VX is not None:
             _VX.vxn_model_free(self._h)
             self._h = None
+
+
+PRIMITIVES = {"sphere": 0, "box_shell": 1, "menger": 2, "checker": 3}
+
+
+def grid_primitive(kind: str, depth: int):
+    """gen_primitive(kind, depth) as (VoxelGrid bitset as numpy uint64 words,
+    grid depth = log2 of its resolution)."""
+    import numpy as np
+    gd = C.c_uint32()
+    n = voxanim().vxn_grid_primitive(PRIMITIVES[kind], depth, None, 0, C.byref(gd))
+    if n < 0:
+        raise VoxanimError(_err())
+    out = np.zeros(n, np.uint64)
+    if voxanim().vxn_grid_primitive(PRIMITIVES[kind], depth, out.ctypes.data, out.size, C.byref(gd)) < 0:
+        raise VoxanimError(_err())
+    return out, gd.value
 
 
 class HitBuffer:

@@ -161,7 +161,8 @@ except ImportError:  # pragma: no cover
 # Every symbol include/vxa.h declares (checked by tests/test_abi.py).
 VXA_SYMBOLS = [
     "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
-    "vxa_upload_model", "vxa_release_model", "vxa_model_info",
+    "vxa_upload_model", "vxa_release_model", "vxa_model_info", "vxa_build_model", "vxa_model_download",
+    "vxa_model_counts",
     "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_render", "vxa_submit", "vxa_submit_readback",
     "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
@@ -169,7 +170,7 @@ VXA_SYMBOLS = [
 ]
 VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
-    "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
+    "vxn_model_from_grid", "vxn_grid_primitive", "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
     "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit", "vxn_scene_stream",
     "vxn_hbo_create", "vxn_hbo_free", "vxn_render", "vxn_traverse", "vxn_context",
@@ -198,6 +199,9 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_upload_model", i, P, P, u32, P, u32, u32, C.POINTER(u32))
     _declare(lib, "vxa_release_model", i, P, u32)
     _declare(lib, "vxa_model_info", i, P, u32, C.POINTER(u64), C.POINTER(u32))
+    _declare(lib, "vxa_build_model", i, P, P, u32, u32, u32, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))
+    _declare(lib, "vxa_model_download", i, P, u32, P, u64, P, u64)
+    _declare(lib, "vxa_model_counts", i, P, u32, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))
     _declare(lib, "vxa_render", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32, P, P,
              C.POINTER(vxa_stats))
     _declare(lib, "vxa_submit", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32)
@@ -236,6 +240,8 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_model_dense_sphere", P, u32)
     _declare(lib, "vxn_model_random", P, u64, u32, d)
     _declare(lib, "vxn_model_full_cube", P)
+    _declare(lib, "vxn_model_from_grid", P, P, u32, u32, u32, i)
+    _declare(lib, "vxn_grid_primitive", C.c_int64, i, u32, P, C.c_size_t, C.POINTER(u32))
     _declare(lib, "vxn_model_deserialize", P, P, C.c_size_t)
     _declare(lib, "vxn_model_serialize", C.c_int64, P, P, C.c_size_t)
     _declare(lib, "vxn_model_info", i, P, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))

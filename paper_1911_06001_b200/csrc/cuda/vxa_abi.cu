@@ -10,6 +10,7 @@
 #include "vxa.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -105,7 +106,27 @@ struct ModelEntry {
     uint32_t* cwords = nullptr; // compact words when the model is canonical
     uint32_t* side = nullptr;
     uint32_t* attrs = nullptr;
+    uint32_t* raw = nullptr; // the 12-byte SvoNode records (vxa_model_download)
+    void* block = nullptr;   // device-built models: one allocation holds all of the above
+    uint64_t attr_count = 0;
     uint64_t bytes = 0;
+    void free_all() {
+        if (block) {
+            cudaFree(block);
+        } else {
+            cudaFree(words);
+            cudaFree(cwords);
+            cudaFree(side);
+            cudaFree(attrs);
+            cudaFree(raw);
+        }
+        block = nullptr;
+        words = nullptr;
+        cwords = nullptr;
+        side = nullptr;
+        attrs = nullptr;
+        raw = nullptr;
+    }
 };
 
 template <typename T> struct DevBuf {
@@ -136,6 +157,7 @@ struct vxa_ctx {
     cudaStream_t stream = nullptr;
     std::map<uint32_t, ModelEntry> models;
     uint32_t next_handle = 1;
+    BuildScratch build; // vxa_build_model scratch (grid staging, pyramid, level lists)
 
     DevBuf<uint32_t> fb;  // resident RGBA8 framebuffer
     int32_t fb_w = 0, fb_h = 0;
@@ -491,12 +513,10 @@ int vxa_destroy(vxa_ctx* ctx) {
     if (ctx == nullptr) return VXA_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (auto& [h, m] : ctx->models) {
-        cudaFree(m.cwords);
-        cudaFree(m.words);
-        cudaFree(m.side);
-        cudaFree(m.attrs);
-    }
+    for (auto& [h, m] : ctx->models) m.free_all();
+    ctx->build.grid.release();
+    ctx->build.pyramid.release();
+    ctx->build.levels.release();
     if (ctx->peer_fb) cudaIpcCloseMemHandle(ctx->peer_fb);
     for (auto& [h, b] : ctx->hbos) cudaFree(b.rec);
     ctx->fb.release();
@@ -610,12 +630,9 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(raw_dev);
+    m.raw = raw_dev;
     if (e != cudaSuccess) {
-        cudaFree(m.words);
-        cudaFree(m.cwords);
-        cudaFree(m.side);
-        cudaFree(m.attrs);
+        m.free_all();
         return fail(e == cudaErrorMemoryAllocation ? VXA_ERR_OOM : VXA_ERR_CUDA,
                     std::string("model upload: ") + cudaGetErrorString(e));
     }
@@ -625,8 +642,9 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
     m.dev.attrs = m.attrs;
     m.dev.depth = depth;
     m.dev.node_count = node_count;
+    m.attr_count = attr_count;
     m.bytes = sizeof(uint2) * uint64_t{node_count} + (any_mixed ? 4ull * node_count : 0) + 4ull * attr_count +
-              (m.cwords ? 4ull * node_count : 0);
+              (m.cwords ? 4ull * node_count : 0) + raw_bytes;
     const uint32_t handle = ctx->next_handle++;
     ctx->models[handle] = m;
     *handle_out = handle;
@@ -639,10 +657,7 @@ int vxa_release_model(vxa_ctx* ctx, uint32_t handle) {
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    cudaFree(it->second.words);
-    cudaFree(it->second.cwords);
-    cudaFree(it->second.side);
-    cudaFree(it->second.attrs);
+    it->second.free_all();
     ctx->models.erase(it);
     return VXA_OK;
 }
@@ -653,6 +668,88 @@ int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     if (device_bytes) *device_bytes = it->second.bytes;
     if (node_format) *node_format = it->second.cwords ? 1 : 2;
+    return VXA_OK;
+}
+
+int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, uint32_t color_mode,
+                    uint32_t color_rgba, uint32_t* handle_out, uint64_t* node_count, uint64_t* attr_count) {
+    if (ctx == nullptr || handle_out == nullptr || grid_words == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    // build_from_grid's argument checks (svo.cpp:80-87) plus the dense-grid cap (ingest.cpp:15)
+    if (depth < 1 || depth > 10) return fail(VXA_ERR_INVALID, "octree depth must be in [1, 10] for a dense grid");
+    if (color_mode > 2) return fail(VXA_ERR_INVALID, "unknown colour mode");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t n = uint64_t{1} << depth;
+    const size_t grid_bytes = 8 * ((n * n * n + 63) / 64);
+    VXA_CUDA(ctx->build.grid.ensure(grid_bytes));
+    auto* grid_dev = static_cast<uint64_t*>(ctx->build.grid.p);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaMemcpyAsync(grid_dev, grid_words, grid_bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (std::getenv("VOXANIM_BUILD_TRACE")) {
+        cudaStreamSynchronize(ctx->stream);
+        std::fprintf(stderr, "[build] grid H2D     %8.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    BuiltModel b;
+    if (e == cudaSuccess) e = build_svo(ctx->stream, grid_dev, depth, color_mode, color_rgba, ctx->build, b);
+    ModelEntry m;
+    m.block = b.block;
+    m.raw = b.records;
+    m.attrs = b.attrs;
+    m.cwords = b.cwords;
+    m.words = b.words;
+    if (e == cudaSuccess) {
+        // canonical by construction: no mixed nodes, so no side table
+        repack_nodes<<<static_cast<unsigned>((b.node_count + 255) / 256), 256, 0, ctx->stream>>>(
+            m.raw, static_cast<uint32_t>(b.node_count), m.words, nullptr);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(ctx->stream);
+        m.free_all();
+        if (e == cudaErrorInvalidValue) return fail(VXA_ERR_MODEL, "model exceeds 2^32 nodes or attributes");
+        return fail(e == cudaErrorMemoryAllocation ? VXA_ERR_OOM : VXA_ERR_CUDA,
+                    std::string("device model build: ") + cudaGetErrorString(e));
+    }
+    m.dev.words = m.words;
+    m.dev.cwords = m.cwords;
+    m.dev.side = nullptr;
+    m.dev.attrs = m.attrs;
+    m.dev.depth = depth;
+    m.dev.node_count = static_cast<uint32_t>(b.node_count);
+    m.attr_count = b.attr_count;
+    m.bytes = (8 + 12 + (m.cwords ? 4 : 0)) * b.node_count + 4 * b.attr_count;
+    const uint32_t handle = ctx->next_handle++;
+    ctx->models[handle] = m;
+    *handle_out = handle;
+    if (node_count) *node_count = b.node_count;
+    if (attr_count) *attr_count = b.attr_count;
+    return VXA_OK;
+}
+
+int vxa_model_download(vxa_ctx* ctx, uint32_t handle, void* nodes, uint64_t node_cap, uint32_t* attrs,
+                       uint64_t attr_cap) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    const auto it = ctx->models.find(handle);
+    if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
+    const ModelEntry& m = it->second;
+    if ((nodes && node_cap < m.dev.node_count) || (attrs && attr_cap < m.attr_count))
+        return fail(VXA_ERR_INVALID, "output arrays too small");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    if (nodes) VXA_CUDA(cudaMemcpyAsync(nodes, m.raw, 12 * uint64_t{m.dev.node_count}, cudaMemcpyDeviceToHost, ctx->stream));
+    if (attrs && m.attr_count)
+        VXA_CUDA(cudaMemcpyAsync(attrs, m.attrs, 4 * m.attr_count, cudaMemcpyDeviceToHost, ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VXA_OK;
+}
+
+int vxa_model_counts(vxa_ctx* ctx, uint32_t handle, uint32_t* depth, uint64_t* node_count, uint64_t* attr_count) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    const auto it = ctx->models.find(handle);
+    if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
+    if (depth) *depth = it->second.dev.depth;
+    if (node_count) *node_count = it->second.dev.node_count;
+    if (attr_count) *attr_count = it->second.attr_count;
     return VXA_OK;
 }
 

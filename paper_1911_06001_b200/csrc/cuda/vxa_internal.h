@@ -74,4 +74,41 @@ cudaError_t launch_traverse_f64(const DevModel& m, const TraverseRayIn* rays, ui
 cudaError_t launch_traverse_f32(const DevModel& m, const TraverseRayIn* rays, uint32_t n, TraverseRayOut* out,
                                 VisitOut* log, uint32_t log_cap, cudaStream_t s);
 
+// Grow-only device scratch kept by a context between calls.
+struct Arena {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Device build of a dense grid (build.cu; reference svo.cpp:52-132).
+struct BuildScratch {
+    Arena grid, pyramid, levels;
+};
+struct BuiltModel {
+    void* block = nullptr;       // one allocation holding everything below
+    uint32_t* records = nullptr; // 12-byte SvoNode records
+    uint32_t* attrs = nullptr;
+    uint32_t* cwords = nullptr;  // compact render words (null when bases exceed 24 bits)
+    uint2* words = nullptr;      // wide render words (filled by the caller's repack)
+    uint64_t node_count = 0, attr_count = 0;
+};
+// Enqueues the build on s (returns after the level sizes are known; the
+// emission passes are still in flight). On error out.block may be set.
+cudaError_t build_svo(cudaStream_t s, const uint64_t* grid_dev, uint32_t depth, uint32_t color_mode,
+                      uint32_t color_constant, BuildScratch& scratch, BuiltModel& out);
+
 } // namespace vxa

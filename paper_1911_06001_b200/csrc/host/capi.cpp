@@ -9,6 +9,7 @@
 
 #include "bench_scenes.hpp"
 #include "voxanim/gpu.hpp"
+#include "voxanim/ingest.hpp"
 #include "voxanim/procedural.hpp"
 #include "voxanim/renderer.hpp"
 #include "voxanim/svo.hpp"
@@ -89,6 +90,37 @@ vxn_model* vxn_model_full_cube(void) {
             return wrap(voxanim::build_from_grid(g, 1));
         },
         static_cast<vxn_model*>(nullptr));
+}
+
+vxn_model* vxn_model_from_grid(const uint64_t* words, uint32_t depth, uint32_t color_mode, uint32_t color_rgba,
+                               int device) {
+    return guard(
+        [&] {
+            if (words == nullptr || depth < 1 || depth > 10 || color_mode > 2)
+                throw voxanim::ValidationError("vxn_model_from_grid: bad arguments");
+            voxanim::ColorSpec cs;
+            cs.mode = static_cast<voxanim::ColorMode>(color_mode);
+            cs.constant = {static_cast<std::uint8_t>(color_rgba), static_cast<std::uint8_t>(color_rgba >> 8),
+                           static_cast<std::uint8_t>(color_rgba >> 16), static_cast<std::uint8_t>(color_rgba >> 24)};
+            voxanim::VoxelGrid g(1u << depth, cs);
+            g.assign_words(words);
+            return wrap(device ? voxanim::gpu::build_from_grid(g, depth) : voxanim::build_from_grid(g, depth));
+        },
+        static_cast<vxn_model*>(nullptr));
+}
+
+int64_t vxn_grid_primitive(int kind, uint32_t depth, uint64_t* out, size_t cap_words, uint32_t* grid_depth) {
+    return guard(
+        [&]() -> int64_t {
+            if (kind < 0 || kind > 3) throw voxanim::ValidationError("unknown primitive kind");
+            const voxanim::VoxelGrid g = voxanim::gen_primitive(static_cast<voxanim::PrimitiveKind>(kind), depth);
+            if (grid_depth) *grid_depth = g.depth();
+            if (out == nullptr) return static_cast<int64_t>(g.word_count());
+            if (cap_words < g.word_count()) throw voxanim::ValidationError("output too small");
+            std::memcpy(out, g.words(), 8 * g.word_count());
+            return static_cast<int64_t>(g.word_count());
+        },
+        int64_t{-1});
 }
 
 vxn_model* vxn_model_deserialize(const uint8_t* bytes, size_t n) {

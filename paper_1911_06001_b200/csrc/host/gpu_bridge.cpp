@@ -132,4 +132,40 @@ std::uint32_t model_handle(const SvoModel& m) {
     return handle;
 }
 
+SvoModel build_from_grid(const VoxelGrid& grid, std::uint32_t depth) {
+    // the reference's argument checks (svo.cpp:80-87), same messages
+    if (depth < 1 || depth > 16)
+        throw ValidationError("octree depth must be in [1, 16], got " + std::to_string(depth));
+    if (grid.resolution() != (1u << depth))
+        throw ValidationError("grid resolution " + std::to_string(grid.resolution()) +
+                              " does not match 2^depth = " + std::to_string(1u << depth));
+    const ColorSpec& cs = grid.colors();
+    const std::uint32_t rgba = cs.constant.r | (std::uint32_t{cs.constant.g} << 8) |
+                               (std::uint32_t{cs.constant.b} << 16) | (std::uint32_t{cs.constant.a} << 24);
+    std::lock_guard<std::mutex> lk(g_mu);
+    vxa_ctx* ctx = ctx_locked();
+    std::uint32_t handle = 0;
+    std::uint64_t nn = 0, na = 0;
+    check(vxa_build_model(ctx, grid.words(), depth, static_cast<std::uint32_t>(cs.mode), rgba, &handle, &nn, &na),
+          "vxa_build_model");
+    SvoModel m;
+    m.depth = depth;
+    try {
+        m.nodes.resize(nn);
+        m.attributes.resize(na);
+        check(vxa_model_download(ctx, handle, m.nodes.data(), nn, reinterpret_cast<std::uint32_t*>(m.attributes.data()),
+                                 na),
+              "vxa_model_download");
+    } catch (...) {
+        vxa_release_model(ctx, handle);
+        throw;
+    }
+    std::uint64_t bytes = 0;
+    vxa_model_info(ctx, handle, &bytes, nullptr);
+    g_cache.push_front({m.nodes.data(), m.attributes.data(), m.nodes.size(), m.attributes.size(), m.depth, signature(m),
+                        handle, bytes});
+    g_cache_bytes += bytes;
+    return m;
+}
+
 } // namespace voxanim::gpu
