@@ -69,6 +69,14 @@ int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t
 int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const void* attrs,
                      uint32_t attr_count, uint32_t depth, uint32_t* handle_out);
 int vxa_release_model(vxa_ctx* ctx, uint32_t handle);
+/* Uploads a model straight from its .svo byte stream (the format of reference
+ * proj/src/svo.cpp:205-229): the header is checked like deserialize()
+ * (svo.cpp:231-291) and the 12-byte node records are uploaded in place (no host
+ * SvoModel). On a format error returns VXA_ERR_MODEL and, if format_error is
+ * non-null, stores the voxanim::SvoFormatErrorCode (errors.hpp: 0 BadMagic,
+ * 1 BadVersion, 2 BadHeader, 3 Truncated, 4 TrailingData, 5 NodeIndexOutOfRange,
+ * 6 AttrIndexOutOfRange); -1 when the stream is well-formed. */
+int vxa_upload_svo(vxa_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* handle_out, int32_t* format_error);
 /* Device-side size of a model: bytes of the packed node words and attributes,
  * and which packed format was chosen (1 = 4-byte words, 2 = 8-byte words). */
 int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32_t* node_format);

@@ -161,7 +161,7 @@ except ImportError:  # pragma: no cover
 # Every symbol include/vxa.h declares (checked by tests/test_abi.py).
 VXA_SYMBOLS = [
     "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
-    "vxa_upload_model", "vxa_release_model", "vxa_model_info", "vxa_build_model", "vxa_model_download",
+    "vxa_upload_model", "vxa_release_model", "vxa_model_info", "vxa_build_model", "vxa_model_download", "vxa_upload_svo",
     "vxa_model_counts",
     "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_render", "vxa_submit", "vxa_submit_readback",
     "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
@@ -201,6 +201,7 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_model_info", i, P, u32, C.POINTER(u64), C.POINTER(u32))
     _declare(lib, "vxa_build_model", i, P, P, u32, u32, u32, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))
     _declare(lib, "vxa_model_download", i, P, u32, P, u64, P, u64)
+    _declare(lib, "vxa_upload_svo", i, P, P, C.c_size_t, C.POINTER(u32), C.POINTER(C.c_int32))
     _declare(lib, "vxa_model_counts", i, P, u32, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))
     _declare(lib, "vxa_render", i, P, C.POINTER(vxa_frame_desc), C.POINTER(vxa_instance), u32, P, P,
              C.POINTER(vxa_stats))

@@ -172,7 +172,11 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         for (int k = 0; k < 3; ++k)
             d[k] = static_cast<float>((fma(in.Md[3 * k], rd.dcx, in.Md[3 * k + 1] * rd.dcy) - in.Md[3 * k + 2]) * rd.rnd);
         FastRay fr;
-        if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits)) return;
+        // Only a hit at t <= best.t can change the nearest (t, id) (ties go to
+        // the lower id), so subtrees entered beyond best.t are pruned.
+        const float t_lim = best.have ? nextafterf(static_cast<float>(best.t), __int_as_float(0x7f800000))
+                                      : __int_as_float(0x7f800000);
+        if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits, t_lim)) return;
         FastHit h;
         bool hit;
         if constexpr (kCompact)

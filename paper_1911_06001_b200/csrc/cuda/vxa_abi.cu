@@ -651,6 +651,46 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
     return VXA_OK;
 }
 
+int vxa_upload_svo(vxa_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* handle_out, int32_t* format_error) {
+    if (format_error) *format_error = -1;
+    if (ctx == nullptr || handle_out == nullptr || (bytes == nullptr && size > 0))
+        return fail(VXA_ERR_INVALID, "null argument");
+    const auto bad = [&](int code, const std::string& msg) {
+        if (format_error) *format_error = code;
+        return fail(VXA_ERR_MODEL, msg);
+    };
+    const auto u32 = [&](size_t off) {
+        return uint32_t{bytes[off]} | (uint32_t{bytes[off + 1]} << 8) | (uint32_t{bytes[off + 2]} << 16) |
+               (uint32_t{bytes[off + 3]} << 24);
+    };
+    // deserialize()'s checks, in its order (svo.cpp:232-258)
+    constexpr size_t kHeader = 20;
+    if (size < kHeader) return bad(3, "svo: truncated header");
+    if (std::memcmp(bytes, "SVOA", 4) != 0) return bad(0, "svo: bad magic, not an SVOA file");
+    if (u32(4) != 1) return bad(1, "svo: unsupported version " + std::to_string(u32(4)));
+    const uint32_t depth = u32(8), node_count = u32(12), attr_count = u32(16);
+    if (depth < 1 || depth > kMaxDepth || node_count == 0)
+        return bad(2, "svo: bad header (depth or node count out of range)");
+    const size_t expected = kHeader + 12 * size_t{node_count} + 4 * size_t{attr_count};
+    if (size < expected) return bad(3, "svo: truncated payload");
+    if (size > expected) return bad(4, "svo: trailing bytes after payload");
+    const uint8_t* nodes = bytes + kHeader;
+    for (uint32_t i = 0; i < node_count; ++i) {
+        const uint8_t* r = nodes + 12 * size_t{i};
+        const uint32_t valid = r[8], leaf = r[9];
+        const int ni = __builtin_popcount(valid & ~leaf & 0xffu), nl = __builtin_popcount(valid & leaf);
+        uint32_t cb, ab;
+        std::memcpy(&cb, r, 4);
+        std::memcpy(&ab, r + 4, 4);
+        if (ni > 0 && uint64_t{cb} + ni > node_count)
+            return bad(5, "svo: node " + std::to_string(i) + " child_base out of range");
+        if (nl > 0 && uint64_t{ab} + nl > attr_count)
+            return bad(6, "svo: node " + std::to_string(i) + " attr_base out of range");
+    }
+    // the stream's node records are the 12-byte SvoNode layout (little endian)
+    return vxa_upload_model(ctx, nodes, node_count, nodes + 12 * size_t{node_count}, attr_count, depth, handle_out);
+}
+
 int vxa_release_model(vxa_ctx* ctx, uint32_t handle) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     const auto it = ctx->models.find(handle);

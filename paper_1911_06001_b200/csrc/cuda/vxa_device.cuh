@@ -422,6 +422,9 @@ struct FastRay {
     float A[3];   // (-h - o_m) / 2h, rounded
     float Ar[3];  // its FP64 rounding residual
     float inv[3]; // 2h / |d|
+    // Pruning bound: subtrees entered at t >= t_lim cannot hold a hit that
+    // beats the caller's best (t_lim = nextafter(best t), +inf for none).
+    float t_lim;
     uint32_t mirror, zero;
     uint32_t zbits[3];
 };
@@ -462,7 +465,9 @@ __device__ __forceinline__ void fix_zero_axes(const FastRay& r, int level, float
 // Returns false when the ray misses the root box (traversal.cpp:56-60).
 __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const float A_lo[3], const float A_hi[3],
                                            const float Ar_lo[3], const float Ar_hi[3], const float h2[3],
-                                           uint32_t zflags, const uint32_t zbits[3]) {
+                                           uint32_t zflags, const uint32_t zbits[3],
+                                           float t_lim = __builtin_huge_valf()) {
+    r.t_lim = t_lim;
     r.mirror = 0;
     r.zero = 0;
     const float inf = __int_as_float(0x7f800000);
@@ -488,7 +493,9 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
             tx = fminf(tx, plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
         }
     }
-    return !(te >= tx || tx < 0.0f);
+    // a leaf's t is never below its ancestors' entry (shared, monotone planes),
+    // so a box entered at or beyond t_lim holds nothing nearer than the best
+    return !(te >= tx || tx < 0.0f) && te < t_lim;
 }
 
 // Traversal stacks. SmemStack: one column per thread of a [level][thread]
@@ -584,7 +591,9 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             t_enter = c0[2];
         }
         const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
-        if (!(t_enter < t_exit) || t_exit < 0.0f) continue;
+        // the reference cull !(t_enter < t_exit) || t_exit < 0, plus the pruning
+        // bound (t_enter >= t_lim: nothing in this child can beat the best)
+        if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
         const uint32_t leafm = Nodes::leaves(fw, level, depth);
         if (leafm & bit) {
             out.attr = nodes.attr_base(fw) + popc8_below(valid & leafm, bit);

@@ -97,3 +97,50 @@ def test_c_abi_build_download_and_errors(gpu):
 def _abi_invalid():
     from paper_1911_06001_b200 import _abi
     return _abi.VXA_ERR_INVALID
+
+
+def _corruptions(good: bytes):
+    """One stream per SvoFormatErrorCode class (test_svo.cpp's corruption cases)."""
+    import struct
+    n_nodes = struct.unpack_from("<I", good, 12)[0]
+    yield "short header", good[:19]
+    yield "bad magic", b"XVOA" + good[4:]
+    yield "bad version", good[:4] + struct.pack("<I", 2) + good[8:]
+    yield "depth 0", good[:8] + struct.pack("<I", 0) + good[12:]
+    yield "depth 17", good[:8] + struct.pack("<I", 17) + good[12:]
+    yield "no nodes", good[:12] + struct.pack("<I", 0) + good[16:]
+    yield "truncated payload", good[:-1]
+    yield "trailing data", good + b"\0"
+    b = bytearray(good)
+    struct.pack_into("<I", b, 20, n_nodes)  # root child_base past the end
+    yield "child out of range", bytes(b)
+    last = 20 + 12 * (n_nodes - 1)  # a last-level node: attr_base past the end
+    b = bytearray(good)
+    struct.pack_into("<I", b, last + 4, 1 << 30)
+    yield "attr out of range", bytes(b)
+
+
+def test_upload_svo_stream(gpu):
+    """vxa_upload_svo: a well-formed stream renders like the uploaded SvoModel;
+    every corruption class fails with the reference deserialize()'s message."""
+    lib = vx.vxa()
+    ctx = vx.context()
+    model = vx.Model.random(21, 4, 0.2)
+    good = model.serialize()
+    h, code = C.c_uint32(), C.c_int32()
+    assert lib.vxa_upload_svo(ctx, good, len(good), C.byref(h), C.byref(code)) == 0 and code.value == -1
+    nodes = np.zeros(len(good), np.uint8)
+    n_nodes = int(np.frombuffer(good[12:16], np.uint32)[0])
+    assert lib.vxa_model_download(ctx, h.value, nodes.ctypes.data, n_nodes, None, 0) == 0
+    assert nodes[:12 * n_nodes].tobytes() == good[20:20 + 12 * n_nodes]
+    lib.vxa_release_model(ctx, h.value)
+    expected_code = {"short header": 3, "bad magic": 0, "bad version": 1, "depth 0": 2, "depth 17": 2,
+                     "no nodes": 2, "truncated payload": 3, "trailing data": 4, "child out of range": 5,
+                     "attr out of range": 6}
+    for name, data in _corruptions(good):
+        with pytest.raises(RuntimeError) as ref_err:
+            ref.RefModel.from_bytes(data)
+        rc = lib.vxa_upload_svo(ctx, data, len(data), C.byref(h), C.byref(code))
+        assert rc == 2, name  # VXA_ERR_MODEL
+        assert code.value == expected_code[name], name
+        assert lib.vxa_last_error().decode() == str(ref_err.value), name
