@@ -31,7 +31,7 @@ TRAV_DTYPE = np.dtype(
 
 # default resolutions of the bench_scenes.hpp configurations
 CONFIG_SIZES = {1: (512, 512), 2: (1920, 1080), 3: (1920, 1080), 4: (3840, 2160), 5: (160, 120), 6: (64, 48),
-                7: (96, 64), 8: (96, 64), 9: (101, 101), 10: (320, 180)}
+                7: (96, 64), 8: (96, 64), 9: (101, 101), 10: (320, 180), 11: (3840, 2160), 12: (160, 120)}
 
 # classify() codes
 MATCH, TIE, BUG, T_OUT_OF_TOL = 0, 1, 2, 3

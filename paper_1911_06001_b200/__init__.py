@@ -62,6 +62,8 @@ class config:  # bench_scenes.hpp
     HBO = 8
     AXIS_ALIGNED = 9
     MANY = 10
+    CROWD = 11     # seed = instance count (0: 4096)
+    STACKED = 12
 
 
 class Model:

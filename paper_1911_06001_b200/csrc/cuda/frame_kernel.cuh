@@ -77,6 +77,29 @@ __device__ __forceinline__ SphereRes<Real> sphere_test(const DevInstance<Real>& 
     return s;
 }
 
+// FP32 sphere test from the cull table (same conservative form as above).
+__device__ __forceinline__ SphereRes<float> sphere_test(const float4 c, const float d[3]) {
+    SphereRes<float> s;
+    s.tc = c.x * d[0] + c.y * d[1] + c.z * d[2];
+    const float px = c.x - s.tc * d[0], py = c.y - s.tc * d[1], pz = c.z - s.tc * d[2];
+    const float d2 = px * px + py * py + pz * pz;
+    const float r2 = c.w * c.w;
+    s.hit = (d2 < r2 * 1.00001f + 1e-12f) && (s.tc + c.w * 1.00001f >= 0.0f);
+    const float tb = s.tc - sqrtf(fmaxf(r2 - d2, 0.0f)) - 1e-5f * (fabsf(s.tc) + c.w);
+    s.tb = fmaxf(tb, 0.0f);
+    return s;
+}
+
+// Sphere test of instance i: FP64 from the instance record (reference order),
+// FP32 from the cull table.
+template <typename Real>
+__device__ __forceinline__ SphereRes<Real> sphere_of(const FrameParams<Real>& p, uint32_t i, const Real d[3]) {
+    if constexpr (sizeof(Real) == 8)
+        return sphere_test(p.inst[i], d);
+    else
+        return sphere_test(__ldg(p.cull + i), d);
+}
+
 // Per-pixel primary ray. FP32 kernel: the camera-space direction and its norm
 // are also kept in FP64 (dcd, rnd) so each instance's local direction is formed
 // in FP64 and rounded once: a plane entry t = (A + i s) / d_a is only as
@@ -109,16 +132,17 @@ struct TileCone {
     float cos_a, sin_a;
 };
 
-__device__ __forceinline__ TileCone tile_cone(const FrameParams<float>& p, int x0, int y0) {
-    const float cxs = fmaf(static_cast<float>(x0) + 4.0f, p.inv_w2, -1.0f) * p.sx;
-    const float cys = fmaf(-(static_cast<float>(y0) + 2.0f), p.inv_h2, 1.0f) * p.sy;
+// Cone of the pixel-centre rays of the w x h pixel region at (x0, y0).
+__device__ __forceinline__ TileCone region_cone(const FrameParams<float>& p, int x0, int y0, float w, float h) {
+    const float cxs = fmaf(static_cast<float>(x0) + 0.5f * w, p.inv_w2, -1.0f) * p.sx;
+    const float cys = fmaf(-(static_cast<float>(y0) + 0.5f * h), p.inv_h2, 1.0f) * p.sy;
     const float cn = rsqrtf(cxs * cxs + cys * cys + 1.0f);
     const float ax = cxs * cn, ay = cys * cn, az = -cn;
     float smax = 0.0f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float xs = fmaf(static_cast<float>(x0) + ((k & 1) ? 7.5f : 0.5f), p.inv_w2, -1.0f) * p.sx;
-        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2) ? 3.5f : 0.5f)), p.inv_h2, 1.0f) * p.sy;
+        const float xs = fmaf(static_cast<float>(x0) + ((k & 1) ? w - 0.5f : 0.5f), p.inv_w2, -1.0f) * p.sx;
+        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2) ? h - 0.5f : 0.5f)), p.inv_h2, 1.0f) * p.sy;
         const float n = rsqrtf(xs * xs + ys * ys + 1.0f);
         const float bx = xs * n, by = ys * n, bz = -n;
         // |a x b| = sin of the angle (accurate for small angles, unlike 1 - cos)
@@ -132,10 +156,14 @@ __device__ __forceinline__ TileCone tile_cone(const FrameParams<float>& p, int x
     return c;
 }
 
-__device__ __forceinline__ bool cone_candidate(const DevInstance<float>& in, const TileCone& c) {
-    const float lx = in.L[0], ly = in.L[1], lz = in.L[2];
+__device__ __forceinline__ TileCone tile_cone(const FrameParams<float>& p, int x0, int y0) {
+    return region_cone(p, x0, y0, static_cast<float>(kTileW), static_cast<float>(kTileH));
+}
+
+__device__ __forceinline__ bool cone_candidate(const float4 in, const TileCone& c) {
+    const float lx = in.x, ly = in.y, lz = in.z;
     const float dist2 = lx * lx + ly * ly + lz * lz;
-    const float r = in.r * 1.001f + 1e-5f * sqrtf(dist2) + 1e-6f;
+    const float r = in.w * 1.001f + 1e-5f * sqrtf(dist2) + 1e-6f;
     if (dist2 <= r * r) return true; // camera inside the (inflated) sphere
     const float s = lx * c.a[0] + ly * c.a[1] + lz * c.a[2];
     const float qx = ly * c.a[2] - lz * c.a[1], qy = lz * c.a[0] - lx * c.a[2], qz = lx * c.a[1] - ly * c.a[0];
@@ -254,10 +282,18 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         if constexpr (sizeof(Real) == 4) {
             if (p.culling && n <= 0xffffu) {
                 const TileCone cone = tile_cone(p, tx0, ty0);
+                // source: the super-tile's candidate list when the pre-pass ran
+                const uint16_t* src = nullptr;
+                uint32_t src_n = n;
+                if (p.super_list != nullptr) {
+                    const uint32_t c = __ldg(p.super_count + st);
+                    if (c != 0xffffffffu) src = p.super_list + static_cast<size_t>(st) * p.super_cap, src_n = c;
+                }
                 uint32_t cnt = 0;
-                for (uint32_t base = 0; base < n; base += 32) {
-                    const uint32_t i = base + lane;
-                    const bool c = i < n && cone_candidate(p.inst[i], cone);
+                for (uint32_t base = 0; base < src_n; base += 32) {
+                    const uint32_t j = base + lane;
+                    const uint32_t i = j < src_n ? (src ? __ldg(src + j) : j) : 0u;
+                    const bool c = j < src_n && cone_candidate(__ldg(p.cull + i), cone);
                     const uint32_t m = __ballot_sync(0xffffffffu, c);
                     const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
                     if (c && pos < kListCap) s_list[warp][pos] = static_cast<uint16_t>(i);
@@ -294,12 +330,12 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         unsigned long long hitmask = 0; // list mode: bit k = s_list[warp][k] hit
         if (list_n != 0xffffffffu) {
             for (uint32_t k = 0; k < list_n; ++k)
-                if (sphere_test(p.inst[list[k]], dw).hit) hitmask |= 1ull << k;
+                if (sphere_of(p, list[k], dw).hit) hitmask |= 1ull << k;
             n_hits = __popcll(hitmask);
             if (n_hits) only = list[__ffsll(hitmask) - 1];
         } else if (p.sphere_pass) {
             for (uint32_t i = 0; i < n; ++i) {
-                if (sphere_test(p.inst[i], dw).hit) {
+                if (sphere_of(p, i, dw).hit) {
                     if (n_hits == 0) only = i;
                     ++n_hits;
                 }
@@ -360,7 +396,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
                     Real tcb = Real(0);
                     for (unsigned long long it = rem; it; it &= it - 1) {
                         const int k = __ffsll(it) - 1;
-                        const SphereRes<Real> sr = sphere_test(p.inst[list[k]], dw);
+                        const SphereRes<Real> sr = sphere_of(p, list[k], dw);
                         if (kb < 0 || sr.tc < tcb) kb = k, tcb = sr.tc, cand_tb = sr.tb;
                     }
                     if (kb >= 0) found = true, cand = list[kb], rem &= ~(1ull << kb);
@@ -370,7 +406,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
                     int k = -1;
                     Real k_tc = Real(0);
                     for (uint32_t i = 0; i < n; ++i) {
-                        const SphereRes<Real> sr = sphere_test(p.inst[i], dw);
+                        const SphereRes<Real> sr = sphere_of(p, i, dw);
                         if (p.culling && !sr.hit) continue;
                         const bool after = sr.tc > last_tc || (sr.tc == last_tc && static_cast<int>(i) > last_i);
                         if (!after) continue;
@@ -378,7 +414,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
                     }
                     if (k >= 0) found = true, cand = static_cast<uint32_t>(k), last_tc = k_tc, last_i = k;
                 } else {
-                    while (next_i < n && p.culling && !sphere_test(p.inst[next_i], dw).hit) ++next_i;
+                    while (next_i < n && p.culling && !sphere_of(p, next_i, dw).hit) ++next_i;
                     if (next_i < n) found = true, cand = next_i++;
                 }
                 if (!found) break;
@@ -461,6 +497,34 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         const uint32_t v = __reduce_add_sync(0xffffffffu, vals[k]);
         if (lane == 0 && v) atomicAdd(p.counters + 2 + k, static_cast<unsigned long long>(v));
     }
+}
+
+// Pre-pass for large scenes: one warp per super-tile of this rank cone-tests
+// every instance against the super-tile's cone and writes the survivors (in
+// instance order) to its list; the frame kernel's 8x4 tiles then test only
+// their super-tile's list (tiles x instances / 32 rounds -> super-tiles x
+// instances / 32 + tiles x list / 32).
+static __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__ FrameParams<float> p,
+                                                        uint16_t* __restrict__ list, uint32_t* __restrict__ count) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t st = blockIdx.x * 4u + (threadIdx.x >> 5);
+    const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
+    if (st >= n_mine) return;
+    const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
+    const int x0 = static_cast<int>((s % p.n_super_x) * kSuper), y0 = static_cast<int>((s / p.n_super_x) * kSuper);
+    const float w = static_cast<float>(min(kSuper, p.width - x0)), h = static_cast<float>(min(kSuper, p.height - y0));
+    const TileCone cone = region_cone(p, x0, y0, w, h);
+    uint16_t* out = list + static_cast<size_t>(st) * p.super_cap;
+    uint32_t cnt = 0;
+    for (uint32_t base = 0; base < p.n_inst; base += 32) {
+        const uint32_t i = base + lane;
+        const bool c = i < p.n_inst && cone_candidate(__ldg(p.cull + i), cone);
+        const uint32_t m = __ballot_sync(0xffffffffu, c);
+        const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
+        if (c && pos < p.super_cap) out[pos] = static_cast<uint16_t>(i);
+        cnt += __popc(m);
+    }
+    if (lane == 0) count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
 }
 
 } // namespace vxa

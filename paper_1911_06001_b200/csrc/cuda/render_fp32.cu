@@ -19,6 +19,13 @@ cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, co
     return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f32(p.max_depth), l.stream);
 }
 
+cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, cudaStream_t s) {
+    const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
+    if (n_mine == 0) return cudaSuccess;
+    super_cull_kernel<<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
+    return cudaGetLastError();
+}
+
 size_t frame_smem_bytes_f32(uint32_t max_depth) {
     return sizeof(uint2) * kBlock * (max_depth > 0 ? max_depth : 1);
 }

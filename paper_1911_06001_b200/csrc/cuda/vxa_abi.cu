@@ -19,6 +19,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "vxa_internal.h"
@@ -167,6 +168,9 @@ struct vxa_ctx {
     DevBuf<uint32_t> tile_counter;
     DevBuf<unsigned long long> counters;
     DevBuf<unsigned char> inst_dev;
+    DevBuf<uint16_t> super_list;  // per-super-tile candidate lists (large scenes)
+    DevBuf<uint32_t> super_count;
+    int aux_launches = 0;         // pre-pass kernels since the last stats reset
     unsigned char* inst_host[2] = {nullptr, nullptr};
     size_t inst_host_cap = 0;
     cudaEvent_t inst_done[2] = {nullptr, nullptr};
@@ -212,78 +216,100 @@ template <typename Real> struct HostFrame {
     std::vector<DevInstance<Real>> inst;
 };
 
-// Builds the device instance table in id order (index order == the
-// reference's id tie-break order). Returns VXA_OK or an error.
+// One device instance record: everything the kernels need, folded on the host
+// in FP64 in the reference's operand order and rounded once.
 template <typename Real>
-int build_instances(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n,
-                    std::vector<DevInstance<Real>>& out) {
-    std::vector<uint32_t> order(n);
-    std::iota(order.begin(), order.end(), 0u);
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return in[a].id < in[b].id; });
-    out.resize(n);
+void fold_instance(const std::map<uint32_t, ModelEntry>& models, const vxa_frame_desc* f, const vxa_instance& s,
+                   DevInstance<Real>& d) {
     const double* o = f->camera.position;
     const double* C = f->camera.orientation;
-    for (uint32_t k = 0; k < n; ++k) {
-        const vxa_instance& s = in[order[k]];
-        DevInstance<Real>& d = out[k];
-        std::memset(&d, 0, sizeof(d));
-        d.id = s.id;
-        d.dirty = s.dirty;
-        const auto it = ctx->models.find(s.model);
-        if (it == ctx->models.end()) {
-            d.valid_model = 0; // reference: objects without a model are skipped (renderer.cpp:74-76)
-        } else {
-            d.valid_model = 1;
-            d.model = it->second.dev;
-        }
-        const double* R = s.rotation;
-        const double* t = s.translation;
-        // bounding sphere: centre = translation, r = 0.5 |scale|
-        const double l[3] = {t[0] - o[0], t[1] - o[1], t[2] - o[2]};
-        const double L2 = l[0] * l[0] + l[1] * l[1] + l[2] * l[2];
-        const double r = 0.5 * std::sqrt(s.scale[0] * s.scale[0] + s.scale[1] * s.scale[1] + s.scale[2] * s.scale[2]);
-        const double r2 = r * r;
-        // local ray origin: R^T (o + (-t))
-        const double v[3] = {o[0] + -t[0], o[1] + -t[1], o[2] + -t[2]};
-        double Rt[9];
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) Rt[3 * i + j] = R[3 * j + i];
-        double ol[3];
-        for (int i = 0; i < 3; ++i) ol[i] = Rt[3 * i] * v[0] + Rt[3 * i + 1] * v[1] + Rt[3 * i + 2] * v[2];
-        const double h[3] = {s.scale[0] * 0.5, s.scale[1] * 0.5, s.scale[2] * 0.5};
-        for (int a = 0; a < 3; ++a) {
-            d.L[a] = static_cast<Real>(l[a]);
-            d.A_lo[a] = static_cast<Real>(-h[a] - ol[a]);
-            d.A_hi[a] = static_cast<Real>(h[a] - ol[a]);
-            d.h2[a] = static_cast<Real>(2.0 * h[a]);
-            // FP32 kernel: unit-cube plane offsets (-h - o) / 2h, (h - o) / 2h + residuals
-            const double ulo = (-h[a] - ol[a]) / (2.0 * h[a]), uhi = (h[a] - ol[a]) / (2.0 * h[a]);
-            d.U_lo[a] = static_cast<float>(ulo);
-            d.U_hi[a] = static_cast<float>(uhi);
-            d.Ur_lo[a] = static_cast<float>(ulo - static_cast<double>(d.U_lo[a]));
-            d.Ur_hi[a] = static_cast<float>(uhi - static_cast<double>(d.U_hi[a]));
-            d.zbits[a] = zero_dir_bits(ol[a], h[a]);
-            if (-h[a] > ol[a]) d.zflags |= 1u << a;
-            if (h[a] > ol[a]) d.zflags |= 1u << (3 + a);
-        }
-        d.L2 = static_cast<Real>(L2);
-        d.r = static_cast<Real>(r);
-        d.r2 = static_cast<Real>(r2);
-        for (int i = 0; i < 9; ++i) d.R[i] = static_cast<Real>(R[i]);
-        // camera -> local rotation R^T C in FP64 (FP32 kernel's local direction)
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) {
-                double acc = 0.0;
-                for (int k2 = 0; k2 < 3; ++k2) acc += Rt[3 * i + k2] * C[3 * k2 + j];
-                d.Md[3 * i + j] = acc;
-            }
-        if constexpr (sizeof(Real) == 8) {
-            for (int i = 0; i < 9; ++i) d.M[i] = Rt[i];
-        } else {
-            for (int i = 0; i < 9; ++i) d.M[i] = static_cast<float>(d.Md[i]);
-        }
+    std::memset(&d, 0, sizeof(d));
+    d.id = s.id;
+    d.dirty = s.dirty;
+    const auto it = models.find(s.model);
+    if (it == models.end()) {
+        d.valid_model = 0; // reference: objects without a model are skipped (renderer.cpp:74-76)
+    } else {
+        d.valid_model = 1;
+        d.model = it->second.dev;
     }
-    return VXA_OK;
+    const double* R = s.rotation;
+    const double* t = s.translation;
+    // bounding sphere: centre = translation, r = 0.5 |scale|
+    const double l[3] = {t[0] - o[0], t[1] - o[1], t[2] - o[2]};
+    const double L2 = l[0] * l[0] + l[1] * l[1] + l[2] * l[2];
+    const double r = 0.5 * std::sqrt(s.scale[0] * s.scale[0] + s.scale[1] * s.scale[1] + s.scale[2] * s.scale[2]);
+    const double r2 = r * r;
+    // local ray origin: R^T (o + (-t))
+    const double v[3] = {o[0] + -t[0], o[1] + -t[1], o[2] + -t[2]};
+    double Rt[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Rt[3 * i + j] = R[3 * j + i];
+    double ol[3];
+    for (int i = 0; i < 3; ++i) ol[i] = Rt[3 * i] * v[0] + Rt[3 * i + 1] * v[1] + Rt[3 * i + 2] * v[2];
+    const double h[3] = {s.scale[0] * 0.5, s.scale[1] * 0.5, s.scale[2] * 0.5};
+    for (int a = 0; a < 3; ++a) {
+        d.L[a] = static_cast<Real>(l[a]);
+        d.A_lo[a] = static_cast<Real>(-h[a] - ol[a]);
+        d.A_hi[a] = static_cast<Real>(h[a] - ol[a]);
+        d.h2[a] = static_cast<Real>(2.0 * h[a]);
+        // FP32 kernel: unit-cube plane offsets (-h - o) / 2h, (h - o) / 2h + residuals
+        const double ulo = (-h[a] - ol[a]) / (2.0 * h[a]), uhi = (h[a] - ol[a]) / (2.0 * h[a]);
+        d.U_lo[a] = static_cast<float>(ulo);
+        d.U_hi[a] = static_cast<float>(uhi);
+        d.Ur_lo[a] = static_cast<float>(ulo - static_cast<double>(d.U_lo[a]));
+        d.Ur_hi[a] = static_cast<float>(uhi - static_cast<double>(d.U_hi[a]));
+        d.zbits[a] = zero_dir_bits(ol[a], h[a]);
+        if (-h[a] > ol[a]) d.zflags |= 1u << a;
+        if (h[a] > ol[a]) d.zflags |= 1u << (3 + a);
+    }
+    d.L2 = static_cast<Real>(L2);
+    d.r = static_cast<Real>(r);
+    d.r2 = static_cast<Real>(r2);
+    for (int i = 0; i < 9; ++i) d.R[i] = static_cast<Real>(R[i]);
+    // camera -> local rotation R^T C in FP64 (FP32 kernel's local direction)
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int k2 = 0; k2 < 3; ++k2) acc += Rt[3 * i + k2] * C[3 * k2 + j];
+            d.Md[3 * i + j] = acc;
+        }
+    if constexpr (sizeof(Real) == 8) {
+        for (int i = 0; i < 9; ++i) d.M[i] = Rt[i];
+    } else {
+        for (int i = 0; i < 9; ++i) d.M[i] = static_cast<float>(d.Md[i]);
+    }
+}
+
+// Builds the device instance table in id order (index order == the
+// reference's id tie-break order) straight into `out` (the pinned staging
+// slot), plus the FP32 cull table; large scenes fold on several threads.
+template <typename Real>
+void build_instances(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, DevInstance<Real>* out,
+                     float4* cull) {
+    const auto by_id = [&](uint32_t a, uint32_t b) { return in[a].id < in[b].id; };
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    if (!std::is_sorted(order.begin(), order.end(), by_id)) std::stable_sort(order.begin(), order.end(), by_id);
+    const auto work = [&](uint32_t k0, uint32_t k1) {
+        for (uint32_t k = k0; k < k1; ++k) {
+            fold_instance(ctx->models, f, in[order[k]], out[k]);
+            if (cull)
+                cull[k] = make_float4(static_cast<float>(out[k].L[0]), static_cast<float>(out[k].L[1]),
+                                      static_cast<float>(out[k].L[2]), static_cast<float>(out[k].r));
+        }
+    };
+    const uint32_t threads = n >= 2048 ? std::min<uint32_t>(8, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    if (threads <= 1) {
+        work(0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const uint32_t chunk = (n + threads - 1) / threads;
+    for (uint32_t t = 1; t < threads; ++t)
+        pool.emplace_back(work, std::min(n, t * chunk), std::min(n, (t + 1) * chunk));
+    work(0, std::min(n, chunk));
+    for (auto& th : pool) th.join();
 }
 
 template <typename Real> void fill_camera(FrameParams<Real>& p, const vxa_frame_desc* f) {
@@ -333,15 +359,19 @@ int check_frame(const vxa_frame_desc* f) {
 template <typename Real>
 int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov,
                   HitRec* hbo, bool reset_counters) {
-    std::vector<DevInstance<Real>> tab;
-    if (int rc = build_instances<Real>(ctx, f, in, n, tab); rc != VXA_OK) return rc;
-    const size_t bytes = tab.size() * sizeof(DevInstance<Real>);
+    // one upload: the instance records, then (FP32) the float4 cull table,
+    // folded straight into the pinned staging slot
+    const size_t inst_bytes = (size_t{n} * sizeof(DevInstance<Real>) + 15) & ~size_t{15};
+    const size_t cull_bytes = sizeof(Real) == 4 ? size_t{n} * sizeof(float4) : 0;
+    const size_t bytes = inst_bytes + cull_bytes;
     if (int rc = ensure_staging(ctx, bytes); rc != VXA_OK) return rc;
-    VXA_CUDA(ctx->inst_dev.ensure(std::max<size_t>(bytes, 1)));
+    VXA_CUDA(ctx->inst_dev.ensure(std::max<size_t>(bytes, 16)));
     const int slot = ctx->inst_slot;
     ctx->inst_slot ^= 1;
     VXA_CUDA(cudaEventSynchronize(ctx->inst_done[slot])); // staging slot no longer read by an earlier copy
-    if (bytes) std::memcpy(ctx->inst_host[slot], tab.data(), bytes);
+    auto* tab = reinterpret_cast<DevInstance<Real>*>(ctx->inst_host[slot]);
+    build_instances<Real>(ctx, f, in, n, tab,
+                          cull_bytes ? reinterpret_cast<float4*>(ctx->inst_host[slot] + inst_bytes) : nullptr);
 
     const int32_t W = f->camera.width, H = f->camera.height;
     VXA_CUDA(ctx->fb.ensure(static_cast<size_t>(W) * H));
@@ -356,6 +386,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     FrameParams<Real> p{};
     fill_camera(p, f);
     p.inst = reinterpret_cast<const DevInstance<Real>*>(ctx->inst_dev.ptr);
+    p.cull = cull_bytes ? reinterpret_cast<const float4*>(ctx->inst_dev.ptr + inst_bytes) : nullptr;
     p.n_inst = n;
     p.background = f->background[0] | (uint32_t{f->background[1]} << 8) | (uint32_t{f->background[2]} << 16) | 0xff000000u;
     p.culling = f->culling ? 1u : 0u;
@@ -382,8 +413,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.fb = target;
     p.max_depth = 1;
     p.compact = sizeof(Real) == 4 ? 1u : 0u;
-    for (const auto& di : tab)
-        if (di.valid_model) {
+    for (uint32_t k = 0; k < n; ++k)
+        if (const auto& di = tab[k]; di.valid_model) {
             p.max_depth = std::max(p.max_depth, std::min(di.model.depth, kMaxDepth));
             if (di.model.cwords == nullptr) p.compact = 0;
         }
@@ -413,11 +444,23 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
         VXA_CUDA(cudaEventCreate(&ctx->k_end[slot_k]));
     }
     VXA_CUDA(cudaEventRecord(ctx->k_begin[slot_k], ctx->stream));
-    cudaError_t e;
-    if constexpr (sizeof(Real) == 8)
+    cudaError_t e = cudaSuccess;
+    if constexpr (sizeof(Real) == 8) {
         e = launch_frame_f64(p, a, h, l);
-    else
-        e = launch_frame_f32(p, a, h, l);
+    } else {
+        // large scenes: per-super-tile candidate lists first (same stream)
+        if (p.culling && n > kSuperCullMin && n <= 0xffffu) {
+            const size_t mine_super = p.n_tiles / kTilesPerSuper;
+            VXA_CUDA(ctx->super_list.ensure(std::max<size_t>(mine_super * kSuperCap, 1)));
+            VXA_CUDA(ctx->super_count.ensure(std::max<size_t>(mine_super, 1)));
+            p.super_list = ctx->super_list.ptr;
+            p.super_count = ctx->super_count.ptr;
+            p.super_cap = kSuperCap;
+            e = launch_super_cull(p, ctx->super_list.ptr, ctx->super_count.ptr, ctx->stream);
+            ++ctx->aux_launches;
+        }
+        if (e == cudaSuccess) e = launch_frame_f32(p, a, h, l);
+    }
     if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
     VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
     ++ctx->k_count;
@@ -449,7 +492,7 @@ int read_counters(vxa_ctx* ctx, vxa_stats* s) {
         total += ms;
     }
     s->gpu_ms = total;
-    s->kernel_launches = static_cast<uint64_t>(ctx->k_count);
+    s->kernel_launches = static_cast<uint64_t>(ctx->k_count + ctx->aux_launches);
     s->h2d_bytes = ctx->h2d;
     s->d2h_bytes = ctx->d2h + sizeof(c);
     return VXA_OK;
@@ -523,6 +566,8 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->tile_counter.release();
     ctx->counters.release();
     ctx->inst_dev.release();
+    ctx->super_list.release();
+    ctx->super_count.release();
     ctx->aov.release();
     ctx->hbo.release();
     ctx->rgb.release();
@@ -822,12 +867,13 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         ctx->h2d += npix * sizeof(HitRec);
     }
     ctx->k_count = 0;
+    ctx->aux_launches = 0;
     ctx->h2d = ctx->d2h = 0;
     ctx->n_rays = ctx->n_sphere_tests = 0;
     VXA_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
     if (int rc = enqueue_any(ctx, f, in, n, aov, hbo, true); rc != VXA_OK) return rc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
-    uint64_t launches = 1;
+    uint64_t launches = 1 + static_cast<uint64_t>(ctx->aux_launches);
     if (rgb_out) {
         VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
         const size_t quads = (npix + 3) / 4;
@@ -958,6 +1004,7 @@ int vxa_stats_reset(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
     ctx->k_count = 0;
+    ctx->aux_launches = 0;
     ctx->h2d = ctx->d2h = 0;
     ctx->n_rays = ctx->n_sphere_tests = 0;
     return VXA_OK;

@@ -38,6 +38,9 @@ constexpr uint32_t kMixed = 1u << 16;
 constexpr int kTileW = 8, kTileH = 4;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
+// Scenes with more instances than this get the per-super-tile culling pre-pass.
+constexpr uint32_t kSuperCullMin = 128;
+constexpr uint32_t kSuperCap = 1024; // super-tile list capacity (overflow: scan all)
 
 // Screen partition: 64x64 super-tile s = (y / 64) * n_super_x + x / 64 belongs
 // to rank s % world. The frame kernel enumerates a rank's super-tiles as
@@ -121,6 +124,16 @@ template <typename Real> struct DevInstance {
 
 template <typename Real> struct FrameParams {
     const DevInstance<Real>* inst;
+    // FP32 culling data, one float4 {L (sphere centre - camera), r} per
+    // instance (16 B, coalesced and L1-friendly: the cone and sphere tests read
+    // only this, not the 300-byte instance records)
+    const float4* cull;
+    // Large scenes (n_inst > kSuperCullMin): per-super-tile candidate lists
+    // from the pre-pass (super_cull_kernel), super_cap entries per rank-local
+    // super-tile in instance order; count 0xffffffff = overflow (scan all).
+    const uint16_t* super_list;
+    const uint32_t* super_count;
+    uint32_t super_cap;
     uint32_t n_inst;
     int32_t width, height;
     // camera

@@ -98,6 +98,30 @@ void add_c4_instances(Scene& s, const std::shared_ptr<const SvoModel>& model) {
     }
 }
 
+void add_crowd(Scene& s, const std::vector<std::shared_ptr<const SvoModel>>& models, int count) {
+    for (int i = 0; i < count; ++i) {
+        std::mt19937_64 rng(5000 + static_cast<std::uint64_t>(i));
+        const Vec3 axis = unit_normal3(rng);
+        std::uniform_real_distribution<double> omega_dist(20.0, 90.0), scale_dist(0.5, 0.9);
+        const double omega = omega_dist(rng);
+        const double sc = scale_dist(rng);
+        const Vec3 base{(i % 32) - 15.5, ((i / 32) % 16) - 7.5, -1.5 * (i / 512)};
+        AnimationTrack tr;
+        tr.object_id = i;
+        for (int k = 0; k <= 8; ++k) {
+            const double t = 0.5 * k;
+            Keyframe key;
+            key.time = t;
+            key.rotation = axis_angle_deg(axis, omega * t);
+            key.translation = base + Vec3{0.0, 0.1 * std::sin(kPi * t + i), 0.0};
+            key.scale = {sc, sc, sc};
+            tr.keys.push_back(key);
+        }
+        s.objects.push_back(object(i, models[static_cast<std::size_t>(i) % models.size()], transform_of(tr.keys.front())));
+        s.tracks.push_back(tr);
+    }
+}
+
 } // namespace
 
 Scene make_config_scene(int config, const std::vector<std::shared_ptr<const SvoModel>>& models, std::uint64_t seed,
@@ -191,6 +215,26 @@ Scene make_config_scene(int config, const std::vector<std::shared_ptr<const SvoM
         }
         s.camera = make_look_at_camera({0, 0, 6}, {0, 0, -1}, {0, 1, 0}, 70, 320, 180);
         w = 320, h = 180;
+        break;
+    }
+    case kCrowd: {
+        add_crowd(s, models, seed ? static_cast<int>(seed) : 4096);
+        s.camera = make_look_at_camera({0.0, 0.0, 22.0}, {0, 0, 0}, {0, 1, 0}, 60.0, 3840, 2160);
+        w = 3840, h = 2160;
+        break;
+    }
+    case kStacked: {
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> jitter(-0.15, 0.15), scl(0.6, 1.2);
+        for (int i = 0; i < 96; ++i) {
+            RigidTransform tf;
+            tf.translation = {jitter(rng), jitter(rng), -0.35 * i};
+            tf.scale = {scl(rng), scl(rng), scl(rng)};
+            tf.rotation = rotation_from_quaternion(unit_quaternion(rng));
+            s.objects.push_back(object(i, models[static_cast<std::size_t>(i) % models.size()], tf));
+        }
+        s.camera = make_look_at_camera({0, 0, 4}, {0, 0, -1}, {0, 1, 0}, 40, 160, 120);
+        w = 160, h = 120;
         break;
     }
     default:

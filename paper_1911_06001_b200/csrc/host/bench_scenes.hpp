@@ -26,6 +26,10 @@ enum SceneConfig : int {
     kAxisAligned = 9,      // camera on the z axis, odd resolution: a row and a column of rays with
                            // exactly zero local direction components (zero-direction convention)
     kManyInstances = 10,   // 4 x models.size() x 50 instances on a grid (wide candidate lists)
+    kCrowd = 11,           // `seed` (default 4096) animated instances on a 32 x 16 x k lattice, 3840x2160
+                           // (scaling with the instance count)
+    kStacked = 12,         // 96 instances stacked along the view axis: tile candidate lists
+                           // overflow (> 64), exercising the per-ray fallback pass
 };
 
 // models: C1-C4 use models[0]; kRandomScene uses every model; kSortedTracing

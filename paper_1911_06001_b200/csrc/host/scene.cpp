@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <iterator>
+#include <unordered_map>
 
 namespace voxanim {
 
@@ -99,8 +100,23 @@ RigidTransform evaluate_track(const AnimationTrack& track, double time) {
 
 void evaluate_animation(Scene& scene, double time) {
     if (time < 0.0) throw ValidationError("animation time must be nonnegative");
+    // The reference resolves each track with Scene::find_object, a linear scan
+    // (O(tracks x objects): ~8 M comparisons per frame at 4096 instances). Same
+    // answer -- the first object with the id -- from a map built once per call.
+    const bool use_map = scene.tracks.size() > 8;
+    std::unordered_map<std::int32_t, SceneObject*> by_id;
+    if (use_map) {
+        by_id.reserve(scene.objects.size());
+        for (SceneObject& o : scene.objects) by_id.emplace(o.id, &o); // keeps the first
+    }
     for (const AnimationTrack& track : scene.tracks) {
-        SceneObject* obj = scene.find_object(track.object_id);
+        SceneObject* obj;
+        if (use_map) {
+            const auto it = by_id.find(track.object_id);
+            obj = it == by_id.end() ? nullptr : it->second;
+        } else {
+            obj = scene.find_object(track.object_id);
+        }
         if (obj == nullptr) continue;
         const RigidTransform next = evaluate_track(track, time);
         if (!(next == obj->transform)) {

@@ -174,6 +174,29 @@ def test_many_instances_overflow_the_tile_list(gpu):
         check_fp32(s, o, o_aov, o_img, culling, sorting)
 
 
+def test_stacked_instances_overflow_tile_lists(gpu):
+    """96 instances stacked along the view axis: the tiles around the axis meet
+    all 96 (> the 64-entry tile list), so they take the per-ray fallback pass
+    over every instance, next to list tiles elsewhere in the frame."""
+    models = [vx.Model.procedural(6, shell=True), vx.Model.random(9, 5, 0.1)]
+    s, o = pair(vx.config.STACKED, models, seed=5)
+    for culling, sorting in ((True, True), (True, False), (False, True)):
+        o_aov, o_img = check_fp64(s, o, culling, sorting)
+        check_fp32(s, o, o_aov, o_img, culling, sorting)
+
+
+def test_crowd_reduced(gpu):
+    """The crowd configuration with 512 animated
+    instances at 640x360, two animation times."""
+    models = [vx.Model.procedural(7, shell=True)]
+    s, o = pair(vx.config.CROWD, models, seed=512, w=640, h=360)
+    for t in (0.4, 2.3):
+        s.evaluate(t)
+        o.evaluate(t)
+        o_aov, o_img = check_fp64(s, o)
+        check_fp32(s, o, o_aov, o_img)
+
+
 def test_deep_model_depth_12(gpu):
     """A depth-12 shell (21 M nodes, 44 M attributes -- past the compact words'
     2^24 range, so the general words run at scale): FP64 per-ray bit-exact vs the
