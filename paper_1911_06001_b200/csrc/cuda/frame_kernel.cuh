@@ -262,6 +262,9 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
     uint32_t n_trav = 0, n_reuse = 0, n_fetch = 0, n_leaf = 0;
     const uint32_t n = p.n_inst;
     BlockStack stack{static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack + threadIdx.x))};
+    // opaque to the optimiser: kept in a register instead of being re-derived
+    // from %tid / the CTA window (6 instructions) on every push
+    asm volatile("" : "+r"(stack.base));
     const uint16_t* const list = s_list[warp];
 
     while (true) {
