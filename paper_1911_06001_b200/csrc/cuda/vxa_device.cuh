@@ -433,7 +433,7 @@ struct FastRay {
     // cells (x' = (x + h) / 2h), so node planes sit at exact dyadic positions
     // c * 2^-L and the scale 2h only multiplies t (folded into inv).
     float A[3];   // (-h - o_m) / 2h, rounded
-    float Ar[3];  // its FP64 rounding residual
+    float Ar[3];  // its FP64 rounding residual, times inv
     float inv[3]; // 2h / |d|
     // Pruning bound: subtrees entered at t >= t_lim cannot hold a hit that
     // beats the caller's best (t_lim = nextafter(best t), +inf for none).
@@ -450,12 +450,13 @@ struct FastHit {
 };
 
 // t of the plane at position i * sz (i integer-valued, sz = 2^-L) of one
-// mirrored axis: i * sz + A is exact inside the FMA up to one rounding; the
-// residual keeps it accurate when it cancels (a plane close to the origin).
-// Every plane gets one value whatever the level that computes it, so sibling
-// cells share planes bit for bit (the traversal is watertight).
-__device__ __forceinline__ float plane_t(float i, float sz, float A, float Ar, float inv) {
-    return __fmul_rn(__fadd_rn(__fmaf_rn(i, sz, A), Ar), inv);
+// mirrored axis: X = i * sz + A is exact inside the FMA up to one rounding, and
+// t = X * inv + Ari with Ari = A's FP64 rounding residual times inv, one more
+// rounding in the second FMA (the residual keeps t accurate when X cancels: a
+// plane close to the origin). Every plane gets one value whatever the level
+// that computes it, so sibling cells share planes bit for bit (watertight).
+__device__ __forceinline__ float plane_t(float i, float sz, float A, float Ari, float inv) {
+    return __fmaf_rn(__fmaf_rn(i, sz, A), inv, Ari);
 }
 
 __device__ __forceinline__ float zero_mid(const FastRay& r, int a, int level) {
@@ -500,8 +501,8 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
             const bool m = d[a] < 0.0f;
             if (m) r.mirror |= axis_bit(a);
             r.A[a] = m ? -A_hi[a] : A_lo[a];
-            r.Ar[a] = m ? -Ar_hi[a] : Ar_lo[a];
             r.inv[a] = __fdiv_rn(h2[a], fabsf(d[a]));
+            r.Ar[a] = __fmul_rn(m ? -Ar_hi[a] : Ar_lo[a], r.inv[a]);
             te = fmaxf(te, plane_t(0.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
             tx = fminf(tx, plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
         }
