@@ -276,6 +276,12 @@ __device__ __forceinline__ uint32_t first_child(const Real t0[3], const Real tm[
     return q;
 }
 
+// FP32 core: the entry value as one 3-way max (plane parameters are never NaN).
+__device__ __forceinline__ uint32_t first_child(const float t0[3], const float tm[3]) {
+    const float te = fmaxf(fmaxf(t0[0], t0[1]), t0[2]);
+    return (tm[0] < te ? 4u : 0u) | (tm[1] < te ? 2u : 0u) | (tm[2] < te ? 1u : 0u);
+}
+
 // next_node (traversal.cpp:88-103): exit axis = argmin t1 (strict <, x first).
 template <typename Real> __device__ __forceinline__ uint32_t next_child(const Real t1[3], uint32_t q) {
     uint32_t bit = 4u;
@@ -594,16 +600,10 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         float c0[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) c0[a] = (q & axis_bit(a)) ? tm[a] : t0[a];
-        int entry = 0;
-        float t_enter = c0[0];
-        if (c0[1] > t_enter) {
-            entry = 1;
-            t_enter = c0[1];
-        }
-        if (c0[2] > t_enter) {
-            entry = 2;
-            t_enter = c0[2];
-        }
+        // plane parameters are never NaN (finite, or +-inf on zero-direction
+        // axes), so max/min equal the reference's compare chains; the entry
+        // axis itself is only needed on a hit (below)
+        const float t_enter = fmaxf(fmaxf(c0[0], c0[1]), c0[2]);
         const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
         // the reference cull !(t_enter < t_exit) || t_exit < 0, plus the pruning
         // bound (t_enter >= t_lim: nothing in this child can beat the best)
@@ -614,7 +614,12 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             out.t = fmaxf(t_enter, 0.0f);
             out.parent = fidx;
             out.level = static_cast<uint32_t>(level + 1);
-            out.axis = static_cast<uint32_t>(entry);
+            // entry axis: argmax of c0, ties to the lower axis (traversal.cpp:214-222)
+            uint32_t entry = 0;
+            float te = c0[0];
+            if (c0[1] > te) entry = 1, te = c0[1];
+            if (c0[2] > te) entry = 2;
+            out.axis = entry;
             out.fetches = fetches;
             const uint32_t top = (2u << level) - 1u; // 2^(level+1) - 1
 #pragma unroll
