@@ -589,7 +589,13 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         float c1[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) c1[a] = (q & axis_bit(a)) ? t1[a] : tm[a];
-        fcur = next_child(c1, q);
+        // next_node: the exit axis is the first axis attaining min c1 (the
+        // strict-< chain's x-first tie rule); the min is also the child's t_exit
+        const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
+        {
+            const uint32_t xb = c1[0] == t_exit ? 4u : (c1[1] == t_exit ? 2u : 1u);
+            fcur = (q & xb) ? kExit : (q | xb);
+        }
         // An absent child is skipped before its interval is evaluated: the
         // reference culls first and checks node_child second, but both only
         // `continue`, so the order of the two tests is not observable.
@@ -604,7 +610,6 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         // axes), so max/min equal the reference's compare chains; the entry
         // axis itself is only needed on a hit (below)
         const float t_enter = fmaxf(fmaxf(c0[0], c0[1]), c0[2]);
-        const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
         // the reference cull !(t_enter < t_exit) || t_exit < 0, plus the pruning
         // bound (t_enter >= t_lim: nothing in this child can beat the best)
         if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
