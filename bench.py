@@ -258,6 +258,21 @@ def ncu_traffic(workload):
     return e.get("dram_bytes_per_launch") if e else None
 
 
+def ncu_compute(workload):
+    """Issue-side utilisation of the frame kernel from the same committed ncu
+    summary: the kernel is issue-bound, which the HBM fraction alone hides."""
+    p = os.path.join(ROOT, "profiles", "ncu_frame_kernel.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        e = json.load(f).get(workload)
+    if not e or "issue_active_pct" not in e:
+        return None
+    return {"bound": "instruction issue", "issue_active_pct": e["issue_active_pct"],
+            "alu_pipe_pct": e.get("alu_pipe_pct"), "active_lanes_per_inst": e.get("active_lanes_per_inst"),
+            "source": "profiles/ncu_frame_kernel.json (ncu --set full)"}
+
+
 def exchange_handle(dist, rank, handle: bytes) -> bytes:
     """Broadcast rank 0's 64-byte CUDA IPC framebuffer handle to every rank."""
     obj = [handle if rank == 0 else None]
@@ -621,7 +636,8 @@ def run_ours(args):
                          "per_ray": {"node_fetches": round(st.node_fetches / frames / pixels_mine, 4),
                                      "leaf_hits": round(st.leaf_hits / frames / pixels_mine, 4),
                                      "traversals": round(st.svo_traversals / frames / pixels_mine, 4),
-                                     "bytes": round(alg_bytes / pixels_mine, 3)}},
+                                     "bytes": round(alg_bytes / pixels_mine, 3)},
+                         "compute": ncu_compute(args.workload)},
             "cpu_baseline": base,
             "e2e": e2e,
             "extras": extras,
