@@ -278,6 +278,11 @@ void fold_instance(const std::map<uint32_t, ModelEntry>& models, const vxa_frame
         for (int i = 0; i < 9; ++i) d.M[i] = Rt[i];
     } else {
         for (int i = 0; i < 9; ++i) d.M[i] = static_cast<float>(d.Md[i]);
+        // A box with a non-positive (or non-finite) extent holds no hit for the
+        // reference (empty or inverted slab: the root test fails); the FP32
+        // unit-cube planes would divide by 2h, so the traversal is skipped.
+        for (int a = 0; a < 3; ++a)
+            if (!(h[a] > 0.0) || !std::isfinite(h[a])) d.valid_model = 0;
     }
 }
 

@@ -218,3 +218,42 @@ def test_deep_model_depth_12(gpu):
     s, o = pair(vx.config.C1, [m], w=128, h=128)
     o_aov, o_img = check_fp64(s, o)
     check_fp32(s, o, o_aov, o_img)
+
+
+def _rotation(seed):
+    q = np.random.default_rng(seed).normal(size=4)
+    w, x, y, z = q / np.linalg.norm(q)
+    return [1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w),
+            2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w),
+            2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_camera_inside_an_instance(gpu, seed):
+    """The camera inside an instance's box and bounding sphere (ray origins inside
+    the root cell: negative entry parameters, hits on the shell's inner side),
+    next to an ordinary instance; every culling/sorting option."""
+    models = [vx.Model.procedural(7, shell=True), vx.Model.random(seed, 5, 0.05)]
+    s, o = pair(vx.config.TWO_OBJECTS, models)
+    for sc in (s, o):
+        sc.set_object(0, _rotation(seed) + [0.1, -0.05, 7.8] + [3.0, 2.5, 3.5], True)
+        sc.set_object(1, _rotation(seed + 10) + [0.3, 0.2, 6.9] + [0.8, 0.8, 0.8], True)
+    for culling, sorting in ((True, True), (False, False), (True, False)):
+        o_aov, o_img = check_fp64(s, o, culling, sorting)
+        assert (o_aov["object_id"] >= 0).mean() > 0.5  # the inner shell fills the view
+        check_fp32(s, o, o_aov, o_img, culling, sorting)
+
+
+def test_degenerate_scales(gpu):
+    """Zero and negative scale components (rejected by the scene loader but
+    reachable through the API): the reference finds no hit in such a box; both
+    kernels agree with it (the FP32 kernel skips the instance)."""
+    models = [vx.Model.procedural(6, shell=True), vx.Model.random(3, 4, 0.4)]
+    s, o = pair(vx.config.TWO_OBJECTS, models)
+    for sc in (s, o):
+        sc.set_object(0, _rotation(5) + [-1.0, 0.0, 0.0] + [2.0, 0.0, 2.0], True)
+        sc.set_object(1, _rotation(6) + [1.5, 0.2, 0.0] + [-1.5, 1.5, 1.5], True)
+    for culling, sorting in ((True, True), (False, True)):
+        o_aov, o_img = check_fp64(s, o, culling, sorting)
+        rgb, aov, _ = s.render(culling, sorting, precision=vx.VXA_FP32, aov=True)
+        assert (rgb == o_img).all()
