@@ -72,6 +72,39 @@ __global__ void leaf_masks(const uint64_t* __restrict__ grid, uint32_t n, uint64
     }
 }
 
+// Four Morton-consecutive cubes 4q..4q+3 per thread (they differ in the
+// cube's lowest y and z bits): 2 x-rows x 4 y-rows of 4 z-bits each -- 8 word
+// loads and one 32-bit store for 4 cubes instead of 16 loads and 4 byte stores.
+__global__ void leaf_masks4(const uint64_t* __restrict__ grid, uint32_t n, uint64_t quads, uint32_t* __restrict__ v) {
+    for (uint64_t q = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; q < quads;
+         q += uint64_t{gridDim.x} * blockDim.x) {
+        const uint32_t code = static_cast<uint32_t>(q) << 2; // cube of the first of the four
+        const uint64_t x = compact3(code >> 2), y = compact3(code >> 1), z = compact3(code);
+        // voxel rows: x in {2x, 2x+1}, y in {2y .. 2y+3}; z bits 2z .. 2z+3 (2z is a multiple of 4)
+        uint32_t nib[2][4];
+#pragma unroll
+        for (uint32_t i = 0; i < 2; ++i)
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                const uint64_t b = ((2 * x + i) * n + (2 * y + j)) * n + 2 * z;
+                nib[i][j] = static_cast<uint32_t>(__ldg(grid + (b >> 6)) >> (b & 63)) & 0xfu;
+            }
+        uint32_t out = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) { // cube 4q + k: z0 = k & 1, y0 = k >> 1
+            const uint32_t z0 = k & 1u, y0 = k >> 1;
+            uint32_t mask = 0;
+#pragma unroll
+            for (uint32_t i = 0; i < 2; ++i)
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j)
+                    mask |= ((nib[i][2 * y0 + j] >> (2 * z0)) & 3u) << (4 * i + 2 * j);
+            out |= mask << (8 * k);
+        }
+        v[q] = out;
+    }
+}
+
 // V_{L-1}[c] bit o = (V_L[8c + o] != 0)
 __global__ void parent_masks(const uint64_t* __restrict__ child, uint64_t cubes, uint8_t* __restrict__ v) {
     for (uint64_t c = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; c < cubes;
@@ -172,6 +205,68 @@ __global__ void emit_level(LevelArgs a) {
     }
 }
 
+// Position of the r-th (0-based) set bit of an 8-bit mask (branch-free).
+__device__ __forceinline__ uint32_t nth_set_bit8(uint32_t m, uint32_t r) {
+    uint32_t p = 0;
+    const uint32_t c4 = __popc(m & 0xfu);
+    if (r >= c4) r -= c4, p = 4;
+    const uint32_t c2 = __popc((m >> p) & 0x3u);
+    if (r >= c2) r -= c2, p += 2;
+    return p + (r >= ((m >> p) & 1u) ? 1u : 0u);
+}
+
+// The last level (children are voxels), warp-cooperatively: a warp takes 32
+// consecutive nodes, whose attributes are one contiguous range of the output
+// (the scan). Lane j produces outputs j, j + 32, ... of that range; the node
+// of an output is found from the 32-bit map of node starts inside the current
+// 32-output chunk (one OR-reduction) plus the count of nodes starting before
+// it (one ballot); its octant is the r-th set bit of the node's mask. The
+// colour hash runs with every lane busy and the stores are fully coalesced
+// (the per-node octant loop of emit_level is divergent and its stores strided).
+__global__ void __launch_bounds__(256) emit_leaves(LevelArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warps = gridDim.x * (blockDim.x / 32u);
+    for (uint32_t g = blockIdx.x * (blockDim.x / 32u) + (threadIdx.x >> 5); g * 32u < a.n; g += warps) {
+        const uint32_t i = g * 32u + lane;
+        const uint32_t n_live = min(32u, a.n - g * 32u);
+        const bool live = lane < n_live;
+        const uint32_t c = live ? a.codes[i] : 0u;
+        const uint32_t valid = live ? a.v[c] : 0u;
+        const uint32_t e = live ? a.excl[i] : 0u;
+        if (live) {
+            const uint32_t node = a.first + i;
+            const uint32_t attr_base = valid ? e : 0u;
+            a.records[3 * size_t{node}] = 0u;
+            a.records[3 * size_t{node} + 1] = attr_base;
+            a.records[3 * size_t{node} + 2] = valid | (valid << 8);
+            if (a.cwords) a.cwords[node] = valid | (attr_base << 8);
+        }
+        // the node's cube, 10 bits per axis, voxel = 2 * cube + octant bit
+        const uint32_t xyz = (compact3(c >> 2) << 20) | (compact3(c >> 1) << 10) | compact3(c);
+        const uint32_t e0 = __shfl_sync(0xffffffffu, e, 0);
+        const uint32_t total = __shfl_sync(0xffffffffu, e + __popc(valid), n_live - 1u) - e0;
+        const uint32_t rel = e - e0; // this node's first output, relative to e0
+        for (uint32_t o0 = 0; o0 < total; o0 += 32u) {
+            // every live node has >= 1 voxel, so node starts are distinct
+            const bool starts_here = live && rel >= o0 && rel < o0 + 32u;
+            const uint32_t starts = __reduce_or_sync(0xffffffffu, starts_here ? 1u << (rel - o0) : 0u);
+            const uint32_t before = __popc(__ballot_sync(0xffffffffu, live && rel < o0));
+            const uint32_t k = before + __popc(starts & ((2u << lane) - 1u)) - 1u;
+            const uint32_t rk = __shfl_sync(0xffffffffu, rel, k);
+            const uint32_t vk = __shfl_sync(0xffffffffu, valid, k);
+            const uint32_t pk = __shfl_sync(0xffffffffu, xyz, k);
+            const uint32_t o = o0 + lane;
+            if (o < total) {
+                const uint32_t oct = nth_set_bit8(vk, o - rk);
+                const uint32_t x = 2u * (pk >> 20) + ((oct >> 2) & 1u);
+                const uint32_t y = 2u * ((pk >> 10) & 0x3ffu) + ((oct >> 1) & 1u);
+                const uint32_t z = 2u * (pk & 0x3ffu) + (oct & 1u);
+                a.attrs[e0 + o] = voxel_color(a.color_mode, a.color_constant, a.resolution, x, y, z);
+            }
+        }
+    }
+}
+
 inline size_t align_up(uint64_t b) { return static_cast<size_t>((b + 255) & ~uint64_t{255}); }
 
 } // namespace
@@ -213,7 +308,10 @@ cudaError_t build_svo(cudaStream_t s, const uint64_t* grid_dev, uint32_t depth, 
                                                                           8, uint64_t{1} << (3 * (depth - 1)))));
     tr.mark(s, "alloc V");
     const uint64_t top = uint64_t{1} << (3 * (depth - 1));
-    leaf_masks<<<grid_for(top), kThreads, 0, s>>>(grid_dev, n, top, V[depth - 1]);
+    if (top % 4 == 0)
+        leaf_masks4<<<grid_for(top / 4), kThreads, 0, s>>>(grid_dev, n, top / 4, reinterpret_cast<uint32_t*>(V[depth - 1]));
+    else
+        leaf_masks<<<grid_for(top), kThreads, 0, s>>>(grid_dev, n, top, V[depth - 1]);
     for (uint32_t L = depth - 1; L >= 1; --L) {
         const uint64_t cubes = uint64_t{1} << (3 * (L - 1));
         parent_masks<<<grid_for(cubes), kThreads, 0, s>>>(reinterpret_cast<const uint64_t*>(V[L]), cubes, V[L - 1]);
@@ -296,7 +394,10 @@ cudaError_t build_svo(cudaStream_t s, const uint64_t* grid_dev, uint32_t depth, 
         a.color_mode = color_mode;
         a.color_constant = color_constant;
         a.resolution = n;
-        emit_level<<<grid_for(nl), kThreads, 0, s>>>(a);
+        if (a.last)
+            emit_leaves<<<grid_for(nl), kThreads, 0, s>>>(a);
+        else
+            emit_level<<<grid_for(nl), kThreads, 0, s>>>(a);
         first += nl;
         std::swap(codes_a, codes_b);
     }
