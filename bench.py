@@ -622,7 +622,7 @@ def run_ours(args):
             "metric": "Mrays/s", "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "fps": round(1000.0 / ms_per_step, 2), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
                        "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False,
                        "partition": f"64x64 super-tiles round-robin over {world} GPU(s), NVLink peer stores",
