@@ -396,14 +396,25 @@ def run_ours(args):
             raise RuntimeError(f"{what}: {lib.vxa_last_error().decode()}")
 
     # multi-GPU: map rank 0's framebuffer into every rank (NVLink peer stores)
+    composition = "NVLink peer stores into rank 0's framebuffer (CUDA IPC)" if world > 1 else "single device"
     if world > 1:
         handle = (C.c_char * 64)()
         if rank == 0:
             check(lib.vxa_fb_export(ctx, W, H, handle), "fb_export")
         got = exchange_handle(dist, rank, bytes(handle))
+        ok = 1
         if rank != 0:
             h2 = (C.c_char * 64).from_buffer_copy(got)
-            check(lib.vxa_fb_import(ctx, W, H, h2), "fb_import")
+            if lib.vxa_fb_import(ctx, W, H, h2) != 0:
+                print(f"rank {rank}: vxa_fb_import failed ({lib.vxa_last_error().decode()}); "
+                      "rendering into the local framebuffer", file=sys.stderr)
+                ok = 0
+        import torch
+        t = torch.tensor([ok], dtype=torch.int32, device="cpu" if args.same_device else f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 0:
+            composition = ("none: CUDA IPC unavailable, each rank renders its super-tiles into its own "
+                           "framebuffer (no gather measured)")
 
     vxl = vx.voxanim()
 
@@ -480,7 +491,7 @@ def run_ours(args):
                 raise RuntimeError(vxl.vxn_last_error().decode())
             alone = np.empty((H, W, 3), np.uint8)
             check(lib.vxa_read_framebuffer(ctx, alone.ctypes.data, W, H), "read_framebuffer")
-            multi_ok = bool((composed == alone).all())
+            multi_ok = bool((composed == alone).all()) if composition.startswith("NVLink") else None
         barrier()
 
     # end to end through the public API (voxanim::render_frame with host buffers)
@@ -625,7 +636,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
                        "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False,
-                       "partition": f"64x64 super-tiles round-robin over {world} GPU(s), NVLink peer stores",
+                       "partition": f"64x64 super-tiles round-robin over {world} GPU(s)",
+                       "composition": composition,
                        "l2": "flushed between timed steps (256 MB write)" if not args.no_flush else "warm",
                        "model_bytes_device": None},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
