@@ -257,3 +257,16 @@ def test_degenerate_scales(gpu):
         o_aov, o_img = check_fp64(s, o, culling, sorting)
         rgb, aov, _ = s.render(culling, sorting, precision=vx.VXA_FP32, aov=True)
         assert (rgb == o_img).all()
+
+
+def test_super_tile_list_overflow(gpu):
+    """1500 instances in a 64x36 frame: one super-tile whose cone meets more than
+    the 1024-entry super-tile list, so its tiles fall back to testing every
+    instance (the pre-pass overflow path); 8x4 tile lists then overflow too."""
+    models = [vx.Model.procedural(5, shell=True)]
+    s, o = pair(vx.config.CROWD, models, seed=1500, w=64, h=36)
+    for t in (0.0, 1.7):
+        s.evaluate(t)
+        o.evaluate(t)
+        o_aov, o_img = check_fp64(s, o)
+        check_fp32(s, o, o_aov, o_img)
