@@ -133,16 +133,19 @@ struct TileCone {
 };
 
 // Cone of the pixel-centre rays of the w x h pixel region at (x0, y0).
-__device__ __forceinline__ TileCone region_cone(const FrameParams<float>& p, int x0, int y0, float w, float h) {
-    const float cxs = fmaf(static_cast<float>(x0) + 0.5f * w, p.inv_w2, -1.0f) * p.sx;
-    const float cys = fmaf(-(static_cast<float>(y0) + 0.5f * h), p.inv_h2, 1.0f) * p.sy;
+template <typename Real>
+__device__ __forceinline__ TileCone region_cone(const FrameParams<Real>& p, int x0, int y0, float w, float h) {
+    const float inv_w2 = static_cast<float>(p.inv_w2), inv_h2 = static_cast<float>(p.inv_h2);
+    const float sx = static_cast<float>(p.sx), sy = static_cast<float>(p.sy);
+    const float cxs = fmaf(static_cast<float>(x0) + 0.5f * w, inv_w2, -1.0f) * sx;
+    const float cys = fmaf(-(static_cast<float>(y0) + 0.5f * h), inv_h2, 1.0f) * sy;
     const float cn = rsqrtf(cxs * cxs + cys * cys + 1.0f);
     const float ax = cxs * cn, ay = cys * cn, az = -cn;
     float smax = 0.0f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float xs = fmaf(static_cast<float>(x0) + ((k & 1) ? w - 0.5f : 0.5f), p.inv_w2, -1.0f) * p.sx;
-        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2) ? h - 0.5f : 0.5f)), p.inv_h2, 1.0f) * p.sy;
+        const float xs = fmaf(static_cast<float>(x0) + ((k & 1) ? w - 0.5f : 0.5f), inv_w2, -1.0f) * sx;
+        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2) ? h - 0.5f : 0.5f)), inv_h2, 1.0f) * sy;
         const float n = rsqrtf(xs * xs + ys * ys + 1.0f);
         const float bx = xs * n, by = ys * n, bz = -n;
         // |a x b| = sin of the angle (accurate for small angles, unlike 1 - cos)
@@ -152,11 +155,13 @@ __device__ __forceinline__ TileCone region_cone(const FrameParams<float>& p, int
     TileCone c;
     c.sin_a = fminf(1.0f, smax * 1.01f + 1e-6f);
     c.cos_a = sqrtf(fmaxf(0.0f, 1.0f - c.sin_a * c.sin_a));
-    for (int k = 0; k < 3; ++k) c.a[k] = p.C[3 * k] * ax + p.C[3 * k + 1] * ay + p.C[3 * k + 2] * az;
+    for (int k = 0; k < 3; ++k)
+        c.a[k] = static_cast<float>(p.C[3 * k]) * ax + static_cast<float>(p.C[3 * k + 1]) * ay +
+                 static_cast<float>(p.C[3 * k + 2]) * az;
     return c;
 }
 
-__device__ __forceinline__ TileCone tile_cone(const FrameParams<float>& p, int x0, int y0) {
+template <typename Real> __device__ __forceinline__ TileCone tile_cone(const FrameParams<Real>& p, int x0, int y0) {
     return region_cone(p, x0, y0, static_cast<float>(kTileW), static_cast<float>(kTileH));
 }
 
@@ -280,9 +285,12 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         const int px = tx0 + static_cast<int>(lane % kTileW);
         const int py = ty0 + static_cast<int>(lane / kTileW);
 
-        // ---- tile candidate list (FP32 production kernel with culling)
+        // ---- tile candidate list (culling on). Conservative: a sphere missing the
+        // inflated tile cone misses every ray of the tile, in either kernel; the
+        // list keeps instance order, so the FP64 kernel's candidates, their order
+        // and its ties are those of the per-ray pass over every instance.
         uint32_t list_n = 0xffffffffu; // 0xffffffff: per-ray pass over every instance
-        if constexpr (sizeof(Real) == 4) {
+        {
             if (p.culling && n <= 0xffffu) {
                 const TileCone cone = tile_cone(p, tx0, ty0);
                 // source: the super-tile's candidate list when the pre-pass ran

@@ -367,7 +367,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     // one upload: the instance records, then (FP32) the float4 cull table,
     // folded straight into the pinned staging slot
     const size_t inst_bytes = (size_t{n} * sizeof(DevInstance<Real>) + 15) & ~size_t{15};
-    const size_t cull_bytes = sizeof(Real) == 4 ? size_t{n} * sizeof(float4) : 0;
+    const size_t cull_bytes = size_t{n} * sizeof(float4); // tile culling (both kernels)
     const size_t bytes = inst_bytes + cull_bytes;
     if (int rc = ensure_staging(ctx, bytes); rc != VXA_OK) return rc;
     VXA_CUDA(ctx->inst_dev.ensure(std::max<size_t>(bytes, 16)));
