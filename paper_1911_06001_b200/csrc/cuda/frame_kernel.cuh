@@ -202,8 +202,27 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         if constexpr (kAov) path_to_voxel(h.path, h.level, vox);
     } else {
         float d[3];
-        for (int k = 0; k < 3; ++k)
-            d[k] = static_cast<float>((fma(in.Md[3 * k], rd.dcx, in.Md[3 * k + 1] * rd.dcy) - in.Md[3 * k + 2]) * rd.rnd);
+        double dd[3];
+        for (int k = 0; k < 3; ++k) {
+            dd[k] = (fma(in.Md[3 * k], rd.dcx, in.Md[3 * k + 1] * rd.dcy) - in.Md[3 * k + 2]) * rd.rnd;
+            d[k] = static_cast<float>(dd[k]);
+        }
+        // Content sphere (conservative, margin included): every leaf lies inside
+        // it, so a ray whose line misses it -- or that is outside it and moving
+        // away -- hits nothing here; the traversal is skipped. FP64 unit-cube
+        // coordinates: origin -U_lo (plus residual) relative to the centre 0.5.
+        if (in.model.content_r2 < 0.75f) {
+            double qq = 0.0, qw = 0.0, ww = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                const double q = -(static_cast<double>(in.U_lo[k]) + static_cast<double>(in.Ur_lo[k])) - 0.5;
+                const double w = dd[k] / static_cast<double>(in.h2[k]);
+                qq = fma(q, q, qq);
+                qw = fma(q, w, qw);
+                ww = fma(w, w, ww);
+            }
+            const double r2 = static_cast<double>(in.model.content_r2);
+            if (qq - qw * qw / ww > r2 || (qw > 0.0 && qq > r2)) return;
+        }
         FastRay fr;
         // Only a hit at t <= best.t can change the nearest (t, id) (ties go to
         // the lower id), so subtrees entered beyond best.t are pruned.

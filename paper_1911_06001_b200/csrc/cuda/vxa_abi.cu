@@ -610,6 +610,50 @@ int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t
     return VXA_OK;
 }
 
+// Radius, in unit-cube coordinates about the cube centre, of a sphere holding
+// every leaf: the farthest corner of any occupied cell at level min(depth, 5)
+// (a cell bounds its whole subtree) or of a leaf above that level. Returned
+// squared with a small margin; the FP32 kernel skips the traversal of rays whose
+// line misses it (a shell's box corners). Walks at most 4681 nodes.
+float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
+    const int K = static_cast<int>(std::min<uint32_t>(depth, 5u));
+    struct Cell {
+        uint32_t idx, x, y, z;
+    };
+    std::vector<Cell> cur{{0, 0, 0, 0}}, next;
+    double r2 = 0.0;
+    const auto corner2 = [](uint32_t x, uint32_t y, uint32_t z, int L) {
+        const double sz = std::ldexp(1.0, -L);
+        double acc = 0.0;
+        for (const uint32_t c : {x, y, z}) {
+            const double lo = c * sz - 0.5, hi = (c + 1) * sz - 0.5;
+            acc += std::max(lo * lo, hi * hi);
+        }
+        return acc;
+    };
+    for (int L = 0; L < K; ++L) {
+        next.clear();
+        for (const Cell& c : cur) {
+            if (c.idx >= node_count) return 1.0f; // not a well-formed model: no bound
+            const uint8_t* r = raw + 12 * size_t{c.idx};
+            uint32_t cb;
+            std::memcpy(&cb, r, 4);
+            const uint32_t valid = r[8], leaf = r[9], internal = valid & ~leaf & 0xffu;
+            for (uint32_t o = 0; o < 8; ++o) {
+                if (!((valid >> o) & 1u)) continue;
+                const uint32_t x = 2 * c.x + ((o >> 2) & 1u), y = 2 * c.y + ((o >> 1) & 1u), z = 2 * c.z + (o & 1u);
+                if (((leaf >> o) & 1u) || L + 1 == K)
+                    r2 = std::max(r2, corner2(x, y, z, L + 1));
+                else
+                    next.push_back({cb + static_cast<uint32_t>(__builtin_popcount(internal & ((1u << o) - 1u))), x, y, z});
+            }
+        }
+        cur.swap(next);
+    }
+    const double rho = std::sqrt(r2) * (1.0 + 1e-5) + 1e-5;
+    return static_cast<float>(rho * rho);
+}
+
 int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const void* attrs, uint32_t attr_count,
                      uint32_t depth, uint32_t* handle_out) {
     if (ctx == nullptr || handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
@@ -692,6 +736,7 @@ int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const
     m.dev.attrs = m.attrs;
     m.dev.depth = depth;
     m.dev.node_count = node_count;
+    m.dev.content_r2 = content_r2(raw, node_count, depth);
     m.attr_count = attr_count;
     m.bytes = sizeof(uint2) * uint64_t{node_count} + (any_mixed ? 4ull * node_count : 0) + 4ull * attr_count +
               (m.cwords ? 4ull * node_count : 0) + raw_bytes;
@@ -807,6 +852,13 @@ int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, ui
     m.dev.attrs = m.attrs;
     m.dev.depth = depth;
     m.dev.node_count = static_cast<uint32_t>(b.node_count);
+    {
+        // the top levels are the first records (BFS order): at most 4681 nodes above level 5
+        const size_t top = std::min<uint64_t>(b.node_count, 4681);
+        std::vector<uint8_t> head(12 * top);
+        VXA_CUDA(cudaMemcpy(head.data(), m.raw, head.size(), cudaMemcpyDeviceToHost));
+        m.dev.content_r2 = content_r2(head.data(), static_cast<uint32_t>(top), depth);
+    }
     m.attr_count = b.attr_count;
     m.bytes = (8 + 12 + (m.cwords ? 4 : 0)) * b.node_count + 4 * b.attr_count;
     const uint32_t handle = ctx->next_handle++;

@@ -58,6 +58,11 @@ struct DevModel {
     const uint32_t* attrs;
     uint32_t depth;
     uint32_t node_count;
+    // Squared radius (unit-cube coordinates, about the cube centre, margin
+    // included) of a sphere holding every leaf (vxa_abi.cu: content_radius);
+    // >= 0.75 when it is no tighter than the cube's own corners.
+    float content_r2;
+    uint32_t pad;
 };
 
 // Node word policies of the FP32 core.
