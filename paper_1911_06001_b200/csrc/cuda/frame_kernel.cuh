@@ -27,7 +27,9 @@ constexpr int kBlock = 128;
 #endif
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kListCap = 64;
-using BlockStack = SmemStack<kBlock * sizeof(uint2)>; // per-warp tile candidate list (bit positions of a u64 mask)
+struct BlockStack : SmemStack<kBlock * sizeof(uint2)> {
+    uint32_t base_top; // shared address of the staged top node words (VXA_SMEM_TOP)
+}; // per-warp tile candidate list (bit positions of a u64 mask)
 
 template <typename Real> struct Best {
     bool have;
@@ -231,8 +233,16 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits, t_lim)) return;
         FastHit h;
         bool hit;
-        if constexpr (kCompact)
-            hit = traverse_fast<kAov>(CompactNodes{in.model.cwords}, static_cast<int>(in.model.depth), fr, h, stack);
+        if constexpr (kCompact) {
+            CompactNodes nodes{in.model.cwords};
+            if constexpr (VXA_SMEM_TOP > 0) {
+                if (in.model.cwords == p.top_words) {
+                    nodes.top_base = stack.base_top;
+                    nodes.top_n = p.top_n;
+                }
+            }
+            hit = traverse_fast<kAov>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+        }
         else
             hit = traverse_fast<kAov>(WideNodes{in.model.words, in.model.side}, static_cast<int>(in.model.depth), fr, h,
                                       stack);
@@ -285,7 +295,40 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
     // rays and sphere tests per frame are known on the host (pixels x objects)
     uint32_t n_trav = 0, n_reuse = 0, n_fetch = 0, n_leaf = 0;
     const uint32_t n = p.n_inst;
-    BlockStack stack{static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack + threadIdx.x))};
+    BlockStack stack;
+    stack.base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack + threadIdx.x));
+    stack.base_top = 0;
+    if constexpr (sizeof(Real) == 4 && VXA_SMEM_TOP > 0) {
+        // Stage the scene model's first VXA_SMEM_TOP node words (its top levels, BFS
+        // order) into shared memory behind the stack: one bulk copy (TMA engine)
+        // completing on an mbarrier, issued by one thread.
+        __shared__ __align__(8) unsigned long long top_bar;
+        const uint32_t top = static_cast<uint32_t>(__cvta_generic_to_shared(
+            reinterpret_cast<unsigned char*>(smem_stack) + sizeof(uint2) * kBlock * p.max_depth));
+        stack.base_top = top;
+        if (p.top_words != nullptr && p.top_n > 0) {
+            const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&top_bar));
+            const uint32_t bytes = 4u * p.top_n;
+            if (threadIdx.x == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(top),
+                    "l"(p.top_words), "r"(bytes), "r"(bar)
+                    : "memory");
+            }
+            __syncthreads(); // the barrier is initialised before anyone waits on it
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done)
+                    : "r"(bar)
+                    : "memory");
+            }
+        }
+    }
     // opaque to the optimiser: kept in a register instead of being re-derived
     // from %tid / the CTA window (6 instructions) on every push
     asm volatile("" : "+r"(stack.base));

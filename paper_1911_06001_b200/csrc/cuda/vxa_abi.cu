@@ -423,6 +423,24 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
             p.max_depth = std::max(p.max_depth, std::min(di.model.depth, kMaxDepth));
             if (di.model.cwords == nullptr) p.compact = 0;
         }
+    // the scene's single model (compact words), whose top node words the FP32
+    // kernel stages in shared memory in VXA_SMEM_TOP builds
+    p.top_words = nullptr;
+    p.top_n = 0;
+    if constexpr (sizeof(Real) == 4) {
+        const uint32_t* only = nullptr;
+        uint32_t nodes = 0;
+        bool single = true;
+        for (uint32_t k = 0; k < n && single; ++k)
+            if (tab[k].valid_model) {
+                if (only == nullptr) only = tab[k].model.cwords, nodes = tab[k].model.node_count;
+                else if (tab[k].model.cwords != only) single = false;
+            }
+        if (single && only != nullptr) {
+            p.top_words = only;
+            p.top_n = std::min<uint32_t>(kSmemTopWords, nodes) & ~3u;
+        }
+    }
     // VOXANIM_NODE_WORDS=wide forces the general words (tests, A/B timing); read per frame
     if (const char* env = std::getenv("VOXANIM_NODE_WORDS"); env && std::strcmp(env, "wide") == 0) p.compact = 0;
     p.tile_counter = ctx->tile_counter.ptr;

@@ -65,6 +65,9 @@ struct DevModel {
     uint32_t pad;
 };
 
+// (FrameParams::top_words: the model whose first VXA_SMEM_TOP node words the
+// frame kernel stages in shared memory, when every instance uses it.)
+
 // Node word policies of the FP32 core.
 // WideNodes: {valid | leaf << 8 | mixed, base} for any valid model.
 // CompactNodes: valid | base << 8 (base < 2^24), for canonical models -- leaves
@@ -87,10 +90,27 @@ struct WideNodes {
     }
 };
 
+// Node words staged in shared memory (build variant VXA_SMEM_TOP = words):
+// the first top_n words of the scene's model (BFS order: its top levels).
+#ifndef VXA_SMEM_TOP
+#define VXA_SMEM_TOP 0
+#endif
+
 struct CompactNodes {
     const uint32_t* w;
+    uint32_t top_base = 0; // shared address of the staged words (VXA_SMEM_TOP builds)
+    uint32_t top_n = 0;    // words staged for this model (0: none)
     using Word = uint32_t;
-    __device__ __forceinline__ Word load(uint32_t i) const { return __ldg(w + i); }
+    __device__ __forceinline__ Word load(uint32_t i) const {
+        if constexpr (VXA_SMEM_TOP > 0) {
+            if (i < top_n) {
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(top_base + 4u * i));
+                return v;
+            }
+        }
+        return __ldg(w + i);
+    }
     __device__ __forceinline__ static uint32_t valid(Word x) { return x & 0xffu; }
     __device__ __forceinline__ static uint32_t leaves(Word x, int level, int depth) {
         return level + 1 == depth ? (x & 0xffu) : 0u;
@@ -139,6 +159,8 @@ template <typename Real> struct FrameParams {
     const uint16_t* super_list;
     const uint32_t* super_count;
     uint32_t super_cap;
+    const uint32_t* top_words; // compact words of the scene's single model, or null
+    uint32_t top_n;            // words to stage (<= VXA_SMEM_TOP and the model size, multiple of 4)
     uint32_t n_inst;
     int32_t width, height;
     // camera

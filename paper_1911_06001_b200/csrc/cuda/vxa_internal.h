@@ -33,6 +33,8 @@ struct FrameLaunch {
     cudaStream_t stream;
 };
 
+// Node words the FP32 frame kernel stages in shared memory (0 = off; build variant).
+constexpr uint32_t kSmemTopWords = VXA_SMEM_TOP;
 // Per-super-tile candidate lists for large scenes (frame_kernel.cuh: super_cull_kernel).
 cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, cudaStream_t s);
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l);
