@@ -51,6 +51,9 @@ vxn_scene* vxn_scene_config(int config, vxn_model* const* models, uint32_t n_mod
 int vxn_scene_evaluate(vxn_scene* s, double time);
 int vxn_scene_mark_clean(vxn_scene* s);
 int vxn_scene_set_camera_dirty(vxn_scene* s, int dirty);
+/* camera = make_look_at_camera(position, look_at, up, fov, width, height) (scene.cpp:22-55); dirty set */
+int vxn_scene_set_camera(vxn_scene* s, const double* position3, const double* look_at3, const double* up3,
+                         double vertical_fov_deg, int width, int height);
 int vxn_scene_object_count(const vxn_scene* s);
 /* Per-object RigidTransform (15 doubles: rotation 9, translation 3, scale 3) + dirty flag. */
 int vxn_scene_get_object(const vxn_scene* s, int index, int32_t* id, double* transform15, int* dirty);

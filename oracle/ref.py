@@ -64,6 +64,7 @@ def lib() -> C.CDLL:
             "vref_scene_evaluate": (i, P, d),
             "vref_scene_mark_clean": (i, P),
             "vref_scene_set_camera_dirty": (i, P, i),
+            "vref_scene_set_camera": (i, P, P, P, P, d, i, i),
             "vref_scene_get_object": (i, P, i, C.POINTER(C.c_int32), C.POINTER(d), C.POINTER(i)),
             "vref_scene_set_object": (i, P, i, C.POINTER(d), i),
             "vref_scene_free": (None, P),
@@ -171,6 +172,13 @@ class RefScene:
         oid, tf, dirty = C.c_int32(), (C.c_double * 15)(), C.c_int()
         _ok(lib().vref_scene_get_object(self._h, i, C.byref(oid), tf, C.byref(dirty)), "get_object")
         return oid.value, list(tf), bool(dirty.value)
+
+    def set_camera(self, position, look_at, up=(0.0, 1.0, 0.0), fov_deg=60.0, width=None, height=None):
+        w, h = width or self.width, height or self.height
+        P3 = C.c_double * 3
+        _ok(lib().vref_scene_set_camera(self._h, P3(*position), P3(*look_at), P3(*up), float(fov_deg), w, h),
+            "set_camera")
+        self.width, self.height = w, h
 
     def set_object(self, i, transform15, dirty):
         tf = (C.c_double * 15)(*transform15)

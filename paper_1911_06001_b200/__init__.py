@@ -179,6 +179,14 @@ class Scene:
     def mark_clean(self) -> None:
         voxanim().vxn_scene_mark_clean(self._h)
 
+    def set_camera(self, position, look_at, up=(0.0, 1.0, 0.0), fov_deg=60.0, width=None, height=None) -> None:
+        """camera = make_look_at_camera(...) (dirty); the resolution is kept unless given."""
+        w, h = width or self.width, height or self.height
+        P3 = C.c_double * 3
+        _check(voxanim().vxn_scene_set_camera(self._h, P3(*position), P3(*look_at), P3(*up), float(fov_deg), w, h),
+               "set_camera")
+        self.width, self.height = w, h
+
     def set_camera_dirty(self, dirty: bool) -> None:
         voxanim().vxn_scene_set_camera_dirty(self._h, 1 if dirty else 0)
 

@@ -172,6 +172,7 @@ VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
     "vxn_model_from_grid", "vxn_grid_primitive", "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
+    "vxn_scene_set_camera",
     "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit", "vxn_scene_stream",
     "vxn_hbo_create", "vxn_hbo_free", "vxn_render", "vxn_traverse", "vxn_context",
 ]
@@ -252,6 +253,7 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_scene_evaluate", i, P, d)
     _declare(lib, "vxn_scene_mark_clean", i, P)
     _declare(lib, "vxn_scene_set_camera_dirty", i, P, i)
+    _declare(lib, "vxn_scene_set_camera", i, P, P, P, P, d, i, i)
     _declare(lib, "vxn_scene_object_count", i, P)
     _declare(lib, "vxn_scene_get_object", i, P, i, C.POINTER(C.c_int32), C.POINTER(d), C.POINTER(i))
     _declare(lib, "vxn_scene_set_object", i, P, i, C.POINTER(d), i)

@@ -178,6 +178,18 @@ int vxn_scene_mark_clean(vxn_scene* s) {
     return 0;
 }
 
+int vxn_scene_set_camera(vxn_scene* s, const double* pos, const double* at, const double* up, double fov, int width,
+                         int height) {
+    return guard(
+        [&] {
+            s->s.camera = voxanim::make_look_at_camera({pos[0], pos[1], pos[2]}, {at[0], at[1], at[2]},
+                                                       {up[0], up[1], up[2]}, fov, width, height);
+            s->s.camera.dirty = true;
+            return 0;
+        },
+        -1);
+}
+
 int vxn_scene_set_camera_dirty(vxn_scene* s, int dirty) {
     s->s.camera.dirty = dirty != 0;
     return 0;
