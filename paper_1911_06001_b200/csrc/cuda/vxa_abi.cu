@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -152,6 +153,9 @@ template <typename T> struct DevBuf {
 } // namespace
 
 struct vxa_ctx {
+    // Serialises the API calls on this context (its buffers, streams and
+    // counters are shared state); recursive: some entry points call others.
+    std::recursive_mutex mu;
     int device = 0;
     int sm_count = 0;
     char name[256] = {};
@@ -622,6 +626,7 @@ int vxa_destroy(vxa_ctx* ctx) {
 
 int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t name_len) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (device) *device = ctx->device;
     if (sm_count) *sm_count = ctx->sm_count;
     if (name && name_len) std::snprintf(name, name_len, "%s", ctx->name);
@@ -675,6 +680,7 @@ float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
 int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const void* attrs, uint32_t attr_count,
                      uint32_t depth, uint32_t* handle_out) {
     if (ctx == nullptr || handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (nodes == nullptr || node_count == 0) return fail(VXA_ERR_MODEL, "model has no root node");
     if (depth < 1 || depth > kMaxDepth) return fail(VXA_ERR_MODEL, "depth out of range [1, 16]");
     if (attr_count > 0 && attrs == nullptr) return fail(VXA_ERR_INVALID, "null attribute array");
@@ -768,6 +774,7 @@ int vxa_upload_svo(vxa_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* ha
     if (format_error) *format_error = -1;
     if (ctx == nullptr || handle_out == nullptr || (bytes == nullptr && size > 0))
         return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto bad = [&](int code, const std::string& msg) {
         if (format_error) *format_error = code;
         return fail(VXA_ERR_MODEL, msg);
@@ -806,6 +813,7 @@ int vxa_upload_svo(vxa_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* ha
 
 int vxa_release_model(vxa_ctx* ctx, uint32_t handle) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->models.find(handle);
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     cudaSetDevice(ctx->device);
@@ -817,6 +825,7 @@ int vxa_release_model(vxa_ctx* ctx, uint32_t handle) {
 
 int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32_t* node_format) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->models.find(handle);
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     if (device_bytes) *device_bytes = it->second.bytes;
@@ -827,6 +836,7 @@ int vxa_model_info(vxa_ctx* ctx, uint32_t handle, uint64_t* device_bytes, uint32
 int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, uint32_t color_mode,
                     uint32_t color_rgba, uint32_t* handle_out, uint64_t* node_count, uint64_t* attr_count) {
     if (ctx == nullptr || handle_out == nullptr || grid_words == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     // build_from_grid's argument checks (svo.cpp:80-87) plus the dense-grid cap (ingest.cpp:15)
     if (depth < 1 || depth > 10) return fail(VXA_ERR_INVALID, "octree depth must be in [1, 10] for a dense grid");
     if (color_mode > 2) return fail(VXA_ERR_INVALID, "unknown colour mode");
@@ -890,6 +900,7 @@ int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, ui
 int vxa_model_download(vxa_ctx* ctx, uint32_t handle, void* nodes, uint64_t node_cap, uint32_t* attrs,
                        uint64_t attr_cap) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->models.find(handle);
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     const ModelEntry& m = it->second;
@@ -905,6 +916,7 @@ int vxa_model_download(vxa_ctx* ctx, uint32_t handle, void* nodes, uint64_t node
 
 int vxa_model_counts(vxa_ctx* ctx, uint32_t handle, uint32_t* depth, uint64_t* node_count, uint64_t* attr_count) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->models.find(handle);
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     if (depth) *depth = it->second.dev.depth;
@@ -916,6 +928,7 @@ int vxa_model_counts(vxa_ctx* ctx, uint32_t handle, uint32_t* depth, uint64_t* n
 int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, uint8_t* rgb_out,
                vxa_pixel_aov* aov_out, vxa_stats* stats) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (int rc = check_frame(f); rc != VXA_OK) return rc;
     if (n > 0 && in == nullptr) return fail(VXA_ERR_INVALID, "null instance array");
     VXA_CUDA(cudaSetDevice(ctx->device));
@@ -976,6 +989,7 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
 
 int vxa_hbo_create(vxa_ctx* ctx, int32_t width, int32_t height, uint32_t* handle_out) {
     if (ctx == nullptr || handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (width < 1 || height < 1) return fail(VXA_ERR_INVALID, "bad hit buffer size");
     VXA_CUDA(cudaSetDevice(ctx->device));
     const size_t n = static_cast<size_t>(width) * height;
@@ -997,6 +1011,7 @@ int vxa_hbo_create(vxa_ctx* ctx, int32_t width, int32_t height, uint32_t* handle
 
 int vxa_hbo_release(vxa_ctx* ctx, uint32_t handle) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->hbos.find(handle);
     if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
     cudaSetDevice(ctx->device);
@@ -1008,6 +1023,7 @@ int vxa_hbo_release(vxa_ctx* ctx, uint32_t handle) {
 
 int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out) {
     if (ctx == nullptr || out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->hbos.find(handle);
     if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
     VXA_CUDA(cudaSetDevice(ctx->device));
@@ -1019,6 +1035,7 @@ int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out) {
 
 int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (int rc = check_frame(f); rc != VXA_OK) return rc;
     if (f->hbo) return fail(VXA_ERR_INVALID, "vxa_submit does not take a host hit buffer");
     if (n > 0 && in == nullptr) return fail(VXA_ERR_INVALID, "null instance array");
@@ -1037,6 +1054,7 @@ int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
 int vxa_submit_readback(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n,
                         uint8_t* rgb_out, uint64_t* ticket) {
     if (ctx == nullptr || rgb_out == nullptr || ticket == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (int rc = vxa_submit(ctx, f, in, n); rc != VXA_OK) return rc;
     const size_t npix = static_cast<size_t>(f->camera.width) * f->camera.height;
     const int slot = static_cast<int>(ctx->rb_next & 1u);
@@ -1057,6 +1075,7 @@ int vxa_submit_readback(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instanc
 
 int vxa_wait_readback(vxa_ctx* ctx, uint64_t ticket) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (ticket >= ctx->rb_next) return fail(VXA_ERR_INVALID, "unknown readback ticket");
     if (ticket + 2 < ctx->rb_next) return VXA_OK; // its slot has been reused: already complete
     VXA_CUDA(cudaEventSynchronize(ctx->rb_done[ticket & 1u]));
@@ -1065,18 +1084,21 @@ int vxa_wait_readback(vxa_ctx* ctx, uint64_t ticket) {
 
 int vxa_synchronize(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
     return VXA_OK;
 }
 
 int vxa_stats_read(vxa_ctx* ctx, vxa_stats* stats) {
     if (ctx == nullptr || stats == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     *stats = vxa_stats{};
     return read_counters(ctx, stats);
 }
 
 int vxa_stats_reset(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
     ctx->k_count = 0;
     ctx->aux_launches = 0;
@@ -1087,6 +1109,7 @@ int vxa_stats_reset(vxa_ctx* ctx) {
 
 int vxa_read_framebuffer(vxa_ctx* ctx, uint8_t* rgb_out, int32_t width, int32_t height) {
     if (ctx == nullptr || rgb_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (width != ctx->fb_w || height != ctx->fb_h) return fail(VXA_ERR_INVALID, "framebuffer size mismatch");
     const size_t npix = static_cast<size_t>(width) * height;
     VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
@@ -1100,6 +1123,7 @@ int vxa_read_framebuffer(vxa_ctx* ctx, uint8_t* rgb_out, int32_t width, int32_t 
 
 int vxa_host_register(vxa_ctx* ctx, void* ptr, size_t bytes) {
     if (ctx == nullptr || ptr == nullptr || bytes == 0) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaSetDevice(ctx->device));
     VXA_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
     return VXA_OK;
@@ -1107,6 +1131,7 @@ int vxa_host_register(vxa_ctx* ctx, void* ptr, size_t bytes) {
 
 int vxa_host_unregister(vxa_ctx* ctx, void* ptr) {
     if (ctx == nullptr || ptr == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaSetDevice(ctx->device));
     VXA_CUDA(cudaHostUnregister(ptr));
     return VXA_OK;
@@ -1114,12 +1139,14 @@ int vxa_host_unregister(vxa_ctx* ctx, void* ptr) {
 
 int vxa_timer_begin(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaEventRecord(ctx->t_a, ctx->stream));
     return VXA_OK;
 }
 
 int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms) {
     if (ctx == nullptr || elapsed_ms == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaEventRecord(ctx->t_b, ctx->stream));
     VXA_CUDA(cudaEventSynchronize(ctx->t_b));
     float ms = 0.f;
@@ -1130,6 +1157,7 @@ int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms) {
 
 int vxa_flush_l2(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const size_t bytes = size_t{256} << 20; // 2x the 126 MB L2
     VXA_CUDA(ctx->l2_scratch.ensure(bytes));
     VXA_CUDA(cudaMemsetAsync(ctx->l2_scratch.ptr, ctx->inst_slot, bytes, ctx->stream));
@@ -1140,6 +1168,7 @@ void* vxa_stream(vxa_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : 
 
 int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_out) {
     if (ctx == nullptr || ipc_handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (width < 1 || height < 1) return fail(VXA_ERR_INVALID, "bad framebuffer size");
     VXA_CUDA(cudaSetDevice(ctx->device));
     VXA_CUDA(ctx->fb.ensure(static_cast<size_t>(width) * height));
@@ -1153,6 +1182,7 @@ int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_
 
 int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle) {
     if (ctx == nullptr || ipc_handle == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaSetDevice(ctx->device));
     if (ctx->peer_fb) {
         cudaIpcCloseMemHandle(ctx->peer_fb);
@@ -1179,6 +1209,7 @@ int vxa_traverse(vxa_ctx* ctx, uint32_t model, const vxa_local_ray* rays, uint32
     static_assert(sizeof(vxa_traverse_hit) == sizeof(TraverseRayOut));
     static_assert(sizeof(vxa_visit) == sizeof(VisitOut));
     if (ctx == nullptr || (n > 0 && (rays == nullptr || hits == nullptr))) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     const auto it = ctx->models.find(model);
     if (it == ctx->models.end()) return fail(VXA_ERR_INVALID, "unknown model handle");
     if (n == 0) return VXA_OK;

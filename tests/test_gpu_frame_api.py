@@ -182,3 +182,37 @@ def test_streaming_readback_matches_synchronous_frames(gpu):
     assert (bufs[5 % 2] == frames[5]).all()
     for b in bufs:
         lib.vxa_host_unregister(ctx, b.ctypes.data)
+
+
+def test_concurrent_render_calls_from_host_threads(gpu):
+    """render_frame from several host threads at once (the reference's renderer
+    has no shared state, so callers may do this): every call serialises on the
+    process-wide context and returns exactly its sequential frame."""
+    import threading
+
+    models = [vx.Model.procedural(6, shell=True), vx.Model.random(7, 4, 0.3)]
+    scenes = [vx.Scene(cfg, models, 3, 160, 96) for cfg in (vx.config.RANDOM, vx.config.HBO, vx.config.C1,
+                                                             vx.config.MANY)]
+    times = [0.0, 0.4, 0.0, 0.0]
+    expected = []
+    for sc, t in zip(scenes, times):
+        sc.evaluate(t)
+        expected.append([sc.render(precision=p)[0] for p in (vx.VXA_FP32, vx.VXA_FP64)])
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(6):
+                for j, p in enumerate((vx.VXA_FP32, vx.VXA_FP64)):
+                    img = scenes[k].render(precision=p)[0]
+                    if not (img == expected[k][j]).all():
+                        errors.append((k, p))
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(scenes))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
