@@ -72,7 +72,8 @@ def dist_env():
 # ---------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons, sampled in the background during the timed region."""
+    """SM clocks + throttle reasons (NVML every 5 ms, nvidia-smi as the fallback), sampled in the
+    background during the timed region."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
