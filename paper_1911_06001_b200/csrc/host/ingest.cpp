@@ -6,9 +6,13 @@
 // the sparse procedural builder (procedural.cpp) evaluates per cube.
 #include "voxanim/ingest.hpp"
 
+#include <algorithm>
 #include <bit>
+#include <charconv>
 #include <cmath>
 #include <string>
+#include <string_view>
+#include <vector>
 
 namespace voxanim {
 
@@ -129,6 +133,94 @@ PrimitiveKind primitive_kind_from_name(const std::string& name) {
     if (name == "menger") return PrimitiveKind::Menger;
     if (name == "checker") return PrimitiveKind::Checker;
     throw ValidationError("unknown shape \"" + name + "\"; expected sphere, box_shell, menger, or checker");
+}
+
+namespace {
+
+// Whitespace-separated fields of one header line.
+std::vector<std::string_view> fields_of(std::string_view line) {
+    std::vector<std::string_view> out;
+    std::size_t i = 0;
+    while (i < line.size()) {
+        while (i < line.size() && (line[i] == ' ' || line[i] == '\t')) ++i;
+        std::size_t j = i;
+        while (j < line.size() && line[j] != ' ' && line[j] != '\t') ++j;
+        if (j > i) out.push_back(line.substr(i, j - i));
+        i = j;
+    }
+    return out;
+}
+
+// leading integer of a field, as `istream >> long long` reads it
+bool integer_field(std::string_view f, long long& v) {
+    if (!f.empty() && f[0] == '+') f.remove_prefix(1);
+    const auto [end, ec] = std::from_chars(f.data(), f.data() + f.size(), v);
+    return ec == std::errc{};
+}
+
+} // namespace
+
+VoxelGrid parse_binvox(std::span<const std::uint8_t> bytes) {
+    const std::string_view text(reinterpret_cast<const char*>(bytes.data()), bytes.size());
+    std::size_t pos = 0;
+    // one header line ('\n'-terminated, a trailing '\r' dropped)
+    const auto line = [&]() {
+        if (pos >= text.size()) throw ParseError("binvox: truncated header");
+        std::size_t eol = text.find('\n', pos);
+        if (eol == std::string_view::npos) eol = text.size();
+        std::string_view l = text.substr(pos, eol - pos);
+        pos = std::min(text.size(), eol + 1);
+        if (!l.empty() && l.back() == '\r') l.remove_suffix(1);
+        return l;
+    };
+    {
+        const auto f = fields_of(line());
+        long long version = -1;
+        if (f.size() < 2 || f[0] != "#binvox" || !integer_field(f[1], version) || version != 1)
+            throw ParseError("binvox: bad header, expected \"#binvox 1\"");
+    }
+    // dim lists depth, height, width: the x, z and y extents
+    std::uint64_t nx = 0, nz = 0, ny = 0;
+    bool dims = false;
+    for (bool data = false; !data;) {
+        const auto f = fields_of(line());
+        if (f.empty()) continue;
+        if (f[0] == "data") {
+            data = true;
+        } else if (f[0] == "dim") {
+            long long d[3] = {-1, -1, -1};
+            for (int k = 0; k < 3; ++k)
+                if (f.size() > static_cast<std::size_t>(k + 1) && !integer_field(f[k + 1], d[k])) d[k] = -1;
+            if (d[0] <= 0 || d[1] <= 0 || d[2] <= 0) throw ParseError("binvox: bad dim line");
+            nx = static_cast<std::uint64_t>(d[0]);
+            nz = static_cast<std::uint64_t>(d[1]);
+            ny = static_cast<std::uint64_t>(d[2]);
+            dims = true;
+        } // translate, scale and unknown keywords carry no voxels
+    }
+    if (!dims) throw ParseError("binvox: missing dim line");
+    const std::uint64_t extent = std::max({nx, ny, nz});
+    if (extent > (std::uint64_t{1} << kDenseDepthCap))
+        throw ParseError("binvox: dimensions too large for the dense-grid cap");
+    VoxelGrid grid(std::bit_ceil(static_cast<std::uint32_t>(extent)));
+
+    const std::uint64_t total = nx * ny * nz, slab = ny * nz;
+    std::uint64_t done = 0;
+    for (; pos < text.size(); pos += 2) {
+        if (pos + 1 >= text.size()) throw ParseError("binvox: truncated RLE stream (dangling value byte)");
+        const std::uint8_t value = bytes[pos], count = bytes[pos + 1];
+        if (value > 1 || count == 0) throw ParseError("binvox: invalid RLE pair");
+        if (done + count > total) throw ParseError("binvox: RLE run count exceeds dim product");
+        if (value)
+            for (std::uint64_t i = done; i < done + count; ++i)
+                grid.set(static_cast<std::uint32_t>(i / slab), static_cast<std::uint32_t>(i % ny),
+                         static_cast<std::uint32_t>((i % slab) / ny));
+        done += count;
+    }
+    if (done != total)
+        throw ParseError("binvox: RLE decodes " + std::to_string(done) + " voxels, dim product is " +
+                         std::to_string(total));
+    return grid;
 }
 
 } // namespace voxanim

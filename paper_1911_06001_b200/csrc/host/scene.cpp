@@ -9,8 +9,15 @@
 #include "voxanim/scene.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <fstream>
 #include <iterator>
+#include <map>
+#include <numbers>
+#include <sstream>
 #include <unordered_map>
+
+#include "json_lite.hpp"
 
 namespace voxanim {
 
@@ -129,6 +136,185 @@ void evaluate_animation(Scene& scene, double time) {
 void mark_clean(Scene& scene) {
     for (SceneObject& o : scene.objects) o.dirty = false;
     scene.camera.dirty = false;
+}
+
+// ---------------------------------------------------------------------------
+// Scene documents (reference scene.cpp:75-306): the same schema, the same
+// check order and error texts, over this library's own JSON reader.
+
+namespace {
+
+using json_lite::Value;
+
+Vec3 vec3_of(const Value& j, const std::string& where) {
+    if (!j.is_array() || j.size() != 3 || !j[0].is_number() || !j[1].is_number() || !j[2].is_number())
+        throw ParseError("scene: " + where + " must be an array of 3 numbers");
+    return {j[0].number(), j[1].number(), j[2].number()};
+}
+
+double number_of(const Value& j, const std::string& where) {
+    if (!j.is_number()) throw ParseError("scene: " + where + " must be a number");
+    return j.number();
+}
+
+// {"quat": [w, x, y, z]} (normalised) or {"axis": [x, y, z], "angle_deg": a}
+Quaternion rotation_of(const Value& j, const std::string& where) {
+    if (j.contains("quat")) {
+        const Value& q = j["quat"];
+        if (!q.is_array() || q.size() != 4) throw ParseError("scene: " + where + ".quat must be an array of 4 numbers");
+        const Quaternion quat{number_of(q[0], where + ".quat[0]"), number_of(q[1], where + ".quat[1]"),
+                              number_of(q[2], where + ".quat[2]"), number_of(q[3], where + ".quat[3]")};
+        if (quat.norm() <= 1e-12) throw ValidationError("scene: bad rotation at " + where + " (near-zero quaternion)");
+        return quat.normalized();
+    }
+    if (j.contains("axis")) {
+        const Vec3 axis = vec3_of(j["axis"], where + ".axis");
+        if (!j.contains("angle_deg") || !j["angle_deg"].is_number())
+            throw ParseError("scene: " + where + " needs a numeric angle_deg");
+        if (axis.norm() <= 1e-12) throw ValidationError("scene: bad rotation at " + where + " (near-zero axis)");
+        return Quaternion::from_axis_angle(axis, j["angle_deg"].number() * std::numbers::pi / 180.0);
+    }
+    throw ParseError("scene: " + where + " must contain either quat or axis/angle_deg");
+}
+
+void require_positive(const Vec3& scale, const std::string& where) {
+    if (!(scale.x > 0.0 && scale.y > 0.0 && scale.z > 0.0))
+        throw ValidationError("scene: " + where + " scale components must be positive");
+}
+
+std::int32_t int32_of(const Value& j) { return static_cast<std::int32_t>(j.integer()); }
+
+void load_models(const Value& doc, const std::filesystem::path& base_dir,
+                 std::map<std::string, std::shared_ptr<const SvoModel>>& models) {
+    if (!doc.contains("models")) return;
+    const Value& m = doc["models"];
+    if (!m.is_object()) throw ParseError("scene: models must map names to paths");
+    for (const auto& [name, value] : m.o) { // key order
+        if (!value.is_string()) throw ParseError("scene: models." + name + " must be a path string");
+        const std::filesystem::path path = base_dir / value.s;
+        if (!std::filesystem::exists(path))
+            throw IoError("scene: model not found: " + path.string() + " (models." + name + ")");
+        auto model = std::make_shared<SvoModel>(load_svo(path));
+        if (const SvoValidationReport rep = validate(*model); !rep.ok())
+            throw ValidationError("scene: model " + name + " fails validation: " + rep.violations.front().message);
+        models.emplace(name, std::move(model));
+    }
+}
+
+void load_objects(const Value& doc, const std::map<std::string, std::shared_ptr<const SvoModel>>& models, Scene& scene) {
+    if (!doc.contains("objects")) return;
+    const Value& list = doc["objects"];
+    if (!list.is_array()) throw ParseError("scene: objects must be an array");
+    for (std::size_t k = 0; k < list.a.size(); ++k) {
+        const Value& j = list.a[k];
+        const std::string where = "objects[" + std::to_string(k) + "]";
+        SceneObject obj;
+        if (!j.contains("id") || !j["id"].is_number_integer()) throw ParseError("scene: " + where + " needs an integer id");
+        obj.id = int32_of(j["id"]);
+        if (scene.find_object(obj.id))
+            throw ValidationError("scene: duplicate object id " + std::to_string(obj.id) + " at " + where);
+        if (!j.contains("model") || !j["model"].is_string()) throw ParseError("scene: " + where + " needs a model name");
+        obj.model_name = j["model"].s;
+        const auto it = models.find(obj.model_name);
+        if (it == models.end())
+            throw ValidationError("scene: " + where + " references unknown model \"" + obj.model_name + "\"");
+        obj.model = it->second;
+        if (j.contains("translation")) obj.transform.translation = vec3_of(j["translation"], where + ".translation");
+        if (j.contains("rotation"))
+            obj.transform.rotation = rotation_from_quaternion(rotation_of(j["rotation"], where + ".rotation"));
+        if (j.contains("scale")) obj.transform.scale = vec3_of(j["scale"], where + ".scale");
+        require_positive(obj.transform.scale, where);
+        obj.dirty = false;
+        scene.objects.push_back(std::move(obj));
+    }
+}
+
+void load_tracks(const Value& doc, Scene& scene) {
+    if (!doc.contains("tracks")) return;
+    const Value& list = doc["tracks"];
+    if (!list.is_array()) throw ParseError("scene: tracks must be an array");
+    for (std::size_t k = 0; k < list.a.size(); ++k) {
+        const Value& j = list.a[k];
+        const std::string where = "tracks[" + std::to_string(k) + "]";
+        AnimationTrack track;
+        if (!j.contains("object") || !j["object"].is_number_integer())
+            throw ParseError("scene: " + where + " needs an integer object id");
+        track.object_id = int32_of(j["object"]);
+        if (!scene.find_object(track.object_id))
+            throw ValidationError("scene: " + where + " references unknown object id " + std::to_string(track.object_id));
+        if (!j.contains("keys") || !j["keys"].is_array() || j["keys"].a.empty())
+            throw ParseError("scene: " + where + " needs a nonempty keys array");
+        const Value& keys = j["keys"];
+        for (std::size_t q = 0; q < keys.a.size(); ++q) {
+            const Value& kj = keys.a[q];
+            const std::string kw = where + ".keys[" + std::to_string(q) + "]";
+            Keyframe key;
+            if (!kj.contains("time") || !kj["time"].is_number()) throw ParseError("scene: " + kw + " needs a numeric time");
+            key.time = kj["time"].number();
+            if (kj.contains("translation")) key.translation = vec3_of(kj["translation"], kw + ".translation");
+            if (kj.contains("rotation")) key.rotation = rotation_of(kj["rotation"], kw + ".rotation");
+            if (kj.contains("scale")) key.scale = vec3_of(kj["scale"], kw + ".scale");
+            require_positive(key.scale, kw);
+            if (!track.keys.empty() && key.time <= track.keys.back().time)
+                throw ValidationError("scene: " + kw + " keyframe times must be strictly increasing");
+            track.keys.push_back(key);
+        }
+        scene.tracks.push_back(std::move(track));
+    }
+}
+
+} // namespace
+
+Scene load_scene(const std::string& text, const std::filesystem::path& base_dir) {
+    Value doc;
+    try {
+        doc = json_lite::parse(text);
+    } catch (const json_lite::Error& e) {
+        throw ParseError(std::string("scene: invalid JSON: ") + e.what());
+    }
+    if (!doc.is_object()) throw ParseError("scene: top level must be an object");
+
+    Scene scene;
+    std::map<std::string, std::shared_ptr<const SvoModel>> models;
+    load_models(doc, base_dir, models);
+    load_objects(doc, models, scene);
+    load_tracks(doc, scene);
+
+    // camera: defaults at the origin looking down -z, fov 60, 640x480
+    Vec3 position{0, 0, 0}, look_at{0, 0, -1}, up{0, 1, 0};
+    double fov = 60.0;
+    if (doc.contains("camera")) {
+        const Value& c = doc["camera"];
+        if (!c.is_object()) throw ParseError("scene: camera must be an object");
+        if (c.contains("position")) position = vec3_of(c["position"], "camera.position");
+        if (c.contains("look_at")) look_at = vec3_of(c["look_at"], "camera.look_at");
+        if (c.contains("up")) up = vec3_of(c["up"], "camera.up");
+        if (c.contains("fov_deg")) {
+            if (!c["fov_deg"].is_number()) throw ParseError("scene: camera.fov_deg must be a number");
+            fov = c["fov_deg"].number();
+        }
+    }
+    scene.camera = make_look_at_camera(position, look_at, up, fov, 640, 480);
+
+    if (doc.contains("background")) {
+        const Value& b = doc["background"];
+        if (!b.is_array() || b.size() != 3)
+            throw ParseError("scene: background must be an array of 3 numbers (0..255)");
+        for (std::size_t k = 0; k < 3; ++k) {
+            const double v = number_of(b[k], "background[" + std::to_string(k) + "]");
+            if (v < 0.0 || v > 255.0) throw ValidationError("scene: background channels must be in [0, 255]");
+            scene.background[k] = static_cast<std::uint8_t>(std::lround(v));
+        }
+    }
+    return scene;
+}
+
+Scene load_scene_file(const std::filesystem::path& path) {
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open scene: " + path.string());
+    std::ostringstream text;
+    text << in.rdbuf();
+    return load_scene(text.str(), path.has_parent_path() ? path.parent_path() : std::filesystem::path("."));
 }
 
 } // namespace voxanim

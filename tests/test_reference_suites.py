@@ -5,7 +5,8 @@ tests/cpp/Makefile with a doctest-compatible runner (tests/cpp/doctest.h):
   the reference's own 97 test cases, incl. the DDA equivalence, KATs, HBO
   transparency and thread determinism);
 * our_*  -- the same sources against this repo's drop-in libvoxanim.so:
-  test_math / test_svo run on the CPU; test_traversal / test_renderer drive
+  test_math / test_svo / test_ingest / test_scene run on the CPU (model build,
+  binvox, scene documents, animation); test_traversal / test_renderer drive
   traverse / trace_ray / render_frame through the CUDA kernels (GPU only).
 """
 import os
@@ -32,7 +33,7 @@ def test_reference_suite_passes_against_the_oracle_build(suite):
     run_suite("ref_" + suite)
 
 
-@pytest.mark.parametrize("suite", ["test_math", "test_svo"])
+@pytest.mark.parametrize("suite", ["test_math", "test_svo", "test_ingest", "test_scene"])
 def test_reference_suite_passes_against_our_library_cpu(suite):
     run_suite("our_" + suite)
 
