@@ -467,8 +467,8 @@ def run_ours(args):
     value = rays * args.steps / (total_ms / 1e3) / 1e6
 
     # roofline of the frame kernel: algorithmic bytes / kernel time
-    kernel_ms = st.gpu_ms / max(1, st.kernel_launches)
-    frames = max(1, st.kernel_launches)
+    frames = max(1, st.frames)
+    kernel_ms = st.gpu_ms / frames  # per frame: the culling pre-pass (if any) + the frame kernel
     pixels_mine = st.rays / frames
     alg_bytes = (8.0 * st.node_fetches + 4.0 * st.leaf_hits) / frames + 4.0 * pixels_mine
     peak, peak_src = measured_peaks()

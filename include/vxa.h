@@ -167,6 +167,7 @@ typedef struct vxa_stats {
     double gpu_ms;           /* CUDA-event time of the frame kernels on the context stream */
     uint64_t h2d_bytes;      /* host->device bytes the call(s) copied (instance table, hit buffer) */
     uint64_t d2h_bytes;      /* device->host bytes (image, AOVs, hit buffer, counters) */
+    uint64_t frames;         /* frames submitted (gpu_ms covers them; kernel_launches also counts pre-passes) */
 } vxa_stats;
 
 /* Per-pixel parity outputs (host array of width*height, row-major). */

@@ -80,6 +80,7 @@ class vxa_stats(C.Structure):
         ("gpu_ms", C.c_double),
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
+        ("frames", C.c_uint64),
     ]
 
 

@@ -520,6 +520,7 @@ int read_counters(vxa_ctx* ctx, vxa_stats* s) {
     }
     s->gpu_ms = total;
     s->kernel_launches = static_cast<uint64_t>(ctx->k_count + ctx->aux_launches);
+    s->frames = static_cast<uint64_t>(ctx->k_count);
     s->h2d_bytes = ctx->h2d;
     s->d2h_bytes = ctx->d2h + sizeof(c);
     return VXA_OK;

@@ -39,7 +39,10 @@ constexpr int kTileW = 8, kTileH = 4;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
 // Scenes with more instances than this get the per-super-tile culling pre-pass.
-constexpr uint32_t kSuperCullMin = 128;
+#ifndef VXA_SUPER_MIN
+#define VXA_SUPER_MIN 32
+#endif
+constexpr uint32_t kSuperCullMin = VXA_SUPER_MIN;
 constexpr uint32_t kSuperCap = 1024; // super-tile list capacity (overflow: scan all)
 
 // Screen partition: 64x64 super-tile s = (y / 64) * n_super_x + x / 64 belongs

@@ -73,7 +73,7 @@ def test_struct_layouts():
     assert C.sizeof(_abi.vxa_hit_record) == 48
     assert C.sizeof(_abi.vxa_pixel_aov) == 48
     assert C.sizeof(_abi.vxa_traverse_hit) == 96
-    assert C.sizeof(_abi.vxa_stats) == 80
+    assert C.sizeof(_abi.vxa_stats) == 88
     assert vx.vxa().vxa_abi_version() == 1
 
 
