@@ -577,7 +577,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
 // instance order) to its list; the frame kernel's 8x4 tiles then test only
 // their super-tile's list (tiles x instances / 32 rounds -> super-tiles x
 // instances / 32 + tiles x list / 32).
-static __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__ FrameParams<float> p,
+template <typename Real>
+__global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__ FrameParams<Real> p,
                                                         uint16_t* __restrict__ list, uint32_t* __restrict__ count) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t st = blockIdx.x * 4u + (threadIdx.x >> 5);

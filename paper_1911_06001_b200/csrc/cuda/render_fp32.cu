@@ -22,7 +22,7 @@ cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, co
 cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, cudaStream_t s) {
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (n_mine == 0) return cudaSuccess;
-    super_cull_kernel<<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
+    super_cull_kernel<float><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
     return cudaGetLastError();
 }
 

@@ -14,6 +14,13 @@ void* pick(bool aov, bool hbo, bool /*compact: FP64 keeps the general words*/) {
 }
 } // namespace
 
+cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint32_t* count, cudaStream_t s) {
+    const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
+    if (n_mine == 0) return cudaSuccess;
+    super_cull_kernel<double><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l) {
     void* args[] = {const_cast<FrameParams<double>*>(&p)};
     return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f64(p.max_depth), l.stream);

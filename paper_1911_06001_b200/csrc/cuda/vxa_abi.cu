@@ -472,21 +472,22 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     }
     VXA_CUDA(cudaEventRecord(ctx->k_begin[slot_k], ctx->stream));
     cudaError_t e = cudaSuccess;
-    if constexpr (sizeof(Real) == 8) {
-        e = launch_frame_f64(p, a, h, l);
-    } else {
-        // large scenes: per-super-tile candidate lists first (same stream)
-        if (p.culling && n > kSuperCullMin && n <= 0xffffu) {
-            const size_t mine_super = p.n_tiles / kTilesPerSuper;
-            VXA_CUDA(ctx->super_list.ensure(std::max<size_t>(mine_super * kSuperCap, 1)));
-            VXA_CUDA(ctx->super_count.ensure(std::max<size_t>(mine_super, 1)));
-            p.super_list = ctx->super_list.ptr;
-            p.super_count = ctx->super_count.ptr;
-            p.super_cap = kSuperCap;
-            e = launch_super_cull(p, ctx->super_list.ptr, ctx->super_count.ptr, ctx->stream);
-            ++ctx->aux_launches;
-        }
-        if (e == cudaSuccess) e = launch_frame_f32(p, a, h, l);
+    // larger scenes: per-super-tile candidate lists first (same stream; both kernels)
+    if (p.culling && n > kSuperCullMin && n <= 0xffffu) {
+        const size_t mine_super = p.n_tiles / kTilesPerSuper;
+        VXA_CUDA(ctx->super_list.ensure(std::max<size_t>(mine_super * kSuperCap, 1)));
+        VXA_CUDA(ctx->super_count.ensure(std::max<size_t>(mine_super, 1)));
+        p.super_list = ctx->super_list.ptr;
+        p.super_count = ctx->super_count.ptr;
+        p.super_cap = kSuperCap;
+        e = launch_super_cull(p, ctx->super_list.ptr, ctx->super_count.ptr, ctx->stream);
+        ++ctx->aux_launches;
+    }
+    if (e == cudaSuccess) {
+        if constexpr (sizeof(Real) == 8)
+            e = launch_frame_f64(p, a, h, l);
+        else
+            e = launch_frame_f32(p, a, h, l);
     }
     if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
     VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
