@@ -427,10 +427,11 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         bool single_trace = false;
         HitRec prev;
         if constexpr (kHbo) {
-            prev = reinterpret_cast<const HitRec*>(p.hbo)[pix];
             if (!p.camera_dirty && n_hits == 1) {
                 const DevInstance<Real>& o = p.inst[only];
-                if (prev.kind == kSingle && prev.object_id == o.id && !o.dirty) {
+                // a dirty object is never reused: its record is not even read
+                if (!o.dirty) prev = reinterpret_cast<const HitRec*>(p.hbo)[pix];
+                if (!o.dirty && prev.kind == kSingle && prev.object_id == o.id) {
                     reused = true;
                 } else {
                     single_trace = true; // "trace just this SVO"
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
                                      static_cast<Real>(rec.normal[2])};
                 rgba = shade_rgba(rec.color, nrm, dw);
             }
-            reinterpret_cast<HitRec*>(p.hbo)[pix] = rec;
+            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec*>(p.hbo)[pix] = rec; // a reused record is unchanged
         } else {
             if (best.have) {
                 const uint32_t color = __ldg(p.inst[best.inst].model.attrs + best.attr);
