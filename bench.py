@@ -586,9 +586,11 @@ def run_ours(args):
         m10 = vx.Model.procedural(10, shell=True)
         # "opt" = culling + sorting + the device-resident hit buffer (paper Fig. 6 "w/opt")
         runs = (("c2_animated_1080p", 2, True, False), ("c3_static_1080p", 3, False, False),
-                ("c2_animated_opt_1080p", 2, True, True), ("c3_static_opt_1080p", 3, False, True))
+                ("c2_animated_opt_1080p", 2, True, True), ("c3_static_opt_1080p", 3, False, True),
+                ("c4_1080p", 4, True, False))
         for name, cfg, anim, opt in runs:
-            sc = vx.Scene(cfg, [m10])
+            # C4 at 1080p: the 4K workload's 64 animated depth-11 instances, quarter the rays
+            sc = vx.Scene(cfg, [model], 0, 1920, 1080) if cfg == 4 else vx.Scene(cfg, [m10])
             hbo = C.c_uint32(0)
             if opt:
                 check(lib.vxa_hbo_create(ctx, 1920, 1080, C.byref(hbo)), "hbo_create")
