@@ -543,6 +543,12 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1
         }
         if (best.have) ++n_leaf;
         p.fb[pix] = rgba;
+        if (p.rgb != nullptr) { // streamed frame: the readback's RGB8 bytes too (no pack pass)
+            uint8_t* o = p.rgb + 3 * pix;
+            o[0] = static_cast<uint8_t>(rgba);
+            o[1] = static_cast<uint8_t>(rgba >> 8);
+            o[2] = static_cast<uint8_t>(rgba >> 16);
+        }
 
         if constexpr (kAov) {
             PixelAov a;

@@ -200,6 +200,15 @@ struct vxa_ctx {
     DevBuf<uint8_t> rb_rgb[2];
     cudaEvent_t rb_packed[2] = {nullptr, nullptr}, rb_done[2] = {nullptr, nullptr};
     uint64_t rb_next = 0; // next ticket
+    // The newest frame's D2H is enqueued at the next submission, after that
+    // frame's instance upload, so the small H2D never queues behind a 25 MB D2H
+    // on a shared copy engine (the next kernel would wait for it).
+    bool rb_pending = false;
+    uint8_t* next_rgb = nullptr;          // RGB8 target of the frame being submitted (streaming)
+    cudaEvent_t next_rgb_free = nullptr;  // its slot's previous D2H
+    int rb_pending_slot = 0;
+    uint8_t* rb_pending_out = nullptr;
+    size_t rb_pending_bytes = 0;
     int occ[2][2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][compact][stack height]
 
     // Frame-kernel timing ring: events recorded tight around every frame
@@ -420,6 +429,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     ctx->n_rays += my_pixels;
     if (p.sphere_pass) ctx->n_sphere_tests += my_pixels * n;
     p.fb = target;
+    p.rgb = ctx->next_rgb; // set by vxa_submit_readback for this frame only
+    if (p.rgb != nullptr) VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->next_rgb_free, 0));
     p.max_depth = 1;
     p.compact = sizeof(Real) == 4 ? 1u : 0u;
     for (uint32_t k = 0; k < n; ++k)
@@ -581,9 +592,14 @@ int vxa_create(int device, vxa_ctx** out) {
     return VXA_OK;
 }
 
+namespace {
+int flush_readback(vxa_ctx* ctx);
+}
+
 int vxa_destroy(vxa_ctx* ctx) {
     if (ctx == nullptr) return VXA_OK;
     cudaSetDevice(ctx->device);
+    flush_readback(ctx); // a streamed frame still pending lands before teardown
     cudaStreamSynchronize(ctx->stream);
     for (auto& [h, m] : ctx->models) m.free_all();
     ctx->build.grid.release();
@@ -1053,23 +1069,50 @@ int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     return enqueue_any(ctx, f, in, n, nullptr, hbo, false);
 }
 
+namespace {
+// Enqueues the deferred D2H of the newest streamed frame (caller holds ctx->mu).
+int flush_readback(vxa_ctx* ctx) {
+    if (!ctx->rb_pending) return VXA_OK;
+    const int slot = ctx->rb_pending_slot;
+    ctx->rb_pending = false;
+    VXA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->rb_packed[slot], 0));
+    VXA_CUDA(cudaMemcpyAsync(ctx->rb_pending_out, ctx->rb_rgb[slot].ptr, ctx->rb_pending_bytes, cudaMemcpyDeviceToHost,
+                             ctx->copy_stream));
+    VXA_CUDA(cudaEventRecord(ctx->rb_done[slot], ctx->copy_stream));
+    return VXA_OK;
+}
+} // namespace
+
 int vxa_submit_readback(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n,
                         uint8_t* rgb_out, uint64_t* ticket) {
     if (ctx == nullptr || rgb_out == nullptr || ticket == nullptr) return fail(VXA_ERR_INVALID, "null argument");
     std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
-    if (int rc = vxa_submit(ctx, f, in, n); rc != VXA_OK) return rc;
+    if (int rc = check_frame(f); rc != VXA_OK) return rc;
     const size_t npix = static_cast<size_t>(f->camera.width) * f->camera.height;
     const int slot = static_cast<int>(ctx->rb_next & 1u);
     VXA_CUDA(ctx->rb_rgb[slot].ensure(npix * 3 + 16));
-    // the slot's previous D2H must be done before the pack overwrites it
-    VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->rb_done[slot], 0));
-    const size_t quads = (npix + 3) / 4;
-    pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rb_rgb[slot].ptr, npix);
-    VXA_CUDA(cudaGetLastError());
+    // The frame kernel writes the RGB8 bytes into the slot itself (no pack
+    // pass), after the slot's previous D2H (two frames back) is done.
+    ctx->next_rgb = f->tile_world == 1 ? ctx->rb_rgb[slot].ptr : nullptr;
+    ctx->next_rgb_free = ctx->rb_done[slot];
+    const int rc = vxa_submit(ctx, f, in, n);
+    const bool fused = ctx->next_rgb != nullptr;
+    ctx->next_rgb = nullptr;
+    if (rc != VXA_OK) return rc;
+    if (!fused) { // a partitioned frame: pack the composed framebuffer
+        VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->rb_done[slot], 0));
+        const size_t quads = (npix + 3) / 4;
+        pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rb_rgb[slot].ptr,
+                                                                                      npix);
+        VXA_CUDA(cudaGetLastError());
+    }
     VXA_CUDA(cudaEventRecord(ctx->rb_packed[slot], ctx->stream));
-    VXA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->rb_packed[slot], 0));
-    VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rb_rgb[slot].ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->copy_stream));
-    VXA_CUDA(cudaEventRecord(ctx->rb_done[slot], ctx->copy_stream));
+    // the previous frame's D2H goes to the copy engine now, behind this frame's upload
+    if (int rc = flush_readback(ctx); rc != VXA_OK) return rc;
+    ctx->rb_pending = true;
+    ctx->rb_pending_slot = slot;
+    ctx->rb_pending_out = rgb_out;
+    ctx->rb_pending_bytes = npix * 3;
     ctx->d2h += npix * 3;
     *ticket = ctx->rb_next++;
     return VXA_OK;
@@ -1079,7 +1122,10 @@ int vxa_wait_readback(vxa_ctx* ctx, uint64_t ticket) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     if (ticket >= ctx->rb_next) return fail(VXA_ERR_INVALID, "unknown readback ticket");
-    if (ticket + 2 < ctx->rb_next) return VXA_OK; // its slot has been reused: already complete
+    if (ticket + 1 == ctx->rb_next)
+        if (int rc = flush_readback(ctx); rc != VXA_OK) return rc;
+    // the slot's event marks this ticket's D2H or a later one on the same FIFO
+    // copy stream, so waiting for it covers this ticket
     VXA_CUDA(cudaEventSynchronize(ctx->rb_done[ticket & 1u]));
     return VXA_OK;
 }
@@ -1087,7 +1133,9 @@ int vxa_wait_readback(vxa_ctx* ctx, uint64_t ticket) {
 int vxa_synchronize(vxa_ctx* ctx) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (int rc = flush_readback(ctx); rc != VXA_OK) return rc; // streamed images land too
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->copy_stream) VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     return VXA_OK;
 }
 

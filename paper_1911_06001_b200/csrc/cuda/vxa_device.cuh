@@ -185,6 +185,7 @@ template <typename Real> struct FrameParams {
     uint32_t compact;   // every model has compact 4-byte words (FP32 kernel)
     // outputs
     uint32_t* fb;                 // RGBA8 framebuffer (local or peer-mapped)
+    uint8_t* rgb;                 // streamed frames: RGB8 copy for the readback (or null)
     uint32_t* tile_counter;       // persistent-thread work counter
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
     void* aov;                    // vxa_pixel_aov* or null
