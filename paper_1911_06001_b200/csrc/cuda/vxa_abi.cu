@@ -430,7 +430,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     if (p.sphere_pass) ctx->n_sphere_tests += my_pixels * n;
     p.fb = target;
     p.rgb = ctx->next_rgb; // set by vxa_submit_readback for this frame only
-    if (p.rgb != nullptr) VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->next_rgb_free, 0));
+    if (p.rgb != nullptr && ctx->next_rgb_free != nullptr) VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->next_rgb_free, 0));
     p.max_depth = 1;
     p.compact = sizeof(Real) == 4 ? 1u : 0u;
     for (uint32_t k = 0; k < n; ++k)
@@ -977,10 +977,23 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     ctx->h2d = ctx->d2h = 0;
     ctx->n_rays = ctx->n_sphere_tests = 0;
     VXA_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
-    if (int rc = enqueue_any(ctx, f, in, n, aov, hbo, true); rc != VXA_OK) return rc;
+    // the frame kernel writes the RGB8 image itself for an unpartitioned frame
+    // (this call is synchronous, so the buffer is free: no wait event)
+    const bool fused = rgb_out != nullptr && f->tile_world == 1;
+    if (fused) {
+        VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
+        ctx->next_rgb = ctx->rgb.ptr;
+        ctx->next_rgb_free = nullptr;
+    }
+    const int erc = enqueue_any(ctx, f, in, n, aov, hbo, true);
+    ctx->next_rgb = nullptr;
+    if (erc != VXA_OK) return erc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
     uint64_t launches = 1 + static_cast<uint64_t>(ctx->aux_launches);
-    if (rgb_out) {
+    if (rgb_out && fused) {
+        VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->d2h += npix * 3;
+    } else if (rgb_out) {
         VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
         const size_t quads = (npix + 3) / 4;
         pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rgb.ptr, npix);

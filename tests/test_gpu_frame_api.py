@@ -93,7 +93,7 @@ def test_stats_and_launch_counts(gpu):
     _, rst = o.render()
     for k in ("rays", "sphere_tests", "svo_traversals", "pixels_reused"):
         assert st[k] == rst[k], k
-    assert st["kernel_launches"] == 2  # frame kernel + RGB8 pack
+    assert st["kernel_launches"] == 1  # the frame kernel (it writes the RGB8 image itself)
     assert st["gpu_ms"] > 0
 
 
