@@ -75,6 +75,9 @@ int vxn_scene_stream(vxn_scene* s, double time, int precision, uint8_t* rgb_out,
 
 vxn_hbo* vxn_hbo_create(int width, int height);
 void vxn_hbo_free(vxn_hbo* h);
+/* HitBuffer records through its host accessors (width*height 48-byte records) */
+int vxn_hbo_records(vxn_hbo* h, vxa_hit_record* out);
+int vxn_hbo_set_record(vxn_hbo* h, int x, int y, const vxa_hit_record* rec);
 
 /* voxanim::render_frame (precision < 0: library default) / render_frame_ex.
  * rgb: width*height*3 or NULL (frame stays on the device); aov: width*height

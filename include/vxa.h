@@ -196,8 +196,9 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* frame, const vxa_instance* in
  * to Miss records (a fresh voxanim::HitBuffer). */
 int vxa_hbo_create(vxa_ctx* ctx, int32_t width, int32_t height, uint32_t* handle_out);
 int vxa_hbo_release(vxa_ctx* ctx, uint32_t handle);
-/* Copies a device hit buffer to host records (width*height). */
+/* Copies a device hit buffer to host records (width*height), and back. */
 int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out);
+int vxa_hbo_upload(vxa_ctx* ctx, uint32_t handle, const vxa_hit_record* in);
 
 /* Asynchronous form for benchmarking: enqueues the frame on the context
  * stream (framebuffer stays in HBM), no host outputs; a device hit buffer

@@ -70,6 +70,8 @@ def lib() -> C.CDLL:
             "vref_scene_free": (None, P),
             "vref_hbo_create": (P, i, i),
             "vref_hbo_free": (None, P),
+            "vref_hbo_records": (i, P, P),
+            "vref_hbo_set_record": (i, P, i, i, P),
             "vref_render": (i, P, i, i, i, P, P, C.POINTER(u64), C.POINTER(d)),
             "vref_dump": (i, P, i, i, i, i, i, P, P),
             "vref_render_rows": (i, P, i, i, i, P, C.POINTER(d)),
@@ -142,6 +144,21 @@ class RefModel:
 class RefHitBuffer:
     def __init__(self, w, h):
         self._h = C.c_void_p(lib().vref_hbo_create(w, h))
+        self.width, self.height = w, h
+
+    def records(self):
+        """The reference HitBuffer's records (HBO_DTYPE, height x width)."""
+        import numpy as np
+        from paper_1911_06001_b200._abi import HBO_DTYPE
+        out = np.zeros((self.height, self.width), HBO_DTYPE)
+        lib().vref_hbo_records(self._h, out.ctypes.data)
+        return out
+
+    def set_record(self, x, y, rec):
+        import numpy as np
+        from paper_1911_06001_b200._abi import HBO_DTYPE
+        r = np.array(rec, HBO_DTYPE)
+        lib().vref_hbo_set_record(self._h, x, y, r.ctypes.data)
 
     def __del__(self):
         if getattr(self, "_h", None) and _LIB is not None:

@@ -532,6 +532,19 @@ VREF_API vref_hbo* vref_hbo_create(int w, int h) {
 
 VREF_API void vref_hbo_free(vref_hbo* h) { delete h; }
 
+// The reference HitBuffer's records, read and written through at() (48-byte HitRecord layout).
+VREF_API int vref_hbo_records(const vref_hbo* h, uint8_t* out) {
+    const int w = h->b.width(), hh = h->b.height();
+    for (int y = 0; y < hh; ++y)
+        for (int x = 0; x < w; ++x)
+            std::memcpy(out + 48 * (static_cast<size_t>(y) * w + x), &h->b.at(x, y), 48);
+    return 0;
+}
+VREF_API int vref_hbo_set_record(vref_hbo* h, int x, int y, const uint8_t* rec) {
+    std::memcpy(&h->b.at(x, y), rec, 48);
+    return 0;
+}
+
 // The reference frame: render_frame with its own timing (FrameStats::render_ms).
 VREF_API int vref_render(vref_scene* s, int culling, int sorting, int threads, vref_hbo* hbo, uint8_t* rgb, uint64_t* fs4,
                 double* render_ms) {

@@ -11,7 +11,7 @@ from __future__ import annotations
 import ctypes as C
 
 from . import _abi
-from ._abi import (AOV_DTYPE, RAY_DTYPE, TRAV_DTYPE, VXA_FP32, VXA_FP64, vxa_frame_desc, vxa_instance,
+from ._abi import (AOV_DTYPE, HBO_DTYPE, RAY_DTYPE, TRAV_DTYPE, VXA_FP32, VXA_FP64, vxa_frame_desc, vxa_instance,
                    vxa_stats)
 
 __all__ = ["Model", "Scene", "HitBuffer", "traverse", "vxa", "voxanim", "VoxanimError", "VXA_FP32", "VXA_FP64",
@@ -152,6 +152,20 @@ class HitBuffer:
         if not h:
             raise VoxanimError(_err())
         self._h = C.c_void_p(h)
+        self.width, self.height = width, height
+
+    def records(self):
+        """The records as the host sees them (HitBuffer::data): numpy HBO_DTYPE, height x width."""
+        import numpy as np
+        out = np.zeros((self.height, self.width), HBO_DTYPE)
+        _check(voxanim().vxn_hbo_records(self._h, out.ctypes.data), "hbo_records")
+        return out
+
+    def set_record(self, x: int, y: int, rec) -> None:
+        """HitBuffer::at(x, y) = rec (a HBO_DTYPE scalar)."""
+        import numpy as np
+        r = np.array(rec, HBO_DTYPE)
+        _check(voxanim().vxn_hbo_set_record(self._h, x, y, r.ctypes.data), "hbo_set_record")
 
     def __del__(self):
         if getattr(self, "_h", None) and _VX is not None:

@@ -155,7 +155,13 @@ try:
          ("log_total", "<u4")],
         align=True,
     )
+    # voxanim::HitRecord / vxa_hit_record (48 bytes)
+    HBO_DTYPE = np.dtype(
+        [("color", "u1", (4,)), ("pad0", "u1", (4,)), ("normal", "<f8", (3,)), ("t", "<f8"), ("object_id", "<i4"),
+         ("kind", "u1"), ("pad1", "u1", (3,))]
+    )
     assert AOV_DTYPE.itemsize == 48 and RAY_DTYPE.itemsize == 72 and TRAV_DTYPE.itemsize == 96
+    assert HBO_DTYPE.itemsize == 48
 except ImportError:  # pragma: no cover
     np = None
 
@@ -164,7 +170,7 @@ VXA_SYMBOLS = [
     "vxa_create", "vxa_destroy", "vxa_last_error", "vxa_abi_version", "vxa_device_info",
     "vxa_upload_model", "vxa_release_model", "vxa_model_info", "vxa_build_model", "vxa_model_download", "vxa_upload_svo",
     "vxa_model_counts",
-    "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_render", "vxa_submit", "vxa_submit_readback",
+    "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_hbo_upload", "vxa_render", "vxa_submit", "vxa_submit_readback",
     "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
     "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_traverse",
@@ -175,7 +181,7 @@ VXN_SYMBOLS = [
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
     "vxn_scene_set_camera",
     "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit", "vxn_scene_stream",
-    "vxn_hbo_create", "vxn_hbo_free", "vxn_render", "vxn_traverse", "vxn_context",
+    "vxn_hbo_create", "vxn_hbo_free", "vxn_hbo_records", "vxn_hbo_set_record", "vxn_render", "vxn_traverse", "vxn_context",
 ]
 
 P = C.c_void_p
@@ -214,6 +220,7 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_hbo_create", i, P, C.c_int32, C.c_int32, C.POINTER(u32))
     _declare(lib, "vxa_hbo_release", i, P, u32)
     _declare(lib, "vxa_hbo_download", i, P, u32, P)
+    _declare(lib, "vxa_hbo_upload", i, P, u32, P)
     _declare(lib, "vxa_synchronize", i, P)
     _declare(lib, "vxa_stats_read", i, P, C.POINTER(vxa_stats))
     _declare(lib, "vxa_stats_reset", i, P)
@@ -265,6 +272,8 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_scene_stream", i, P, d, i, P, C.POINTER(u64))
     _declare(lib, "vxn_hbo_create", P, i, i)
     _declare(lib, "vxn_hbo_free", None, P)
+    _declare(lib, "vxn_hbo_records", i, P, P)
+    _declare(lib, "vxn_hbo_set_record", i, P, i, i, P)
     _declare(lib, "vxn_render", i, P, i, i, i, P, P, P, C.POINTER(u64), C.POINTER(d), C.POINTER(vxa_stats))
     _declare(lib, "vxn_traverse", i, P, P, u32, P)
     _declare(lib, "vxn_context", P)

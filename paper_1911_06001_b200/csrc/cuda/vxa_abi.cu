@@ -1064,6 +1064,19 @@ int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out) {
     return VXA_OK;
 }
 
+int vxa_hbo_upload(vxa_ctx* ctx, uint32_t handle, const vxa_hit_record* in) {
+    if (ctx == nullptr || in == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    const auto it = ctx->hbos.find(handle);
+    if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = static_cast<size_t>(it->second.w) * it->second.h;
+    VXA_CUDA(cudaMemcpyAsync(it->second.rec, in, n * sizeof(HitRec), cudaMemcpyHostToDevice, ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->h2d += n * sizeof(HitRec);
+    return VXA_OK;
+}
+
 int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     std::lock_guard<std::recursive_mutex> lock_(ctx->mu);

@@ -351,6 +351,27 @@ int vxn_render(vxn_scene* s, int culling, int sorting, int precision, vxn_hbo* h
         -1);
 }
 
+int vxn_hbo_records(vxn_hbo* h, vxa_hit_record* out) {
+    return guard(
+        [&] {
+            const voxanim::HitBuffer& b = h->b;
+            std::memcpy(out, b.data(), sizeof(voxanim::HitRecord) * static_cast<std::size_t>(b.width()) * b.height());
+            return 0;
+        },
+        -1);
+}
+
+int vxn_hbo_set_record(vxn_hbo* h, int x, int y, const vxa_hit_record* rec) {
+    return guard(
+        [&] {
+            if (x < 0 || y < 0 || x >= h->b.width() || y >= h->b.height())
+                throw voxanim::ValidationError("hit buffer index out of range");
+            std::memcpy(static_cast<void*>(&h->b.at(x, y)), rec, sizeof(voxanim::HitRecord));
+            return 0;
+        },
+        -1);
+}
+
 int vxn_traverse(const vxn_model* m, const vxa_local_ray* rays, uint32_t n, vxa_traverse_hit* hits) {
     return guard(
         [&] {

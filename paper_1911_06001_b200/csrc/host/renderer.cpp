@@ -95,6 +95,83 @@ std::array<std::uint8_t, 3> shade(const HitRecord& rec, const Ray& ray, const st
     return {q(rec.color.r), q(rec.color.g), q(rec.color.b)};
 }
 
+// ---- HitBuffer: GPU-resident, host copy synced on access
+HitBuffer::HitBuffer(int width, int height)
+    : w_(width), h_(height), rec_(static_cast<std::size_t>(width) * static_cast<std::size_t>(height)),
+      mu_(std::make_unique<std::mutex>()) {}
+
+HitBuffer::HitBuffer(const HitBuffer& other)
+    : w_(other.w_), h_(other.h_), rec_((other.sync_host(), other.rec_)), host_newer_(true),
+      mu_(std::make_unique<std::mutex>()) {}
+
+HitBuffer::HitBuffer(HitBuffer&& other) noexcept
+    : w_(other.w_), h_(other.h_), rec_(std::move(other.rec_)), dev_(other.dev_),
+      gpu_newer_(other.gpu_newer_.load()), host_newer_(other.host_newer_), mu_(std::make_unique<std::mutex>()) {
+    other.dev_ = 0;
+    other.gpu_newer_ = false;
+}
+
+HitBuffer& HitBuffer::operator=(const HitBuffer& other) {
+    if (this != &other) {
+        other.sync_host();
+        release_device();
+        w_ = other.w_;
+        h_ = other.h_;
+        rec_ = other.rec_;
+        gpu_newer_ = false;
+        host_newer_ = true;
+    }
+    return *this;
+}
+
+HitBuffer& HitBuffer::operator=(HitBuffer&& other) noexcept {
+    if (this != &other) {
+        release_device();
+        w_ = other.w_;
+        h_ = other.h_;
+        rec_ = std::move(other.rec_);
+        dev_ = other.dev_;
+        gpu_newer_ = other.gpu_newer_.load();
+        host_newer_ = other.host_newer_;
+        other.dev_ = 0;
+        other.gpu_newer_ = false;
+    }
+    return *this;
+}
+
+HitBuffer::~HitBuffer() { release_device(); }
+
+void HitBuffer::release_device() noexcept {
+    if (dev_ != 0) {
+        try {
+            vxa_hbo_release(gpu::context(), dev_);
+        } catch (...) {
+        }
+        dev_ = 0;
+    }
+}
+
+void HitBuffer::pull() const {
+    std::lock_guard<std::mutex> lk(*mu_);
+    if (!gpu_newer_.load(std::memory_order_relaxed)) return;
+    gpu::check(vxa_hbo_download(gpu::context(), dev_, reinterpret_cast<vxa_hit_record*>(rec_.data())),
+               "vxa_hbo_download");
+    gpu_newer_.store(false, std::memory_order_release);
+}
+
+std::uint32_t HitBuffer::device_for_frame() {
+    vxa_ctx* ctx = gpu::context();
+    if (dev_ == 0) {
+        gpu::check(vxa_hbo_create(ctx, w_, h_, &dev_), "vxa_hbo_create"); // Miss records, like a fresh buffer
+    }
+    if (host_newer_) {
+        sync_host();
+        gpu::check(vxa_hbo_upload(ctx, dev_, reinterpret_cast<const vxa_hit_record*>(rec_.data())), "vxa_hbo_upload");
+        host_newer_ = false;
+    }
+    return dev_;
+}
+
 namespace gpu {
 
 void render_frame_into(const Scene& scene, const RenderOptions& opts, const RenderOptionsEx& ex, FrameStats& stats,
@@ -139,13 +216,15 @@ void render_frame_into(const Scene& scene, const RenderOptions& opts, const Rend
     f.camera_dirty = cam.dirty ? 1 : 0;
     f.tile_rank = ex.tile_rank;
     f.tile_world = ex.tile_world;
-    f.hbo = opts.hbo ? reinterpret_cast<vxa_hit_record*>(opts.hbo->data()) : nullptr;
+    f.hbo = nullptr;
+    f.hbo_device = opts.hbo ? opts.hbo->device_for_frame() : 0; // GPU-resident, no per-frame transfers
 
     if (ex.aov) ex.aov->resize(static_cast<std::size_t>(cam.width) * static_cast<std::size_t>(cam.height));
     vxa_stats ds{};
     check(vxa_render(context(), &f, inst.data(), static_cast<std::uint32_t>(inst.size()),
                      rgb_out, ex.aov ? ex.aov->data() : nullptr, &ds),
           "vxa_render");
+    if (opts.hbo) opts.hbo->frame_written();
     stats = FrameStats{};
     stats.rays = ds.rays;
     stats.sphere_tests = ds.sphere_tests;

@@ -54,6 +54,16 @@ def test_hbo_transparency_and_reference_stats(gpu, precision):
             assert (a == r_img).all(), f"frame {frame}: differs from the reference"
             for k in ("pixels_reused", "svo_traversals", "sphere_tests", "rays"):
                 assert sa[k] == r_st[k], (frame, k, sa[k], r_st[k])
+            # the GPU-resident HitBuffer, as the host sees it, equals the reference's records
+            ours, theirs = hbo.records(), rhbo.records()
+            for f in ("color", "normal", "t", "object_id", "kind"):
+                assert (ours[f] == theirs[f]).all(), (frame, f)
+            if frame in (9, 17):
+                # a host write between frames reaches the next frame on both sides
+                rec = theirs[20, 30].copy()
+                rec["kind"], rec["object_id"] = 1, 1
+                hbo.set_record(30, 20, rec)
+                rhbo.set_record(30, 20, rec)
         for sc in (s_hbo, s_plain, o):
             sc.mark_clean()
     assert reused_total > 0
