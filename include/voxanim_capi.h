@@ -40,12 +40,15 @@ vxn_model* vxn_model_from_grid(const uint64_t* words, uint32_t depth, uint32_t c
  * 3^depth rounded up to a power of two). Returns the word count, or -1. */
 int64_t vxn_grid_primitive(int kind, uint32_t depth, uint64_t* out, size_t cap_words, uint32_t* grid_depth);
 vxn_model* vxn_model_deserialize(const uint8_t* bytes, size_t n);
+int vxn_model_save(const vxn_model* m, const char* path);         /* save_svo */
 int64_t vxn_model_serialize(const vxn_model* m, uint8_t* out, size_t cap); /* returns the size */
 int vxn_model_info(const vxn_model* m, uint32_t* depth, uint64_t* nodes, uint64_t* attrs);
 int vxn_model_validate(const vxn_model* m);                     /* number of violations */
 void vxn_model_free(vxn_model* m);
 
 /* scenes (bench_scenes.hpp configurations) */
+/* load_scene_file(path) with the camera resolution set to width x height (the CLI's bench) */
+vxn_scene* vxn_scene_load(const char* path, int width, int height);
 vxn_scene* vxn_scene_config(int config, vxn_model* const* models, uint32_t n_models, uint64_t seed, int width,
                             int height);
 int vxn_scene_evaluate(vxn_scene* s, double time);

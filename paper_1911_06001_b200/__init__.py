@@ -107,6 +107,10 @@ class Model:
         buf = C.create_string_buffer(data, len(data))
         return cls(voxanim().vxn_model_deserialize(buf, len(data)))
 
+    def save(self, path: str) -> None:
+        """voxanim::save_svo."""
+        _check(voxanim().vxn_model_save(self._h, str(path).encode()), "save_svo")
+
     def serialize(self) -> bytes:
         n = voxanim().vxn_model_serialize(self._h, None, 0)
         if n < 0:
@@ -186,6 +190,18 @@ class Scene:
         f = vxa_frame_desc()
         _check(voxanim().vxn_scene_export(self._h, C.byref(f), None, 0, None), "export")
         self.width, self.height = f.camera.width, f.camera.height
+
+    @classmethod
+    def load(cls, path: str, width: int = 640, height: int = 480) -> "Scene":
+        """voxanim::load_scene_file(path), camera resolution width x height."""
+        h = voxanim().vxn_scene_load(str(path).encode(), width, height)
+        if not h:
+            raise VoxanimError(_err())
+        self = cls.__new__(cls)
+        self.models = []
+        self._h = C.c_void_p(h)
+        self.width, self.height = width, height
+        return self
 
     def evaluate(self, t: float) -> None:
         _check(voxanim().vxn_scene_evaluate(self._h, t), "evaluate_animation")

@@ -177,7 +177,7 @@ VXA_SYMBOLS = [
 ]
 VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
-    "vxn_model_from_grid", "vxn_grid_primitive", "vxn_model_deserialize", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
+    "vxn_model_from_grid", "vxn_grid_primitive", "vxn_model_deserialize", "vxn_model_save", "vxn_scene_load", "vxn_model_serialize", "vxn_model_info", "vxn_model_validate", "vxn_model_free",
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
     "vxn_scene_set_camera",
     "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit", "vxn_scene_stream",
@@ -253,6 +253,8 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_model_from_grid", P, P, u32, u32, u32, i)
     _declare(lib, "vxn_grid_primitive", C.c_int64, i, u32, P, C.c_size_t, C.POINTER(u32))
     _declare(lib, "vxn_model_deserialize", P, P, C.c_size_t)
+    _declare(lib, "vxn_model_save", i, P, C.c_char_p)
+    _declare(lib, "vxn_scene_load", P, C.c_char_p, i, i)
     _declare(lib, "vxn_model_serialize", C.c_int64, P, P, C.c_size_t)
     _declare(lib, "vxn_model_info", i, P, C.POINTER(u32), C.POINTER(u64), C.POINTER(u64))
     _declare(lib, "vxn_model_validate", i, P)

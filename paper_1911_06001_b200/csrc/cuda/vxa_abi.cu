@@ -171,6 +171,7 @@ struct vxa_ctx {
 
     DevBuf<uint32_t> tile_counter;
     DevBuf<unsigned long long> counters;
+    unsigned long long* counters_host = nullptr; // pinned, 8 counters
     DevBuf<unsigned char> inst_dev;
     DevBuf<uint16_t> super_list;  // per-super-tile candidate lists (large scenes)
     DevBuf<uint32_t> super_count;
@@ -512,10 +513,16 @@ int enqueue_any(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, u
     return enqueue_frame<float>(ctx, f, in, n, aov, hbo, reset);
 }
 
-int read_counters(vxa_ctx* ctx, vxa_stats* s) {
+// prefetched: the caller already copied the counters into ctx->counters_host
+// on the stream and synchronised it (one synchronisation per render call).
+int read_counters(vxa_ctx* ctx, vxa_stats* s, bool prefetched = false) {
     unsigned long long c[8] = {};
-    VXA_CUDA(cudaMemcpyAsync(c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
-    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (prefetched && ctx->counters_host != nullptr) {
+        std::memcpy(c, ctx->counters_host, sizeof(c));
+    } else {
+        VXA_CUDA(cudaMemcpyAsync(c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+        VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     s->rays = ctx->n_rays;
     s->sphere_tests = ctx->n_sphere_tests;
     s->svo_traversals = c[2];
@@ -638,6 +645,7 @@ int vxa_destroy(vxa_ctx* ctx) {
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->stream);
+    if (ctx->counters_host) cudaFreeHost(ctx->counters_host);
     delete ctx;
     return VXA_OK;
 }
@@ -1010,9 +1018,16 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         VXA_CUDA(cudaMemcpyAsync(f->hbo, hbo, npix * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->d2h += npix * sizeof(HitRec);
     }
+    if (stats) { // counters ride the same synchronisation as the image
+        if (ctx->counters_host == nullptr)
+            VXA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->counters_host), 8 * sizeof(unsigned long long),
+                                   cudaHostAllocDefault));
+        VXA_CUDA(cudaMemcpyAsync(ctx->counters_host, ctx->counters.ptr, 8 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    }
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
     if (stats) {
-        if (int rc = read_counters(ctx, stats); rc != VXA_OK) return rc;
+        if (int rc = read_counters(ctx, stats, true); rc != VXA_OK) return rc;
         stats->kernel_launches = launches;
     }
     return VXA_OK;

@@ -123,6 +123,26 @@ int64_t vxn_grid_primitive(int kind, uint32_t depth, uint64_t* out, size_t cap_w
         int64_t{-1});
 }
 
+int vxn_model_save(const vxn_model* m, const char* path) {
+    return guard(
+        [&] {
+            voxanim::save_svo(path, *m->m);
+            return 0;
+        },
+        -1);
+}
+
+vxn_scene* vxn_scene_load(const char* path, int width, int height) {
+    return guard(
+        [&] {
+            auto* s = new vxn_scene{voxanim::load_scene_file(path)};
+            s->s.camera.width = width;
+            s->s.camera.height = height;
+            return s;
+        },
+        static_cast<vxn_scene*>(nullptr));
+}
+
 vxn_model* vxn_model_deserialize(const uint8_t* bytes, size_t n) {
     return guard([&] { return wrap(voxanim::deserialize(std::span<const std::uint8_t>(bytes, n))); },
                  static_cast<vxn_model*>(nullptr));

@@ -46,17 +46,19 @@ std::uint64_t fold_bytes(std::uint64_t h, const void* p, std::size_t n) {
     return h;
 }
 
-// Whole content for small models, a strided sample for large ones (large
-// models are immutable after build in practice: SPEC, renderer usage).
+// Whole content for tiny models, a strided sample otherwise: it tells apart
+// different models that reuse one storage address (models are shared
+// immutably, shared_ptr<const SvoModel>), and it runs on every frame, so it
+// stays small (a full hash of a 1 MB model per call would dominate small frames).
 std::uint64_t signature(const SvoModel& m) {
     std::uint64_t h = mix64(m.depth, m.nodes.size() * 1315423911ull + m.attributes.size());
     const std::size_t nb = m.nodes.size() * sizeof(SvoNode), ab = m.attributes.size() * sizeof(VoxelAttribute);
-    if (nb + ab <= (std::size_t{1} << 20)) {
+    if (nb + ab <= 4096) {
         h = fold_bytes(h, m.nodes.data(), nb);
         return fold_bytes(h, m.attributes.data(), ab);
     }
     const std::size_t nn = m.nodes.size(), na = m.attributes.size();
-    for (std::size_t k = 0; k < 1024; ++k) {
+    for (std::size_t k = 0; k < 64; ++k) {
         h = fold_bytes(h, &m.nodes[(k * 2654435761ull) % nn], sizeof(SvoNode));
         if (na) h = fold_bytes(h, &m.attributes[(k * 40503ull) % na], sizeof(VoxelAttribute));
     }

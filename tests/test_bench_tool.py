@@ -71,3 +71,17 @@ def test_bench_report_csv_layout():
                                                          "pixels_reused": 4})
     assert out.splitlines() == [CSV_HEADER, "animated-opt,0,0.5,10,20,3,4", "animated-opt,1,0.25,10,20,3,4",
                                 "animated-opt,0.375,2666.6666666666665"]
+
+
+def test_acceptance_fixture_builds_and_loads(tmp_path):
+    """tools/acceptance_perf.py's fixture: the reference acceptance models and
+    scene documents, built with this library and read back by load_scene_file."""
+    import paper_1911_06001_b200 as vx
+    from acceptance_perf import build_fixture
+
+    build_fixture(vx, str(tmp_path))
+    bench = vx.Scene.load(str(tmp_path / "bench.json"), 640, 480)
+    single = vx.Scene.load(str(tmp_path / "single.json"), 320, 240)
+    assert bench.object_count() == 4 and single.object_count() == 1
+    bench.evaluate(0.5)
+    assert bench.get_object(2)[2] and not bench.get_object(0)[2]  # the tracked object moved, the static one not

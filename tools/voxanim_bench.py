@@ -65,9 +65,32 @@ def model_for(vx, config: int):
     return vx.Model.procedural(11, shell=True)
 
 
+def run_mode(vx, scene, mode: str, frames: int, fps: float, width: int, height: int):
+    """cmd_bench's frame loop (cli.cpp:248-278) on one scene: returns (per-frame ms, counter totals)."""
+    animate = mode != "static"
+    opt = mode == "animated-opt"
+    hbo = vx.HitBuffer(width, height) if opt else None
+    # One untimed render first: the device context, the model's one-time
+    # upload to HBM and the first launch of the kernel variant are not frame
+    # costs (a throwaway hit buffer, no mark_clean: the scene's dirty state and
+    # the timed HBO are untouched).
+    scene.render(culling=opt, sorting=opt, hbo=vx.HitBuffer(width, height) if opt else None)
+    per_frame, totals = [], {"rays": 0, "sphere_tests": 0, "svo_traversals": 0, "pixels_reused": 0}
+    for frame in range(frames):
+        if animate:
+            scene.evaluate(frame / fps)
+        _, _, st = scene.render(culling=opt, sorting=opt, hbo=hbo)
+        scene.mark_clean()
+        per_frame.append(st["render_ms"])
+        for k in totals:
+            totals[k] += int(st[k])
+    return per_frame, totals
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("--config", type=int, default=2, help="benchmark configuration (1-4, SURVEY.md §8(d))")
+    ap.add_argument("--scene", default=None, help="a scene document (voxanim::load_scene_file) instead of --config")
     ap.add_argument("--mode", default="static", choices=["static", "animated", "animated-opt"])
     ap.add_argument("--frames", type=int, default=60)
     ap.add_argument("--width", type=int, default=640)
@@ -82,23 +105,11 @@ def main(argv=None) -> int:
 
     import paper_1911_06001_b200 as vx
 
-    scene = vx.Scene(args.config, [model_for(vx, args.config)], 0, args.width, args.height)
-    animate = args.mode != "static"
-    opt = args.mode == "animated-opt"
-    hbo = vx.HitBuffer(args.width, args.height) if opt else None
-    # One untimed render first: the device context and the model's one-time
-    # upload to HBM are not frame costs (no hit buffer, no mark_clean: the
-    # scene's dirty state and the HBO are untouched).
-    scene.render(culling=opt, sorting=opt)
-    per_frame, totals = [], {"rays": 0, "sphere_tests": 0, "svo_traversals": 0, "pixels_reused": 0}
-    for frame in range(args.frames):
-        if animate:
-            scene.evaluate(frame / args.fps)
-        _, _, st = scene.render(culling=opt, sorting=opt, hbo=hbo)
-        scene.mark_clean()
-        per_frame.append(st["render_ms"])
-        for k in totals:
-            totals[k] += int(st[k])
+    if args.scene:
+        scene = vx.Scene.load(args.scene, args.width, args.height)
+    else:
+        scene = vx.Scene(args.config, [model_for(vx, args.config)], 0, args.width, args.height)
+    per_frame, totals = run_mode(vx, scene, args.mode, args.frames, args.fps, args.width, args.height)
     text = bench_report_csv(args.mode, per_frame, totals)
     if args.csv:
         with open(args.csv, "w") as f:
