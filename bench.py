@@ -573,8 +573,9 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step,
                "ms_per_step": round(el * 1e3 / args.e2e_steps, 3),
                "path": "evaluate_animation + vxa_submit_readback per step: instance table H2D from pinned "
-                       "staging, frame kernel, RGB8 pack, D2H into a page-locked host image on a copy "
-                       "stream (overlapping the next frame's kernel); wall clock over all steps",
+                       "staging, culling pre-pass + frame kernel (which also writes the RGB8 image), D2H "
+                       "into a page-locked host image on a copy stream (overlapping the next frame's "
+                       "kernel); wall clock over all steps",
                "sync": {"value": round(rays * args.e2e_steps / el_sync / 1e6, 3),
                         "ms_per_step": round(el_sync * 1e3 / args.e2e_steps, 3),
                         "path": "voxanim::gpu::render_frame_into, one synchronous call per step"}}
