@@ -1,0 +1,31 @@
+"""GPU: the multi-rank path of bench.py end to end on one device. Two ranks
+(torchrun, gloo barriers, --same-device) each render their 64x64 super-tiles of
+the C4 frame; rank 1 maps rank 0's framebuffer through CUDA IPC and stores its
+pixels there; rank 0 checks the composed frame against its own single-device
+render of the same animation time (multi_gpu_frame_identical). On a multi-GPU
+box the same code runs with one device per rank and NVLink peer stores."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_two_ranks_compose_the_single_device_frame(gpu):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--same-device", "--no-cpu-baseline", "--no-extras"]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2
+    assert d["config"]["composition"].startswith("NVLink peer stores")
+    assert d["multi_gpu_frame_identical"] is True
+    assert d["e2e"] is not None and d["e2e"]["value"] > 0
