@@ -226,3 +226,31 @@ def test_concurrent_render_calls_from_host_threads(gpu):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+def test_c_abi_misuse_is_reported_not_fatal(gpu):
+    """Unknown handles, double releases, unknown readback tickets and null
+    arguments return status codes; an instance whose model handle is unknown is
+    skipped like a reference object without a model (renderer.cpp:74-76)."""
+    lib = vx.vxa()
+    ctx = vx.context()
+    inv = _abi.VXA_ERR_INVALID
+    assert lib.vxa_release_model(ctx, 987654) == inv
+    assert lib.vxa_hbo_release(ctx, 987654) == inv
+    assert lib.vxa_model_info(ctx, 987654, None, None) == inv
+    assert lib.vxa_wait_readback(ctx, 1 << 40) == inv
+    assert lib.vxa_build_model(ctx, None, 3, 0, 0, None, None, None) == inv
+    h = C.c_uint32()
+    m = vx.Model.random(5, 3, 0.5).serialize()
+    assert lib.vxa_upload_svo(ctx, m, len(m), C.byref(h), None) == 0
+    assert lib.vxa_release_model(ctx, h.value) == 0
+    assert lib.vxa_release_model(ctx, h.value) == inv  # double release
+    # an instance pointing at no model: skipped, the frame equals the frame without it
+    s = vx.Scene(vx.config.TWO_OBJECTS, [vx.Model.random(4, 3, 0.4)])
+    f, inst, n = s.export()
+    with_ghost = np.zeros((s.height, s.width, 3), np.uint8)
+    inst[0].model = 987654
+    assert lib.vxa_render(ctx, C.byref(f), inst, n, with_ghost.ctypes.data, None, None) == 0
+    without = np.zeros_like(with_ghost)
+    assert lib.vxa_render(ctx, C.byref(f), C.byref(inst[1]), 1, without.ctypes.data, None, None) == 0
+    assert (with_ghost == without).all()
