@@ -270,3 +270,54 @@ def test_super_tile_list_overflow(gpu):
         o.evaluate(t)
         o_aov, o_img = check_fp64(s, o)
         check_fp32(s, o, o_aov, o_img)
+
+
+def _depth_first_layout(svo: bytes) -> bytes:
+    """The same octree with nodes numbered depth-first (each node's children
+    allocated as one contiguous block when the node is visited, so children
+    still follow their parent) and attributes renumbered in that order: a
+    valid .svo that is not in the reference builder's breadth-first order."""
+    import struct
+    depth, nn, na = struct.unpack_from("<III", svo, 8)
+    recs = [struct.unpack_from("<IIBB", svo, 20 + 12 * i) for i in range(nn)]
+    attrs = [svo[20 + 12 * nn + 4 * k: 24 + 12 * nn + 4 * k] for k in range(na)]
+    new_of = {0: 0}
+    out_nodes, out_attrs = [None] * nn, []
+    next_free = 1
+
+    def visit(old):
+        nonlocal next_free
+        cb, ab, valid, leaf = recs[old]
+        internal = valid & ~leaf & 0xFF
+        kids = bin(internal).count("1")
+        leaves = bin(valid & leaf).count("1")
+        new_cb = next_free if kids else 0
+        next_free += kids
+        new_ab = len(out_attrs) if leaves else 0
+        out_attrs.extend(attrs[ab:ab + leaves])
+        out_nodes[new_of[old]] = (new_cb, new_ab, valid, leaf)
+        for k in range(kids):
+            new_of[cb + k] = new_cb + k
+        for k in range(kids):
+            visit(cb + k)
+
+    visit(0)
+    body = b"".join(struct.pack("<IIBBxx", *r) for r in out_nodes)
+    return svo[:20] + body + b"".join(out_attrs)
+
+
+def test_depth_first_node_layout(gpu):
+    """A model whose nodes are not in breadth-first order (any order with
+    children after their parent is a valid .svo): both kernels render it like
+    the reference renders the same bytes."""
+    import sys
+    sys.setrecursionlimit(10000)
+    for base in (vx.Model.random(31, 5, 0.15), vx.Model.procedural(6, shell=True)):
+        dfs = _depth_first_layout(base.serialize())
+        assert dfs != base.serialize()
+        m = vx.Model.from_bytes(dfs)
+        assert m.violations() == 0
+        s, o = pair(vx.config.RANDOM, [m, vx.Model.full_cube()], seed=8)
+        for culling, sorting in ((True, True), (False, False)):
+            o_aov, o_img = check_fp64(s, o, culling, sorting)
+            check_fp32(s, o, o_aov, o_img, culling, sorting)
