@@ -22,6 +22,9 @@ enum : uint32_t { kMiss = 0, kSingle = 1, kMulti = 2 };
 constexpr int kBlock = 128;
 // Minimum resident blocks per SM requested from ptxas for the FP32 kernel
 // (register budget 65536 / (128 * n)); tuned by measurement.
+#ifndef VXA_MIN_BLOCKS_F64
+#define VXA_MIN_BLOCKS_F64 1 // the FP64 parity kernel: no register cap
+#endif
 #ifndef VXA_MIN_BLOCKS
 #define VXA_MIN_BLOCKS 8
 #endif
@@ -287,7 +290,7 @@ __device__ __forceinline__ uint32_t shade_rgba(uint32_t color, const Real n[3], 
 }
 
 template <typename Real, bool kAov, bool kHbo, bool kCompact>
-__global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : 1) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
+__global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : VXA_MIN_BLOCKS_F64) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
     extern __shared__ uint2 smem_stack[]; // FP32 traversal stack: [level][thread]
     __shared__ uint16_t s_list[kWarps][kListCap];
     const uint32_t lane = threadIdx.x & 31u;
