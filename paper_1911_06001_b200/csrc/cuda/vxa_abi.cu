@@ -556,6 +556,10 @@ const char* vxa_last_error(void) { return g_error.c_str(); }
 
 int vxa_abi_version(void) { return VXA_ABI_VERSION; }
 
+namespace {
+int init_ctx(vxa_ctx* ctx);
+}
+
 int vxa_create(int device, vxa_ctx** out) {
     if (out == nullptr) return fail(VXA_ERR_INVALID, "null output pointer");
     *out = nullptr;
@@ -573,10 +577,21 @@ int vxa_create(int device, vxa_ctx** out) {
     if (prop.major != 10)
         return fail(VXA_ERR_NO_DEVICE, std::string("device is not sm_100 (Blackwell): ") + prop.name);
     VXA_CUDA(cudaSetDevice(device));
-    auto ctx = std::make_unique<vxa_ctx>();
+    auto* ctx = new vxa_ctx;
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
     std::snprintf(ctx->name, sizeof(ctx->name), "%s", prop.name);
+    if (const int rc = init_ctx(ctx); rc != VXA_OK) {
+        vxa_destroy(ctx); // releases whatever was created before the failure
+        return rc;
+    }
+    *out = ctx;
+    return VXA_OK;
+}
+
+namespace {
+// Streams, events and the small device buffers of a new context.
+int init_ctx(vxa_ctx* ctx) {
     VXA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     VXA_CUDA(ctx->tile_counter.ensure(1));
     VXA_CUDA(ctx->counters.ensure(8));
@@ -595,9 +610,9 @@ int vxa_create(int device, vxa_ctx** out) {
     VXA_CUDA(cudaEventCreate(&ctx->ev_b));
     VXA_CUDA(cudaEventCreate(&ctx->t_a));
     VXA_CUDA(cudaEventCreate(&ctx->t_b));
-    *out = ctx.release();
     return VXA_OK;
 }
+} // namespace
 
 namespace {
 int flush_readback(vxa_ctx* ctx);
@@ -606,8 +621,10 @@ int flush_readback(vxa_ctx* ctx);
 int vxa_destroy(vxa_ctx* ctx) {
     if (ctx == nullptr) return VXA_OK;
     cudaSetDevice(ctx->device);
-    flush_readback(ctx); // a streamed frame still pending lands before teardown
-    cudaStreamSynchronize(ctx->stream);
+    if (ctx->stream) {
+        flush_readback(ctx); // a streamed frame still pending lands before teardown
+        cudaStreamSynchronize(ctx->stream);
+    }
     for (auto& [h, m] : ctx->models) m.free_all();
     ctx->build.grid.release();
     ctx->build.pyramid.release();
@@ -644,7 +661,7 @@ int vxa_destroy(vxa_ctx* ctx) {
         if (ctx->rb_done[k]) cudaEventDestroy(ctx->rb_done[k]);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
-    cudaStreamDestroy(ctx->stream);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->counters_host) cudaFreeHost(ctx->counters_host);
     delete ctx;
     return VXA_OK;
