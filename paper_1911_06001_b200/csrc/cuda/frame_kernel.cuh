@@ -175,11 +175,17 @@ __device__ __forceinline__ bool cone_candidate(const float4 in, const TileCone& 
     const float dist2 = lx * lx + ly * ly + lz * lz;
     const float r = in.w * 1.001f + 1e-5f * sqrtf(dist2) + 1e-6f;
     if (dist2 <= r * r) return true; // camera inside the (inflated) sphere
+    // Conservative for the reference's sphere test (renderer.cpp:25-43), which
+    // counts a hit when the ray's infinite line passes within r of the centre
+    // and t_c + r >= 0 -- also for a chord wholly behind the camera. So: the
+    // lateral distance is taken to the double cone (|s|), and a sphere behind
+    // the apex is dropped only if even the most favourable direction of the
+    // cone has t_c = L.d < -r.
     const float s = lx * c.a[0] + ly * c.a[1] + lz * c.a[2];
     const float qx = ly * c.a[2] - lz * c.a[1], qy = lz * c.a[0] - lx * c.a[2], qz = lx * c.a[1] - ly * c.a[0];
     const float perp = sqrtf(qx * qx + qy * qy + qz * qz);
-    if (perp * c.cos_a - s * c.sin_a > r) return false; // outside the lateral surface
-    return s * c.cos_a + perp * c.sin_a >= 0.0f;        // else only the apex region remains
+    if (perp * c.cos_a - fabsf(s) * c.sin_a > r) return false; // outside the lateral surface
+    return s * c.cos_a + perp * c.sin_a >= -r;                 // max over the cone of L.d, against -r
 }
 
 template <typename Real, bool kAov, bool kCompact>

@@ -4,6 +4,8 @@ cameras -- far, near, inside an instance, any orientation and field of view --
 and random culling/sorting options. FP64 kernel: bit-exact with the reference
 per pixel (image, hit, node, attribute, level, voxel, t, counts); FP32 kernel:
 hits identical except classified slab-test ties (tests/test_gpu_parity.py)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -33,7 +35,13 @@ def unit(rng):
     return v / np.linalg.norm(v)
 
 
-@pytest.mark.parametrize("seed", range(64))
+# VOXANIM_FUZZ_SEEDS=N widens the sweep (a soak run); 64 by default. Seeds 96, 174
+# and 177 found (in a 400-seed soak) spheres wholly behind the camera that the
+# reference's loose sphere test counts as hit while the tile cone dropped them.
+SEEDS = sorted(set(range(int(os.environ.get("VOXANIM_FUZZ_SEEDS", "64")))) | {96, 174, 177})
+
+
+@pytest.mark.parametrize("seed", SEEDS)
 def test_random_scene_random_camera(gpu, seed):
     rng = np.random.default_rng(1000 + seed)
     models = random_models(rng)
