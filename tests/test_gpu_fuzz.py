@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1911_06001_b200 as vx
+from oracle import ref
 from test_gpu_parity import check_fp32, check_fp64, pair
 
 pytestmark = pytest.mark.gpu
@@ -69,3 +70,69 @@ def test_random_scene_random_camera(gpu, seed):
     culling, sorting = bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
     o_aov, o_img = check_fp64(s, o, culling, sorting)
     check_fp32(s, o, o_aov, o_img, culling, sorting, max_tie_frac=0.02)
+
+
+def _random_camera(rng, s):
+    _, tf, _ = s.get_object(int(rng.integers(0, s.object_count())))
+    at = np.array(tf[9:12]) + rng.uniform(-1.0, 1.0, 3)
+    pos = at + unit(rng) * rng.uniform(0.5, 9.0)
+    up = unit(rng)
+    fwd = (at - pos) / np.linalg.norm(at - pos)
+    if np.linalg.norm(np.cross(fwd, up)) < 0.1:
+        up = np.array([0.0, 1.0, 0.0]) if abs(fwd[1]) < 0.9 else np.array([1.0, 0.0, 0.0])
+    return pos.tolist(), at.tolist(), up.tolist(), float(rng.uniform(25.0, 100.0))
+
+
+SEEDS_MANY = range(int(os.environ.get("VOXANIM_FUZZ_SEEDS_MANY", "12")))
+
+
+@pytest.mark.parametrize("seed", SEEDS_MANY)
+def test_many_instances_random_camera(gpu, seed):
+    """200 instances (config MANY: the super-tile culling pre-pass runs) seen
+    from random cameras, in and around the crowd."""
+    rng = np.random.default_rng(5000 + seed)
+    models = [vx.Model.procedural(int(rng.integers(4, 7)), shell=True), vx.Model.random(seed, 4, 0.3)]
+    s, o = pair(vx.config.MANY, models, seed=seed, w=160, h=120)
+    cam = _random_camera(rng, s)
+    for sc in (s, o):
+        sc.set_camera(*cam)
+    o_aov, o_img = check_fp64(s, o)
+    check_fp32(s, o, o_aov, o_img, max_tie_frac=0.02)
+
+
+SEEDS_HBO = range(int(os.environ.get("VOXANIM_FUZZ_SEEDS_HBO", "8")))
+
+
+@pytest.mark.parametrize("seed", SEEDS_HBO)
+def test_hit_buffer_random_sequences(gpu, seed):
+    """Random scenes and cameras, 12 frames with the hit buffer: objects moved or
+    touched at random, the camera made dirty at random. FP64: image, FrameStats
+    and every record equal the reference's with its own HitBuffer."""
+    rng = np.random.default_rng(7000 + seed)
+    models = random_models(rng)
+    s, o = pair(vx.config.RANDOM, models, seed=int(rng.integers(0, 1 << 30)), w=96, h=64)
+    cam = _random_camera(rng, s)
+    for sc in (s, o):
+        sc.set_camera(*cam)
+    hbo, rhbo = vx.HitBuffer(96, 64), ref.RefHitBuffer(96, 64)
+    for frame in range(12):
+        for _ in range(int(rng.integers(0, 3))):
+            i = int(rng.integers(0, s.object_count()))
+            _, tf, _ = s.get_object(i)
+            if rng.uniform() < 0.5:
+                tf[9:12] = (np.array(tf[9:12]) + rng.uniform(-0.3, 0.3, 3)).tolist()
+            for sc in (s, o):
+                sc.set_object(i, tf, True)
+        if rng.uniform() < 0.2:
+            for sc in (s, o):
+                sc.set_camera_dirty(True)
+        a, _, st = s.render(precision=vx.VXA_FP64, hbo=hbo)
+        r, rst = o.render(hbo=rhbo)
+        assert (a == r).all(), frame
+        for k in ("pixels_reused", "svo_traversals", "sphere_tests"):
+            assert st[k] == rst[k], (frame, k)
+        ours, theirs = hbo.records(), rhbo.records()
+        for f in ("color", "normal", "t", "object_id", "kind"):
+            assert (ours[f] == theirs[f]).all(), (frame, f)
+        for sc in (s, o):
+            sc.mark_clean()
