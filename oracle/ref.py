@@ -59,6 +59,7 @@ def lib() -> C.CDLL:
             "vref_model_random": (P, u64, u32, d),
             "vref_model_from_grid": (P, P, u32, u32, u32),
             "vref_model_serialize": (C.c_int64, P, P, C.c_size_t),
+            "vref_model_validate": (i, P),
             "vref_model_free": (None, P),
             "vref_scene_config": (P, i, C.POINTER(P), u32, u64, i, i),
             "vref_scene_evaluate": (i, P, d),
@@ -128,6 +129,9 @@ class RefModel:
         import numpy as np
         w = np.ascontiguousarray(words, dtype=np.uint64)
         return cls(lib().vref_model_from_grid(w.ctypes.data, depth, color_mode, color_rgba))
+
+    def violations(self) -> int:
+        return lib().vref_model_validate(self._h)
 
     def serialize(self) -> bytes:
         n = lib().vref_model_serialize(self._h, None, 0)

@@ -451,6 +451,10 @@ VREF_API vref_model* vref_model_random(uint64_t seed, uint32_t depth, double fil
         (vref_model*)nullptr);
 }
 
+VREF_API int vref_model_validate(const vref_model* m) {
+    return static_cast<int>(validate(*m->m).violations.size());
+}
+
 VREF_API int64_t vref_model_serialize(const vref_model* m, uint8_t* out, size_t cap) {
     return guard(
         [&]() -> int64_t {

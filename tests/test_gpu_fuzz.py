@@ -136,3 +136,72 @@ def test_hit_buffer_random_sequences(gpu, seed):
             assert (ours[f] == theirs[f]).all(), (frame, f)
         for sc in (s, o):
             sc.mark_clean()
+
+
+SEEDS_BUILD = range(int(os.environ.get("VOXANIM_FUZZ_SEEDS_BUILD", "8")))
+
+
+@pytest.mark.parametrize("seed", SEEDS_BUILD)
+def test_device_builder_random_grids(gpu, seed):
+    """vxa_build_model on random grids (depth 1-7, fills from empty to full,
+    clustered or uniform, every colour mode): byte-identical to the reference."""
+    rng = np.random.default_rng(9000 + seed)
+    depth = int(rng.integers(1, 8))
+    n = 1 << depth
+    if rng.uniform() < 0.5:
+        bits = rng.random(n ** 3) < rng.uniform(0.0, 1.0) ** 3
+    else:  # clusters: a few random boxes
+        g = np.zeros((n, n, n), bool)
+        for _ in range(int(rng.integers(1, 6))):
+            lo = rng.integers(0, n, 3)
+            hi = lo + rng.integers(1, n + 1, 3)
+            g[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]] = True
+        bits = g.ravel()
+    pad = (-bits.size) % 64
+    b = np.concatenate([bits, np.zeros(pad, bool)]).reshape(-1, 64)
+    words = (b.astype(np.uint64) << np.arange(64, dtype=np.uint64)).sum(axis=1, dtype=np.uint64)
+    mode = int(rng.integers(0, 3))
+    rgba = int(rng.integers(0, 1 << 32))
+    ours = vx.Model.from_grid(words, depth, mode, rgba, device=True).serialize()
+    assert ours == ref.RefModel.from_grid(words, depth, mode, rgba).serialize(), (depth, mode)
+
+
+SEEDS_SVO = range(int(os.environ.get("VOXANIM_FUZZ_SEEDS_SVO", "8")))
+
+
+@pytest.mark.parametrize("seed", SEEDS_SVO)
+def test_svo_stream_random_corruption(gpu, seed):
+    """vxa_upload_svo on randomly corrupted .svo streams (byte flips, truncation,
+    extension): whenever the reference's deserialize() rejects a stream, so do we,
+    with its SvoFormatErrorCode class and message; a stream it accepts we accept
+    too unless the reference's validate() flags it (the GPU needs a valid model)."""
+    import ctypes as C
+
+    rng = np.random.default_rng(11000 + seed)
+    good = bytearray(vx.Model.random(int(rng.integers(0, 1 << 30)), int(rng.integers(1, 5)), 0.4).serialize())
+    lib, ctx = vx.vxa(), vx.context()
+    for _ in range(40):
+        data = bytearray(good)
+        op = rng.integers(0, 3)
+        if op == 0:
+            for _ in range(int(rng.integers(1, 4))):
+                data[int(rng.integers(0, len(data)))] = int(rng.integers(0, 256))
+        elif op == 1:
+            data = data[:int(rng.integers(0, len(data)))]
+        else:
+            data += bytes(int(rng.integers(1, 9)))
+        data = bytes(data)
+        h, code = C.c_uint32(), C.c_int32()
+        rc = lib.vxa_upload_svo(ctx, data, len(data), C.byref(h), C.byref(code))
+        try:
+            rm = ref.RefModel.from_bytes(data)
+            ref_err = None
+        except RuntimeError as e:
+            rm, ref_err = None, str(e)
+        if ref_err is not None:
+            assert rc == 2 and code.value >= 0, (ref_err, rc)
+            assert lib.vxa_last_error().decode() == ref_err
+        elif rc == 0:
+            lib.vxa_release_model(ctx, h.value)
+        else:
+            assert code.value == -1 and rm.violations() > 0, lib.vxa_last_error().decode()
