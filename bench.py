@@ -371,6 +371,12 @@ def run_reference(args):
 def run_ours(args):
     rank, world, local = dist_env()
     device = 0 if args.same_device else local
+    if world > 1 and not args.same_device:
+        import torch
+
+        # a launcher that gives each process one visible GPU: LOCAL_RANK is not an ordinal there
+        if torch.cuda.device_count() <= local:
+            device = local = 0
     os.environ["VOXANIM_DEVICE"] = str(device)
     import paper_1911_06001_b200 as vx
     from paper_1911_06001_b200 import _abi
