@@ -419,9 +419,42 @@ def run_ours(args):
         import torch
         t = torch.tensor([ok], dtype=torch.int32, device="cpu" if args.same_device else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if int(t.item()) == 0:
-            composition = ("none: CUDA IPC unavailable, each rank renders its super-tiles into its own "
-                           "framebuffer (no gather measured)")
+        if int(t.item()) == 0 or os.environ.get("VOXANIM_COMPOSE") == "gather":
+            # no CUDA IPC on every rank (or forced): compose by a collective gather instead
+            if rank != 0:
+                lib.vxa_fb_import(ctx, W, H, None)  # detach any peer mapping
+            composition = ("collective gather: each rank packs its super-tiles (vxa_tiles_pack), "
+                           "torch.distributed gather to rank 0, rank 0 unpacks them into its framebuffer")
+
+    gather_buf = None
+    if composition.startswith("collective"):
+        import torch
+
+        n_max = C.c_uint32()
+        check(lib.vxa_tiles_count(W, H, 0, world, C.byref(n_max)), "tiles_count")  # rank 0 has the most
+        dev = "cuda:0" if args.same_device else f"cuda:{local}"
+        gather_buf = torch.zeros(n_max.value * 64 * 64, dtype=torch.int32, device=dev)
+        gather_host = args.same_device  # gloo: the collective runs on host tensors
+
+    def gather_compose():
+        """The frame's super-tiles of every rank into rank 0's framebuffer (gather mode)."""
+        import torch
+
+        gather_buf.zero_()
+        torch.cuda.synchronize()
+        check(lib.vxa_tiles_pack(ctx, W, H, rank, world, C.c_void_p(gather_buf.data_ptr())), "tiles_pack")
+        check(lib.vxa_synchronize(ctx), "sync")
+        send = gather_buf.cpu() if gather_host else gather_buf
+        if rank == 0:
+            parts = [torch.empty_like(send) for _ in range(world)]
+            dist.gather(send, gather_list=parts, dst=0)
+            for r in range(1, world):
+                src = parts[r].to(gather_buf.device) if gather_host else parts[r]
+                torch.cuda.synchronize()
+                check(lib.vxa_tiles_unpack(ctx, W, H, r, world, C.c_void_p(src.data_ptr())), "tiles_unpack")
+            check(lib.vxa_synchronize(ctx), "sync")
+        else:
+            dist.gather(send, dst=0)
 
     vxl = vx.voxanim()
 
@@ -449,6 +482,8 @@ def run_ours(args):
             submit(args.warmup + k)
             if world > 1:
                 check(lib.vxa_synchronize(ctx), "sync")
+                if gather_buf is not None:
+                    gather_compose()
                 barrier()  # the frame is complete in rank 0's framebuffer only when every rank is done
             ms = C.c_double()
             check(lib.vxa_timer_end(ctx, C.byref(ms)), "timer")
@@ -490,6 +525,8 @@ def run_ours(args):
         k_chk = args.warmup + args.steps + 1
         submit(k_chk)
         check(lib.vxa_synchronize(ctx), "sync")
+        if gather_buf is not None:
+            gather_compose()
         barrier()
         if rank == 0:
             composed = np.empty((H, W, 3), np.uint8)
@@ -498,7 +535,7 @@ def run_ours(args):
                 raise RuntimeError(vxl.vxn_last_error().decode())
             alone = np.empty((H, W, 3), np.uint8)
             check(lib.vxa_read_framebuffer(ctx, alone.ctypes.data, W, H), "read_framebuffer")
-            multi_ok = bool((composed == alone).all()) if composition.startswith("NVLink") else None
+            multi_ok = bool((composed == alone).all())
         barrier()
 
     # end to end through the public API (voxanim::render_frame with host buffers)
@@ -517,6 +554,8 @@ def run_ours(args):
         for k in range(args.e2e_steps):
             submit(k)
             check(lib.vxa_synchronize(ctx), "sync")
+            if gather_buf is not None:
+                gather_compose()
             barrier()
             if rank == 0:
                 check(lib.vxa_read_framebuffer(ctx, host_img.ctypes.data, W, H), "read_framebuffer")

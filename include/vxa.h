@@ -242,12 +242,24 @@ void* vxa_stream(vxa_ctx* ctx);
  * store their super-tiles straight into rank 0's framebuffer through the
  * peer mapping (NVLink / NVSwitch). */
 int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_out);
-int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle);
+int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle); /* NULL: detach */
 
 /* Screen partition used when tile_world > 1: the rank that renders pixel
  * (x, y) of a width-wide frame split over `world` devices (64x64 super-tiles,
  * round-robin). Pure function, no device needed. */
 int32_t vxa_tile_owner(int32_t x, int32_t y, int32_t width, int32_t height, int32_t world);
+
+/* Composition without CUDA IPC (a collective gather instead of peer stores):
+ * rank `rank`'s super-tiles (s % world == rank, ascending s) as a tile-major
+ * device buffer of 64x64 RGBA8 pixels per tile (edge tiles padded).
+ * vxa_tiles_count: tiles of that rank (pure function); vxa_tiles_pack copies
+ * them out of this context's framebuffer into `dst` (device memory);
+ * vxa_tiles_unpack writes another rank's packed tiles into this context's
+ * framebuffer (rank 0 composing the frame). Both are ordered on the context
+ * stream (vxa_synchronize before handing `dst` to another stream). */
+int vxa_tiles_count(int32_t width, int32_t height, int32_t rank, int32_t world, uint32_t* count);
+int vxa_tiles_pack(vxa_ctx* ctx, int32_t width, int32_t height, int32_t rank, int32_t world, void* dst_device);
+int vxa_tiles_unpack(vxa_ctx* ctx, int32_t width, int32_t height, int32_t rank, int32_t world, const void* src_device);
 
 /* ---- single-ray traversal (voxanim::traverse / traverse_debug) ---------- */
 

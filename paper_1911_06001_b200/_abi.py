@@ -173,7 +173,7 @@ VXA_SYMBOLS = [
     "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_hbo_upload", "vxa_render", "vxa_submit", "vxa_submit_readback",
     "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
-    "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_traverse",
+    "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_tiles_count", "vxa_tiles_pack", "vxa_tiles_unpack", "vxa_traverse",
 ]
 VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
@@ -235,6 +235,9 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_fb_import", i, P, C.c_int32, C.c_int32, P)
     _declare(lib, "vxa_traverse", i, P, u32, P, u32, u32, P, P, u32)
     _declare(lib, "vxa_tile_owner", C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32)
+    _declare(lib, "vxa_tiles_count", i, i, i, i, i, C.POINTER(u32))
+    _declare(lib, "vxa_tiles_pack", i, P, i, i, i, i, P)
+    _declare(lib, "vxa_tiles_unpack", i, P, i, i, i, i, P)
     return lib
 
 

@@ -1289,13 +1289,14 @@ int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_
 }
 
 int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle) {
-    if (ctx == nullptr || ipc_handle == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
     std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     VXA_CUDA(cudaSetDevice(ctx->device));
     if (ctx->peer_fb) {
         cudaIpcCloseMemHandle(ctx->peer_fb);
         ctx->peer_fb = nullptr;
     }
+    if (ipc_handle == nullptr) return VXA_OK; // detach: frames store into the local framebuffer again
     cudaIpcMemHandle_t h;
     std::memcpy(&h, ipc_handle, sizeof(h));
     void* p = nullptr;
@@ -1309,6 +1310,64 @@ int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_h
 int32_t vxa_tile_owner(int32_t x, int32_t y, int32_t width, int32_t height, int32_t world) {
     if (world < 1 || x < 0 || y < 0 || x >= width || y >= height) return -1;
     return tile_owner(x, y, width, world);
+}
+
+namespace {
+// One thread per pixel of the rank's tiles: tile k is super-tile s = k * world + rank.
+__global__ void tiles_copy(uint32_t* fb, uint32_t* buf, int32_t width, int32_t height, uint32_t n_super_x,
+                           int32_t rank, int32_t world, uint32_t tiles, bool pack) {
+    const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+    if (i >= uint64_t{tiles} * kSuper * kSuper) return;
+    const uint32_t k = static_cast<uint32_t>(i / (kSuper * kSuper)), p = static_cast<uint32_t>(i % (kSuper * kSuper));
+    const uint32_t s = k * static_cast<uint32_t>(world) + static_cast<uint32_t>(rank);
+    const int32_t x = static_cast<int32_t>((s % n_super_x) * kSuper + p % kSuper);
+    const int32_t y = static_cast<int32_t>((s / n_super_x) * kSuper + p / kSuper);
+    if (x >= width || y >= height) {
+        if (pack) buf[i] = 0u; // padding of an edge tile
+        return;
+    }
+    const size_t f = static_cast<size_t>(y) * width + x;
+    if (pack)
+        buf[i] = fb[f];
+    else
+        fb[f] = buf[i];
+}
+
+uint32_t tiles_of(int32_t width, int32_t height, int32_t rank, int32_t world) {
+    const uint32_t n_super = super_tiles_x(width) * static_cast<uint32_t>((height + kSuper - 1) / kSuper);
+    return (n_super + static_cast<uint32_t>(world - rank) - 1) / static_cast<uint32_t>(world);
+}
+
+int tiles_move(vxa_ctx* ctx, int32_t width, int32_t height, int32_t rank, int32_t world, void* buf, bool pack) {
+    if (ctx == nullptr || buf == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (width < 1 || height < 1 || world < 1 || rank < 0 || rank >= world)
+        return fail(VXA_ERR_INVALID, "bad frame size or partition");
+    if (ctx->fb_w != width || ctx->fb_h != height) return fail(VXA_ERR_INVALID, "framebuffer size mismatch");
+    const uint32_t tiles = tiles_of(width, height, rank, world);
+    const uint64_t n = uint64_t{tiles} * kSuper * kSuper;
+    if (n == 0) return VXA_OK;
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    tiles_copy<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->fb.ptr, static_cast<uint32_t*>(buf), width, height, super_tiles_x(width), rank, world, tiles, pack);
+    VXA_CUDA(cudaGetLastError());
+    return VXA_OK;
+}
+} // namespace
+
+int vxa_tiles_count(int32_t width, int32_t height, int32_t rank, int32_t world, uint32_t* count) {
+    if (count == nullptr || width < 1 || height < 1 || world < 1 || rank < 0 || rank >= world)
+        return fail(VXA_ERR_INVALID, "bad frame size or partition");
+    *count = tiles_of(width, height, rank, world);
+    return VXA_OK;
+}
+
+int vxa_tiles_pack(vxa_ctx* ctx, int32_t width, int32_t height, int32_t rank, int32_t world, void* dst_device) {
+    return tiles_move(ctx, width, height, rank, world, dst_device, true);
+}
+
+int vxa_tiles_unpack(vxa_ctx* ctx, int32_t width, int32_t height, int32_t rank, int32_t world, const void* src_device) {
+    return tiles_move(ctx, width, height, rank, world, const_cast<void*>(src_device), false);
 }
 
 int vxa_traverse(vxa_ctx* ctx, uint32_t model, const vxa_local_ray* rays, uint32_t n, uint32_t precision,

@@ -16,16 +16,22 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_two_ranks_compose_the_single_device_frame(gpu):
+@pytest.mark.parametrize("compose,port", [("ipc", 29531), ("gather", 29532)])
+def test_two_ranks_compose_the_single_device_frame(gpu, compose, port):
+    """ipc: peer stores into rank 0's framebuffer; gather: the fallback without
+    CUDA IPC (tiles packed per rank, collective gather, unpacked on rank 0)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--same-device", "--no-cpu-baseline", "--no-extras"]
-    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    env = dict(os.environ)
+    if compose == "gather":
+        env["VOXANIM_COMPOSE"] = "gather"
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, res.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2
-    assert d["config"]["composition"].startswith("NVLink peer stores")
+    assert d["config"]["composition"].startswith("NVLink peer stores" if compose == "ipc" else "collective gather")
     assert d["multi_gpu_frame_identical"] is True
     assert d["e2e"] is not None and d["e2e"]["value"] > 0
