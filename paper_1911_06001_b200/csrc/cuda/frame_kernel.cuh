@@ -28,6 +28,9 @@ constexpr int kBlock = 128;
 #ifndef VXA_MIN_BLOCKS
 #define VXA_MIN_BLOCKS 8
 #endif
+#ifndef VXA_ZERO_SPLIT
+#define VXA_ZERO_SPLIT 1
+#endif
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kListCap = 64;
 struct BlockStack : SmemStack<kBlock * sizeof(uint2)> {
@@ -110,19 +113,20 @@ __device__ __forceinline__ SphereRes<Real> sphere_of(const FrameParams<Real>& p,
 // in FP64 and rounded once: a plane entry t = (A + i s) / d_a is only as
 // accurate as the small component d_a.
 struct RayD {
-    double dcx, dcy; // camera-space direction (z = -1), reference NDC arithmetic
+    double dcx, dcy; // camera-space direction (z = -1)
     double rnd;      // 1 / |(dcx, dcy, -1)|
 };
 
-// FP64 camera-space direction of pixel (px, py) with the reference's NDC
-// arithmetic (renderer.cpp:19-21, divisions included): a centre row/column
-// yields an exact 0 like the reference does, so zero-direction rays stay zero.
+// FP64 camera-space direction of pixel (px, py): the reference's NDC
+// (renderer.cpp:19-21) is ((px + 0.5) / W) * 2 - 1 = (2 px + 1 - W) / W. The
+// numerator is an exact integer, so a component is exactly zero iff the
+// reference's is (its quotient is never within an ulp of 0.5 otherwise: the
+// distance is >= 1/2W), and zero-direction rays stay zero; elsewhere the value
+// is within a few FP64 ulp of the reference's, far below the FP32 rounding.
 template <typename Real>
 __device__ __forceinline__ void camera_dir_f64(const FrameParams<Real>& p, int px, int py, RayD& rd) {
-    const double ndc_x = (px + 0.5) / p.width * 2.0 - 1.0;
-    const double ndc_y = 1.0 - (py + 0.5) / p.height * 2.0;
-    rd.dcx = ndc_x * p.d_sy * p.d_aspect;
-    rd.dcy = ndc_y * p.d_sy;
+    rd.dcx = static_cast<double>(2 * px + 1 - p.width) * p.d_kx;
+    rd.dcy = static_cast<double>(p.height - 2 * py - 1) * p.d_ky;
     rd.rnd = rsqrt(fma(rd.dcx, rd.dcx, fma(rd.dcy, rd.dcy, 1.0)));
 }
 
@@ -146,16 +150,20 @@ __device__ __forceinline__ TileCone region_cone(const FrameParams<Real>& p, int 
     const float cys = fmaf(-(static_cast<float>(y0) + 0.5f * h), inv_h2, 1.0f) * sy;
     const float cn = rsqrtf(cxs * cxs + cys * cys + 1.0f);
     const float ax = cxs * cn, ay = cys * cn, az = -cn;
-    float smax = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float xs = fmaf(static_cast<float>(x0) + ((k & 1) ? w - 0.5f : 0.5f), inv_w2, -1.0f) * sx;
-        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2) ? h - 0.5f : 0.5f)), inv_h2, 1.0f) * sy;
+    // the four corner rays, one per lane (lane & 3; the whole warp calls this),
+    // combined by a two-step butterfly max
+    float smax;
+    {
+        const uint32_t k = threadIdx.x & 3u;
+        const float xs = fmaf(static_cast<float>(x0) + ((k & 1u) ? w - 0.5f : 0.5f), inv_w2, -1.0f) * sx;
+        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2u) ? h - 0.5f : 0.5f)), inv_h2, 1.0f) * sy;
         const float n = rsqrtf(xs * xs + ys * ys + 1.0f);
         const float bx = xs * n, by = ys * n, bz = -n;
         // |a x b| = sin of the angle (accurate for small angles, unlike 1 - cos)
         const float cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
-        smax = fmaxf(smax, sqrtf(cx * cx + cy * cy + cz * cz));
+        smax = sqrtf(cx * cx + cy * cy + cz * cz);
+        smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, 1));
+        smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, 2));
     }
     TileCone c;
     c.sin_a = fminf(1.0f, smax * 1.01f + 1e-6f);
@@ -226,13 +234,14 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
             double qq = 0.0, qw = 0.0, ww = 0.0;
             for (int k = 0; k < 3; ++k) {
                 const double q = -(static_cast<double>(in.U_lo[k]) + static_cast<double>(in.Ur_lo[k])) - 0.5;
-                const double w = dd[k] / static_cast<double>(in.h2[k]);
+                const double w = dd[k] * in.ih2[k];
                 qq = fma(q, q, qq);
                 qw = fma(q, w, qw);
                 ww = fma(w, w, ww);
             }
+            // squared line distance qq - qw^2/ww > r2, without the division (ww > 0)
             const double r2 = static_cast<double>(in.model.content_r2);
-            if (qq - qw * qw / ww > r2 || (qw > 0.0 && qq > r2)) return;
+            if (fma(qq, ww, -qw * qw) > r2 * ww || (qw > 0.0 && qq > r2)) return;
         }
         FastRay fr;
         // Only a hit at t <= best.t can change the nearest (t, id) (ties go to
@@ -250,7 +259,16 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
                     nodes.top_n = p.top_n;
                 }
             }
+#if VXA_ZERO_SPLIT
+            // rays with a zero local direction component are rare: they take the
+            // general copy, every other ray a loop without the zero conventions
+            if (fr.zero)
+                hit = traverse_fast<kAov, true>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+            else
+                hit = traverse_fast<kAov, false>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+#else
             hit = traverse_fast<kAov>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+#endif
         }
         else
             hit = traverse_fast<kAov>(WideNodes{in.model.words, in.model.side}, static_cast<int>(in.model.depth), fr, h,

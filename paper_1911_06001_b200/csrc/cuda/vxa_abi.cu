@@ -267,6 +267,7 @@ void fold_instance(const std::map<uint32_t, ModelEntry>& models, const vxa_frame
         d.A_lo[a] = static_cast<Real>(-h[a] - ol[a]);
         d.A_hi[a] = static_cast<Real>(h[a] - ol[a]);
         d.h2[a] = static_cast<Real>(2.0 * h[a]);
+        d.ih2[a] = 1.0 / (2.0 * h[a]);
         // FP32 kernel: unit-cube plane offsets (-h - o) / 2h, (h - o) / 2h + residuals
         const double ulo = (-h[a] - ol[a]) / (2.0 * h[a]), uhi = (h[a] - ol[a]) / (2.0 * h[a]);
         d.U_lo[a] = static_cast<float>(ulo);
@@ -344,8 +345,8 @@ template <typename Real> void fill_camera(FrameParams<Real>& p, const vxa_frame_
     p.inv_h2 = static_cast<Real>(2.0 / c.height);
     p.sx = static_cast<Real>(tan_half * aspect);
     p.sy = static_cast<Real>(tan_half);
-    p.d_sy = tan_half;
-    p.d_aspect = aspect;
+    p.d_kx = tan_half * aspect / c.width;
+    p.d_ky = tan_half / c.height;
     p.width = c.width;
     p.height = c.height;
 }

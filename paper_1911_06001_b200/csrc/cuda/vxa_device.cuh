@@ -35,7 +35,18 @@ constexpr uint32_t kMixed = 1u << 16;
 
 // Work decomposition: 8x4-pixel warp tiles inside 64x64 super-tiles; super-tiles
 // are the unit of the multi-GPU screen partition.
-constexpr int kTileW = 8, kTileH = 4;
+#ifndef VXA_TILE_W
+#define VXA_TILE_W 8
+#endif
+// Traversal pops: 2 = jump to the deepest ancestor with children
+// left (a bit mask of live saved frames; exhausted frames are never stored) and
+// rebuild its planes from its cell; 1 = the same, finding the ancestor by
+// unwinding saved frames; 0 = one level per iteration, rebuilding one plane per
+// axis from the child's interval.
+#ifndef VXA_MULTI_POP
+#define VXA_MULTI_POP 2
+#endif
+constexpr int kTileW = VXA_TILE_W, kTileH = 32 / VXA_TILE_W;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
 // Scenes with more instances than this get the per-super-tile culling pre-pass.
@@ -81,6 +92,7 @@ struct WideNodes {
     const uint2* w;
     const uint32_t* side;
     using Word = uint2;
+    static constexpr bool kLastLevelLeaves = false;
     __device__ __forceinline__ Word load(uint32_t i) const { return __ldg(w + i); }
     __device__ __forceinline__ static uint32_t valid(Word x) { return x.x & 0xffu; }
     __device__ __forceinline__ static uint32_t leaves(Word x, int /*level*/, int /*depth*/) { return (x.x >> 8) & 0xffu; }
@@ -104,6 +116,7 @@ struct CompactNodes {
     uint32_t top_base = 0; // shared address of the staged words (VXA_SMEM_TOP builds)
     uint32_t top_n = 0;    // words staged for this model (0: none)
     using Word = uint32_t;
+    static constexpr bool kLastLevelLeaves = true; // leaves exist on the last level only
     __device__ __forceinline__ Word load(uint32_t i) const {
         if constexpr (VXA_SMEM_TOP > 0) {
             if (i < top_n) {
@@ -142,6 +155,7 @@ template <typename Real> struct DevInstance {
     float U_lo[3], U_hi[3];   // FP32 kernel: (-h - o) / 2h, (h - o) / 2h (unit-cube plane offsets)
     float Ur_lo[3], Ur_hi[3]; // and their FP64 rounding residuals
     double Md[9]; // FP64 R^T C (camera -> local), FP32 kernel's local direction
+    double ih2[3]; // 1 / 2h: local direction -> unit-cube direction (content-sphere test)
     uint32_t zbits[3]; // zero-direction path: bit L set iff o >= centre at level L
     uint32_t zflags;   // bit a: (-h > o); bit 3+a: (h > o)   (zero-direction slab signs)
     int32_t id;
@@ -173,7 +187,7 @@ template <typename Real> struct FrameParams {
     Real aspect;       // (double)W / H
     Real inv_w2, inv_h2; // FP32 ray setup: 2/W, 2/H
     Real sx, sy;       // FP32 ray setup: tan_half * aspect, tan_half
-    double d_sy, d_aspect; // tan_half and aspect in FP64 (FP32 kernel's local directions)
+    double d_kx, d_ky; // tan_half * aspect / W, tan_half / H in FP64 (FP32 kernel's camera directions)
     uint32_t background; // RGBA8
     uint32_t culling, sorting, sphere_pass;
     uint32_t camera_dirty;
@@ -574,8 +588,10 @@ struct LocalStack {
 // Iterative traversal. The explicit stack holds only ancestor node words
 // (bits 24..27 of .x: the saved next octant) in the caller's stack column
 // (shared memory, [level][thread]); t0/tm/t1 of a parent are rebuilt on a
-// pop from the child's interval plus one plane per axis.
-template <bool kTrackIdx, class Nodes, class Stack>
+// pop from the child's interval plus one plane per axis. kZero = false: the
+// caller guarantees no zero direction component (r.zero == 0), so the
+// zero-direction conventions compile out of the loop.
+template <bool kTrackIdx, bool kZero = true, class Nodes, class Stack>
 __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay& r, FastHit& out, Stack& stack) {
     uint32_t sidx[kTrackIdx ? kMaxDepth : 1]; // ancestor indices (AOV: leaf parent)
     float c[3] = {0.0f, 0.0f, 0.0f};          // cell coordinates (exact integers)
@@ -587,15 +603,57 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         t1[a] = plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]);
         tm[a] = plane_t(1.0f, 0.5f, r.A[a], r.Ar[a], r.inv[a]);
     }
-    if (r.zero) fix_zero_axes(r, 0, t0, tm, t1);
+    if (kZero && r.zero) fix_zero_axes(r, 0, t0, tm, t1);
     typename Nodes::Word fw = nodes.load(0);
     uint32_t fidx = 0, fetches = 1;
     uint32_t fcur = first_child(t0, tm);
     int level = 0;
     const int depth = min(model_depth, static_cast<int>(kMaxDepth));
+#if VXA_MULTI_POP == 2
+    uint32_t live = 0;
+#endif
 
     while (true) {
         if (fcur == kExit) {
+#if VXA_MULTI_POP
+            // Pop every ancestor whose remaining children are exhausted (saved
+            // next octant == exit) in one go, then rebuild the surviving
+            // frame's planes directly from its cell coordinates: a plane's t
+            // depends only on its position (i * sz exact), so the values equal
+            // the ones computed on the way down bit for bit.
+#if VXA_MULTI_POP == 2
+            // live: bit L set iff the frame saved at level L has children left
+            // (only those frames are stored), so the target is its highest bit
+            const uint32_t m = live & ((1u << level) - 1u);
+            if (m == 0) break; // every ancestor is exhausted: miss
+            const int lv = 31 - __clz(m);
+            live = m & ~(1u << lv);
+            fw = Nodes::unpack(stack.load(lv), fcur);
+#else
+            int lv = level;
+            do {
+                if (lv == 0) break;
+                --lv;
+                fw = Nodes::unpack(stack.load(lv), fcur);
+            } while (fcur == kExit);
+            if (fcur == kExit) break; // the root is exhausted: miss
+#endif
+            // 2^-(levels popped) as float bits (exact power of two)
+            const float shrink = __int_as_float((127 - (level - lv)) << 23);
+            level = lv;
+            if constexpr (kTrackIdx) fidx = sidx[level];
+            sz = __int_as_float((127 - level) << 23); // 2^-level
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float cn = floorf(c[a] * shrink);
+                c[a] = cn;
+                t0[a] = plane_t(cn, sz, r.A[a], r.Ar[a], r.inv[a]);
+                t1[a] = plane_t(cn + 1.0f, sz, r.A[a], r.Ar[a], r.inv[a]);
+                tm[a] = plane_t(__fmaf_rn(2.0f, cn, 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
+            }
+            if (kZero && r.zero) fix_zero_axes(r, level, t0, tm, t1);
+            continue;
+#else
             if (level == 0) break;
             --level;
             fw = Nodes::unpack(stack.load(level), fcur);
@@ -613,8 +671,9 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
                 t0[a] = upper ? outer : t0[a];
                 t1[a] = upper ? t1[a] : outer;
             }
-            if (r.zero) fix_zero_axes(r, level, t0, tm, t1);
+            if (kZero && r.zero) fix_zero_axes(r, level, t0, tm, t1);
             continue;
+#endif
         }
         const uint32_t q = fcur;
         float c1[3];
@@ -644,9 +703,18 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         // the reference cull !(t_enter < t_exit) || t_exit < 0, plus the pruning
         // bound (t_enter >= t_lim: nothing in this child can beat the best)
         if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
-        const uint32_t leafm = Nodes::leaves(fw, level, depth);
-        if (leafm & bit) {
-            out.attr = nodes.attr_base(fw) + popc8_below(valid & leafm, bit);
+        // compact words: a (valid) child is a leaf exactly on the last level
+        bool is_leaf;
+        uint32_t leafm;
+        if constexpr (Nodes::kLastLevelLeaves) {
+            is_leaf = level + 1 == depth;
+            leafm = is_leaf ? valid : 0u;
+        } else {
+            leafm = Nodes::leaves(fw, level, depth);
+            is_leaf = (leafm & bit) != 0;
+        }
+        if (is_leaf) {
+            out.attr = nodes.attr_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & leafm, bit);
             out.t = fmaxf(t_enter, 0.0f);
             out.parent = fidx;
             out.level = static_cast<uint32_t>(level + 1);
@@ -665,9 +733,19 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             }
             return true;
         }
-        if (level + 1 >= depth) continue;
-        const uint32_t child = Nodes::child_base(fw) + popc8_below(valid & ~leafm, bit);
+        if constexpr (!Nodes::kLastLevelLeaves) {
+            if (level + 1 >= depth) continue;
+        }
+        const uint32_t child =
+            Nodes::child_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & ~leafm, bit);
+#if VXA_MULTI_POP == 2
+        if (fcur != kExit) {
+            live |= 1u << level;
+            stack.store(level, Nodes::pack(fw, fcur));
+        }
+#else
         stack.store(level, Nodes::pack(fw, fcur));
+#endif
         if constexpr (kTrackIdx) {
             sidx[level] = fidx;
             fidx = child;
@@ -683,7 +761,7 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             t1[a] = c1[a];
             tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
         }
-        if (r.zero) {
+        if (kZero && r.zero) {
 #pragma unroll
             for (int a = 0; a < 3; ++a)
                 if (r.zero & axis_bit(a)) tm[a] = zero_mid(r, a, level);

@@ -1,8 +1,9 @@
 """Print the key fields of gpurun_out/bench*.log lines (helper for A/B runs)."""
 import glob
 import json
+import sys
 
-for f in sorted(glob.glob("gpurun_out/bench*.log")):
+for f in sys.argv[1:] or sorted(glob.glob("gpurun_out/bench*.log")):
     for line in open(f):
         if line.startswith("{"):
             d = json.loads(line)
