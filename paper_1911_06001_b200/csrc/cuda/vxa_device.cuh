@@ -623,11 +623,12 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             // the ones computed on the way down bit for bit.
 #if VXA_MULTI_POP == 2
             // live: bit L set iff the frame saved at level L has children left
-            // (only those frames are stored), so the target is its highest bit
-            const uint32_t m = live & ((1u << level) - 1u);
-            if (m == 0) break; // every ancestor is exhausted: miss
-            const int lv = 31 - __clz(m);
-            live = m & ~(1u << lv);
+            // (only those frames are stored; bits >= level are never set), so
+            // the target is its highest bit
+            if (live == 0) break; // every ancestor is exhausted: miss
+            int lv;
+            asm("bfind.u32 %0, %1;" : "=r"(lv) : "r"(live));
+            live ^= 1u << lv;
             fw = Nodes::unpack(stack.load(lv), fcur);
 #else
             int lv = level;
