@@ -38,14 +38,6 @@ constexpr uint32_t kMixed = 1u << 16;
 #ifndef VXA_TILE_W
 #define VXA_TILE_W 8
 #endif
-// Traversal pops: 2 = jump to the deepest ancestor with children
-// left (a bit mask of live saved frames; exhausted frames are never stored) and
-// rebuild its planes from its cell; 1 = the same, finding the ancestor by
-// unwinding saved frames; 0 = one level per iteration, rebuilding one plane per
-// axis from the child's interval.
-#ifndef VXA_MULTI_POP
-#define VXA_MULTI_POP 2
-#endif
 constexpr int kTileW = VXA_TILE_W, kTileH = 32 / VXA_TILE_W;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
@@ -585,12 +577,24 @@ struct LocalStack {
     __device__ __forceinline__ void store(int level, uint2 v) { a[level] = v; }
 };
 
-// Iterative traversal. The explicit stack holds only ancestor node words
-// (bits 24..27 of .x: the saved next octant) in the caller's stack column
-// (shared memory, [level][thread]); t0/tm/t1 of a parent are rebuilt on a
-// pop from the child's interval plus one plane per axis. kZero = false: the
-// caller guarantees no zero direction component (r.zero == 0), so the
-// zero-direction conventions compile out of the loop.
+// Iterative traversal. Every iteration steps one child of the current frame
+// (t0/tm/t1 of the node and its cell in registers):
+//   * step: the child's exit plane (argmin t1, x first) gives the next octant,
+//     or exit -- encoded as fcur >= kExit (q | xb plus 8 xb when the exit
+//     axis bit is already set, one integer multiply-add instead of a select);
+//   * push: a valid, uncut, internal child becomes the frame. The parent is
+//     saved only while it has children left (its word and next octant in the
+//     caller's stack column, bit `level` of `live`), so exhausted ancestors
+//     are never stored;
+//   * pop: when the frame's next is exit, the deepest live ancestor (the
+//     highest bit of `live`, bfind) becomes the frame in one jump and its
+//     planes are rebuilt from its cell -- a plane's t depends on its position
+//     only (plane_t), so the values are the ones the descent computed, bit
+//     for bit -- and its saved next child is stepped in the same iteration, so
+//     a pop costs its lane no extra iteration (SIMT: fewer iterations for the
+//     lanes that pop the most).
+// kZero = false: the caller guarantees no zero direction component
+// (r.zero == 0), so the zero-direction conventions compile out of the loop.
 template <bool kTrackIdx, bool kZero = true, class Nodes, class Stack>
 __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay& r, FastHit& out, Stack& stack) {
     uint32_t sidx[kTrackIdx ? kMaxDepth : 1]; // ancestor indices (AOV: leaf parent)
@@ -609,38 +613,17 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
     uint32_t fcur = first_child(t0, tm);
     int level = 0;
     const int depth = min(model_depth, static_cast<int>(kMaxDepth));
-#if VXA_MULTI_POP == 2
-    uint32_t live = 0;
-#endif
+    uint32_t live = 0; // bit L: the frame saved at level L has children left (only bits < level)
 
     while (true) {
-        if (fcur == kExit) {
-#if VXA_MULTI_POP
-            // Pop every ancestor whose remaining children are exhausted (saved
-            // next octant == exit) in one go, then rebuild the surviving
-            // frame's planes directly from its cell coordinates: a plane's t
-            // depends only on its position (i * sz exact), so the values equal
-            // the ones computed on the way down bit for bit.
-#if VXA_MULTI_POP == 2
-            // live: bit L set iff the frame saved at level L has children left
-            // (only those frames are stored; bits >= level are never set), so
-            // the target is its highest bit
+        if (fcur >= kExit) {
+            // pop to the deepest live ancestor
             if (live == 0) break; // every ancestor is exhausted: miss
             int lv;
             asm("bfind.u32 %0, %1;" : "=r"(lv) : "r"(live));
             live ^= 1u << lv;
             fw = Nodes::unpack(stack.load(lv), fcur);
-#else
-            int lv = level;
-            do {
-                if (lv == 0) break;
-                --lv;
-                fw = Nodes::unpack(stack.load(lv), fcur);
-            } while (fcur == kExit);
-            if (fcur == kExit) break; // the root is exhausted: miss
-#endif
-            // 2^-(levels popped) as float bits (exact power of two)
-            const float shrink = __int_as_float((127 - (level - lv)) << 23);
+            const float shrink = __int_as_float((127 - (level - lv)) << 23); // 2^-(levels popped)
             level = lv;
             if constexpr (kTrackIdx) fidx = sidx[level];
             sz = __int_as_float((127 - level) << 23); // 2^-level
@@ -653,28 +636,7 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
                 tm[a] = plane_t(__fmaf_rn(2.0f, cn, 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
             }
             if (kZero && r.zero) fix_zero_axes(r, level, t0, tm, t1);
-            continue;
-#else
-            if (level == 0) break;
-            --level;
-            fw = Nodes::unpack(stack.load(level), fcur);
-            if constexpr (kTrackIdx) fidx = sidx[level];
-            sz = 2.0f * sz;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                // the child shares tm and one outer plane with the parent; only the
-                // other outer plane is recomputed (branch-free: one plane per axis)
-                const float cp = floorf(0.5f * c[a]);
-                const bool upper = c[a] != 2.0f * cp; // the child was the upper half
-                c[a] = cp;
-                const float outer = plane_t(upper ? cp : cp + 1.0f, sz, r.A[a], r.Ar[a], r.inv[a]);
-                tm[a] = upper ? t0[a] : t1[a];
-                t0[a] = upper ? outer : t0[a];
-                t1[a] = upper ? t1[a] : outer;
-            }
-            if (kZero && r.zero) fix_zero_axes(r, level, t0, tm, t1);
-            continue;
-#endif
+            // (falls through: the ancestor's saved next child is stepped now)
         }
         const uint32_t q = fcur;
         float c1[3];
@@ -685,7 +647,7 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
         {
             const uint32_t xb = c1[0] == t_exit ? 4u : (c1[1] == t_exit ? 2u : 1u);
-            fcur = (q & xb) ? kExit : (q | xb);
+            fcur = (q | xb) + ((q & xb) << 3); // >= kExit iff the exit axis bit is already set
         }
         // An absent child is skipped before its interval is evaluated: the
         // reference culls first and checks node_child second, but both only
@@ -737,16 +699,13 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         if constexpr (!Nodes::kLastLevelLeaves) {
             if (level + 1 >= depth) continue;
         }
+        // push: save the parent only while it has children left
         const uint32_t child =
             Nodes::child_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & ~leafm, bit);
-#if VXA_MULTI_POP == 2
-        if (fcur != kExit) {
+        if (fcur < kExit) {
             live |= 1u << level;
             stack.store(level, Nodes::pack(fw, fcur));
         }
-#else
-        stack.store(level, Nodes::pack(fw, fcur));
-#endif
         if constexpr (kTrackIdx) {
             sidx[level] = fidx;
             fidx = child;
