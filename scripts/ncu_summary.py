@@ -30,7 +30,8 @@ METRICS = {
     "grid": ("launch__grid_size", None),
     "block": ("launch__block_size", None),
 }
-SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}
+SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+         "nsecond": 1e-6, "ns": 1e-6}
 
 
 def summarise(rep: str) -> dict:
