@@ -37,6 +37,12 @@ struct BlockStack : SmemStack<kBlock * sizeof(uint2)> {
     uint32_t base_top; // shared address of the staged top node words (VXA_SMEM_TOP)
 }; // per-warp tile candidate list (bit positions of a u64 mask)
 
+// Super-tile row of super-tile s: s / n_super_x by a multiply-high when the
+// host found the magic exact for every super-tile of the frame (vxa_abi.cu).
+template <typename Real> __device__ __forceinline__ uint32_t super_row(const FrameParams<Real>& p, uint32_t s) {
+    return p.super_x_magic ? __umulhi(s, p.super_x_magic) : s / p.n_super_x;
+}
+
 template <typename Real> struct Best {
     bool have;
     bool pos_dir; // the unmirrored local direction is positive on the entry axis
@@ -369,8 +375,9 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         if (tile >= p.n_tiles) break;
         const uint32_t st = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
-        const int tx0 = static_cast<int>((s % p.n_super_x) * kSuper + (wt % (kSuper / kTileW)) * kTileW);
-        const int ty0 = static_cast<int>((s / p.n_super_x) * kSuper + (wt / (kSuper / kTileW)) * kTileH);
+        const uint32_t sy = super_row(p, s), sx = s - sy * p.n_super_x;
+        const int tx0 = static_cast<int>(sx * kSuper + (wt % (kSuper / kTileW)) * kTileW);
+        const int ty0 = static_cast<int>(sy * kSuper + (wt / (kSuper / kTileW)) * kTileH);
         const int px = tx0 + static_cast<int>(lane % kTileW);
         const int py = ty0 + static_cast<int>(lane / kTileW);
 
@@ -619,7 +626,8 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (st >= n_mine) return;
     const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
-    const int x0 = static_cast<int>((s % p.n_super_x) * kSuper), y0 = static_cast<int>((s / p.n_super_x) * kSuper);
+    const uint32_t sy = super_row(p, s);
+    const int x0 = static_cast<int>((s - sy * p.n_super_x) * kSuper), y0 = static_cast<int>(sy * kSuper);
     const float w = static_cast<float>(min(kSuper, p.width - x0)), h = static_cast<float>(min(kSuper, p.height - y0));
     const TileCone cone = region_cone(p, x0, y0, w, h);
     uint16_t* out = list + static_cast<size_t>(st) * p.super_cap;

@@ -416,6 +416,15 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.rank = f->tile_rank;
     p.world = f->tile_world;
     p.n_super_x = super_tiles_x(W);
+    {
+        // multiply-high division by n_super_x, exact for every super-tile index
+        // s < n_super when s * (magic * n - 2^32) < 2^32; else 0 (plain division)
+        const uint64_t n = p.n_super_x, n_super_all = n * static_cast<uint64_t>((H + kSuper - 1) / kSuper);
+        const uint64_t m = ((uint64_t{1} << 32) + n - 1) / n, e = m * n - (uint64_t{1} << 32);
+        p.super_x_magic = (n > 1 && m < (uint64_t{1} << 32) && (n_super_all - 1) * e < (uint64_t{1} << 32))
+                              ? static_cast<uint32_t>(m)
+                              : 0u;
+    }
     const uint32_t n_super = p.n_super_x * static_cast<uint32_t>((H + kSuper - 1) / kSuper);
     const uint32_t mine = (n_super + static_cast<uint32_t>(f->tile_world - f->tile_rank) - 1) / static_cast<uint32_t>(f->tile_world);
     p.n_tiles = mine * static_cast<uint32_t>(kTilesPerSuper);

@@ -186,6 +186,7 @@ template <typename Real> struct FrameParams {
     // partition
     int32_t rank, world;
     uint32_t n_super_x;
+    uint32_t super_x_magic; // ceil(2^32 / n_super_x): s / n_super_x = umulhi(s, magic) for s < 2^16
     uint32_t n_tiles; // warp tiles owned by this rank
     uint32_t max_depth; // deepest model of the frame (FP32 shared-memory stack height)
     uint32_t compact;   // every model has compact 4-byte words (FP32 kernel)
@@ -598,7 +599,7 @@ struct LocalStack {
 template <bool kTrackIdx, bool kZero = true, class Nodes, class Stack>
 __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay& r, FastHit& out, Stack& stack) {
     uint32_t sidx[kTrackIdx ? kMaxDepth : 1]; // ancestor indices (AOV: leaf parent)
-    float c[3] = {0.0f, 0.0f, 0.0f};          // cell coordinates (exact integers)
+    float c[3] = {1.0f, 1.0f, 1.0f};          // 2 cell + 1: the node's midplane index in half cells (exact)
     float sz = 1.0f;                          // cell size 2^-level
     float t0[3], tm[3], t1[3];
 #pragma unroll
@@ -629,11 +630,13 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             sz = __int_as_float((127 - level) << 23); // 2^-level
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const float cn = floorf(c[a] * shrink);
-                c[a] = cn;
+                // cell = (c - 1) / 2, ancestor cell = floor(cell * shrink), both exact
+                const float hs = 0.5f * shrink;
+                const float cn = floorf(__fmaf_rn(c[a], hs, -hs));
+                c[a] = __fmaf_rn(2.0f, cn, 1.0f);
+                tm[a] = plane_t(c[a], 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
                 t0[a] = plane_t(cn, sz, r.A[a], r.Ar[a], r.inv[a]);
                 t1[a] = plane_t(cn + 1.0f, sz, r.A[a], r.Ar[a], r.inv[a]);
-                tm[a] = plane_t(__fmaf_rn(2.0f, cn, 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
             }
             if (kZero && r.zero) fix_zero_axes(r, level, t0, tm, t1);
             // (falls through: the ancestor's saved next child is stepped now)
@@ -691,7 +694,7 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
             const uint32_t top = (2u << level) - 1u; // 2^(level+1) - 1
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const uint32_t v = 2u * static_cast<uint32_t>(c[a]) + ((q >> (2 - a)) & 1u);
+                const uint32_t v = static_cast<uint32_t>(c[a]) - 1u + ((q >> (2 - a)) & 1u);
                 out.vox[a] = (r.mirror & axis_bit(a)) ? top - v : v;
             }
             return true;
@@ -716,10 +719,11 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
         sz = 0.5f * sz;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            c[a] = __fmaf_rn(2.0f, c[a], (q & axis_bit(a)) ? 1.0f : 0.0f);
+            // child midplane index: 2 (2 cell + b) + 1 = 2 c + 2 b - 1
+            c[a] = __fmaf_rn(2.0f, c[a], (q & axis_bit(a)) ? 1.0f : -1.0f);
+            tm[a] = plane_t(c[a], 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
             t0[a] = c0[a];
             t1[a] = c1[a];
-            tm[a] = plane_t(__fmaf_rn(2.0f, c[a], 1.0f), 0.5f * sz, r.A[a], r.Ar[a], r.inv[a]);
         }
         if (kZero && r.zero) {
 #pragma unroll
