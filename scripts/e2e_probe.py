@@ -13,11 +13,11 @@ steps = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 lib, vxl, ctx = vx.vxa(), vx.voxanim(), vx.context()
 sc = vx.Scene(vx.config.C4, [vx.Model.procedural(11, shell=True)])
 W, H = sc.width, sc.height
-bufs = [np.empty((H, W, 3), np.uint8) for _ in range(2)]
+bufs = [np.empty((H, W, 3), np.uint8) for _ in range(3)]
 for b in bufs:
     lib.vxa_host_register(ctx, b.ctypes.data, b.nbytes)
 t = C.c_uint64()
-for mode in ("stream", "submit_only"):
+for mode in ("stream", "stream3", "submit_only"):
     tickets = []
     for k in range(5):
         vxl.vxn_scene_stream(sc._h, k / 30.0, vx.VXA_FP32, bufs[k % 2].ctypes.data, C.byref(t))
@@ -25,17 +25,33 @@ for mode in ("stream", "submit_only"):
     lib.vxa_stats_reset(ctx)
     t0 = time.perf_counter()
     for k in range(steps):
-        if mode == "stream":
-            vxl.vxn_scene_stream(sc._h, k / 30.0, vx.VXA_FP32, bufs[k % 2].ctypes.data, C.byref(t))
+        if mode.startswith("stream"):
+            depth = 3 if mode == "stream3" else 2  # host images in flight
+            vxl.vxn_scene_stream(sc._h, k / 30.0, vx.VXA_FP32, bufs[k % depth].ctypes.data, C.byref(t))
             tickets.append(t.value)
-            if len(tickets) >= 2:
-                lib.vxa_wait_readback(ctx, tickets[-2])
+            if len(tickets) >= depth:
+                lib.vxa_wait_readback(ctx, tickets[-depth])
         else:
             vxl.vxn_scene_submit(sc._h, k / 30.0, vx.VXA_FP32, 0, 1, 0)
-    if mode == "stream":
+    if mode.startswith("stream"):
         lib.vxa_wait_readback(ctx, tickets[-1])
     lib.vxa_synchronize(ctx)
     el = (time.perf_counter() - t0) * 1e3 / steps
     st = _abi.vxa_stats()
     lib.vxa_stats_read(ctx, C.byref(st))
     print(f"{mode:12s} wall {el:.4f} ms/step   frame kernels {st.gpu_ms / st.frames:.4f} ms/frame ({st.frames} frames)")
+
+# D2H bandwidth of one RGB8 frame into page-locked host memory (torch, for reference)
+import torch
+
+src = torch.empty(W * H * 3, dtype=torch.uint8, device="cuda")
+dst = torch.empty(W * H * 3, dtype=torch.uint8, pin_memory=True)
+for _ in range(3):
+    dst.copy_(src, non_blocking=True)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(20):
+    dst.copy_(src, non_blocking=True)
+torch.cuda.synchronize()
+el = (time.perf_counter() - t0) / 20
+print(f"D2H {W * H * 3 / 1e6:.1f} MB: {el * 1e3:.3f} ms ({W * H * 3 / el / 1e9:.1f} GB/s)")
