@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= p.n_tiles) break;
-        const uint32_t st = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
+        const uint32_t st_k = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
+        const uint32_t st = p.super_order != nullptr ? __ldg(p.super_order + st_k) : st_k;
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
         const uint32_t sy = super_row(p, s), sx = s - sy * p.n_super_x;
         const int tx0 = static_cast<int>(sx * kSuper + (wt % (kSuper / kTileW)) * kTileW);
@@ -641,6 +642,32 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
         cnt += __popc(m);
     }
     if (lane == 0) count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
+}
+
+// Longest-first order of the rank's super-tiles for the frame kernel's work
+// queue: a counting sort (one block) by descending candidate count from the
+// pre-pass (overflowed lists first, empty ones last). Only the schedule
+// changes -- every pixel's arithmetic is the same -- so the grid's tail is made
+// of cheap tiles instead of whatever the screen order puts last.
+static __global__ void __launch_bounds__(1024) super_order_kernel(const uint32_t* __restrict__ count, uint32_t n,
+                                                          uint32_t* __restrict__ order) {
+    constexpr uint32_t kBuckets = 66; // overflow, 64 .. 0 candidates
+    __shared__ uint32_t start[kBuckets];
+    const auto bucket = [](uint32_t c) { return c == 0xffffffffu ? 0u : 65u - min(c, 64u); };
+    for (uint32_t b = threadIdx.x; b < kBuckets; b += blockDim.x) start[b] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[bucket(__ldg(count + i))], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t b = 0; b < kBuckets; ++b) {
+            const uint32_t c = start[b];
+            start[b] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(__ldg(count + i))], 1u)] = i;
 }
 
 } // namespace vxa

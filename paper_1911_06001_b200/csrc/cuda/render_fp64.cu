@@ -18,6 +18,8 @@ cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (n_mine == 0) return cudaSuccess;
     super_cull_kernel<double><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
+    if (p.super_order != nullptr)
+        super_order_kernel<<<1, 1024, 0, s>>>(count, n_mine, const_cast<uint32_t*>(p.super_order));
     return cudaGetLastError();
 }
 

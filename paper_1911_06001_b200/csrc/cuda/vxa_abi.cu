@@ -175,6 +175,7 @@ struct vxa_ctx {
     DevBuf<unsigned char> inst_dev;
     DevBuf<uint16_t> super_list;  // per-super-tile candidate lists (large scenes)
     DevBuf<uint32_t> super_count;
+    DevBuf<uint32_t> super_order; // longest-first super-tile order (VXA_LPT)
     int aux_launches = 0;         // pre-pass kernels since the last stats reset
     unsigned char* inst_host[2] = {nullptr, nullptr};
     size_t inst_host_cap = 0;
@@ -502,8 +503,12 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
         p.super_list = ctx->super_list.ptr;
         p.super_count = ctx->super_count.ptr;
         p.super_cap = kSuperCap;
+        if (VXA_LPT) {
+            VXA_CUDA(ctx->super_order.ensure(std::max<size_t>(mine_super, 1)));
+            p.super_order = ctx->super_order.ptr;
+        }
         e = launch_super_cull(p, ctx->super_list.ptr, ctx->super_count.ptr, ctx->stream);
-        ++ctx->aux_launches;
+        ctx->aux_launches += p.super_order != nullptr ? 2 : 1; // pre-pass (+ its order kernel)
     }
     if (e == cudaSuccess) {
         if constexpr (sizeof(Real) == 8)
@@ -647,6 +652,7 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->inst_dev.release();
     ctx->super_list.release();
     ctx->super_count.release();
+    ctx->super_order.release();
     ctx->aov.release();
     ctx->hbo.release();
     ctx->rgb.release();

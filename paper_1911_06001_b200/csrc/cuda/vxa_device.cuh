@@ -42,6 +42,10 @@ constexpr int kTileW = VXA_TILE_W, kTileH = 32 / VXA_TILE_W;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
 // Scenes with more instances than this get the per-super-tile culling pre-pass.
+// Longest-first super-tile order after the culling pre-pass (1) or screen order (0).
+#ifndef VXA_LPT
+#define VXA_LPT 1
+#endif
 #ifndef VXA_SUPER_MIN
 #define VXA_SUPER_MIN 32
 #endif
@@ -168,6 +172,9 @@ template <typename Real> struct FrameParams {
     const uint16_t* super_list;
     const uint32_t* super_count;
     uint32_t super_cap;
+    // Processing order of the rank-local super-tiles (super_order_kernel: most
+    // candidates first, so the grid's tail is cheap tiles), or null: natural order.
+    const uint32_t* super_order;
     const uint32_t* top_words; // compact words of the scene's single model, or null
     uint32_t top_n;            // words to stage (<= VXA_SMEM_TOP and the model size, multiple of 4)
     uint32_t n_inst;
