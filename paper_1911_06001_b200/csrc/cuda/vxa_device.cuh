@@ -377,11 +377,18 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
     int level = 0;
     unsigned long long path = 0;
     const int depth = static_cast<int>(m.depth);
+    // bit L: the frame saved at level L has children left (only those are
+    // saved). Popping straight to the deepest one skips exhausted ancestors,
+    // which the reference pops one by one with no other effect, and its saved
+    // next child is stepped in the same iteration (fall through) -- the same
+    // visits in the same order, fewer loop iterations (cf. traverse_fast).
+    uint32_t live = 0;
 
     while (true) {
         if (fcur == kExit) {
-            if (level == 0) break;
-            --level;
+            if (live == 0) break;
+            asm("bfind.u32 %0, %1;" : "=r"(level) : "r"(live));
+            live ^= 1u << level;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 f0[a] = st0[level][a];
@@ -390,7 +397,6 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
             fw = sw[level];
             fidx = sidx[level];
             fcur = scur[level];
-            continue;
         }
         const uint32_t q = fcur;
         Real c0[3], c1[3];
@@ -442,17 +448,23 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
         }
         if (level + 1 >= depth || level + 1 >= static_cast<int>(kMaxDepth)) continue;
         const uint32_t child = fw.y + popc8_below(valid & ~leafm, bit);
-        // push the current frame, descend
+        // push the current frame (only while it has children left), descend
+        if (fcur != kExit) {
+            live |= 1u << level;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                st0[level][a] = f0[a];
+                st1[level][a] = f1[a];
+            }
+            sw[level] = fw;
+            sidx[level] = fidx;
+            scur[level] = fcur;
+        }
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            st0[level][a] = f0[a];
-            st1[level][a] = f1[a];
             f0[a] = c0[a];
             f1[a] = c1[a];
         }
-        sw[level] = fw;
-        sidx[level] = fidx;
-        scur[level] = fcur;
         ++level;
         fidx = child;
         fw = load_node(m, child);
