@@ -172,7 +172,12 @@ struct vxa_ctx {
     DevBuf<uint32_t> tile_counter;
     DevBuf<unsigned long long> counters;
     unsigned long long* counters_host = nullptr; // pinned, 8 counters
-    DevBuf<unsigned char> inst_dev;
+    // Per-frame instance tables, double-buffered on the device: frame k+1's
+    // table is uploaded on upload_stream while frame k renders (the frame waits
+    // for inst_done, the upload for inst_free: the kernel two frames back).
+    DevBuf<unsigned char> inst_dev[2];
+    cudaStream_t upload_stream = nullptr;
+    cudaEvent_t inst_free[2] = {nullptr, nullptr};
     DevBuf<uint16_t> super_list;  // per-super-tile candidate lists (large scenes)
     DevBuf<uint32_t> super_count;
     DevBuf<uint32_t> super_order; // longest-first super-tile order (VXA_LPT)
@@ -386,10 +391,13 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     const size_t cull_bytes = size_t{n} * sizeof(float4); // tile culling (both kernels)
     const size_t bytes = inst_bytes + cull_bytes;
     if (int rc = ensure_staging(ctx, bytes); rc != VXA_OK) return rc;
-    VXA_CUDA(ctx->inst_dev.ensure(std::max<size_t>(bytes, 16)));
     const int slot = ctx->inst_slot;
     ctx->inst_slot ^= 1;
     VXA_CUDA(cudaEventSynchronize(ctx->inst_done[slot])); // staging slot no longer read by an earlier copy
+    if (ctx->inst_dev[slot].cap < std::max<size_t>(bytes, 16)) {
+        VXA_CUDA(cudaEventSynchronize(ctx->inst_free[slot])); // no kernel still reads the old table
+        VXA_CUDA(ctx->inst_dev[slot].ensure(std::max<size_t>(bytes, 16)));
+    }
     auto* tab = reinterpret_cast<DevInstance<Real>*>(ctx->inst_host[slot]);
     build_instances<Real>(ctx, f, in, n, tab,
                           cull_bytes ? reinterpret_cast<float4*>(ctx->inst_host[slot] + inst_bytes) : nullptr);
@@ -406,8 +414,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
 
     FrameParams<Real> p{};
     fill_camera(p, f);
-    p.inst = reinterpret_cast<const DevInstance<Real>*>(ctx->inst_dev.ptr);
-    p.cull = cull_bytes ? reinterpret_cast<const float4*>(ctx->inst_dev.ptr + inst_bytes) : nullptr;
+    p.inst = reinterpret_cast<const DevInstance<Real>*>(ctx->inst_dev[slot].ptr);
+    p.cull = cull_bytes ? reinterpret_cast<const float4*>(ctx->inst_dev[slot].ptr + inst_bytes) : nullptr;
     p.n_inst = n;
     p.background = f->background[0] | (uint32_t{f->background[1]} << 8) | (uint32_t{f->background[2]} << 16) | 0xff000000u;
     p.culling = f->culling ? 1u : 0u;
@@ -475,9 +483,15 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.aov = aov;
     p.hbo = hbo;
 
-    if (bytes) VXA_CUDA(cudaMemcpyAsync(ctx->inst_dev.ptr, ctx->inst_host[slot], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    // the upload runs beside the previous frame's kernel (its own stream and
+    // table slot), off the frame-to-frame critical path
+    VXA_CUDA(cudaStreamWaitEvent(ctx->upload_stream, ctx->inst_free[slot], 0));
+    if (bytes)
+        VXA_CUDA(cudaMemcpyAsync(ctx->inst_dev[slot].ptr, ctx->inst_host[slot], bytes, cudaMemcpyHostToDevice,
+                                 ctx->upload_stream));
     ctx->h2d += bytes;
-    VXA_CUDA(cudaEventRecord(ctx->inst_done[slot], ctx->stream));
+    VXA_CUDA(cudaEventRecord(ctx->inst_done[slot], ctx->upload_stream));
+    VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->inst_done[slot], 0));
     VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, sizeof(uint32_t), ctx->stream));
     if (reset_counters) VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
 
@@ -518,6 +532,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     }
     if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
     VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
+    VXA_CUDA(cudaEventRecord(ctx->inst_free[slot], ctx->stream)); // this table slot may be overwritten now
     ++ctx->k_count;
     return VXA_OK;
 }
@@ -608,12 +623,15 @@ namespace {
 // Streams, events and the small device buffers of a new context.
 int init_ctx(vxa_ctx* ctx) {
     VXA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    VXA_CUDA(cudaStreamCreateWithFlags(&ctx->upload_stream, cudaStreamNonBlocking));
     VXA_CUDA(ctx->tile_counter.ensure(1));
     VXA_CUDA(ctx->counters.ensure(8));
     VXA_CUDA(cudaMemset(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long)));
     for (int s = 0; s < 2; ++s) {
         VXA_CUDA(cudaEventCreateWithFlags(&ctx->inst_done[s], cudaEventDisableTiming));
-        VXA_CUDA(cudaEventRecord(ctx->inst_done[s], ctx->stream));
+        VXA_CUDA(cudaEventRecord(ctx->inst_done[s], ctx->upload_stream));
+        VXA_CUDA(cudaEventCreateWithFlags(&ctx->inst_free[s], cudaEventDisableTiming));
+        VXA_CUDA(cudaEventRecord(ctx->inst_free[s], ctx->stream));
     }
     VXA_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
@@ -649,7 +667,8 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->fb.release();
     ctx->tile_counter.release();
     ctx->counters.release();
-    ctx->inst_dev.release();
+    ctx->inst_dev[0].release();
+    ctx->inst_dev[1].release();
     ctx->super_list.release();
     ctx->super_count.release();
     ctx->super_order.release();
@@ -660,9 +679,11 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->rays.release();
     ctx->hits.release();
     ctx->visits.release();
+    if (ctx->upload_stream) cudaStreamSynchronize(ctx->upload_stream);
     for (int s = 0; s < 2; ++s) {
         if (ctx->inst_host[s]) cudaFreeHost(ctx->inst_host[s]);
         if (ctx->inst_done[s]) cudaEventDestroy(ctx->inst_done[s]);
+        if (ctx->inst_free[s]) cudaEventDestroy(ctx->inst_free[s]);
     }
     for (cudaEvent_t e : {ctx->ev_a, ctx->ev_b, ctx->t_a, ctx->t_b})
         if (e) cudaEventDestroy(e);
@@ -677,6 +698,7 @@ int vxa_destroy(vxa_ctx* ctx) {
         if (ctx->rb_done[k]) cudaEventDestroy(ctx->rb_done[k]);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->upload_stream) cudaStreamDestroy(ctx->upload_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->counters_host) cudaFreeHost(ctx->counters_host);
     delete ctx;

@@ -24,13 +24,18 @@ for mode in ("stream", "stream3", "submit_only"):
     lib.vxa_synchronize(ctx)
     lib.vxa_stats_reset(ctx)
     t0 = time.perf_counter()
+    t_sub = t_wait = 0.0  # host time inside the submission call / blocked in the wait
     for k in range(steps):
         if mode.startswith("stream"):
             depth = 3 if mode == "stream3" else 2  # host images in flight
+            a = time.perf_counter()
             vxl.vxn_scene_stream(sc._h, k / 30.0, vx.VXA_FP32, bufs[k % depth].ctypes.data, C.byref(t))
+            b = time.perf_counter()
             tickets.append(t.value)
             if len(tickets) >= depth:
                 lib.vxa_wait_readback(ctx, tickets[-depth])
+            t_sub += b - a
+            t_wait += time.perf_counter() - b
         else:
             vxl.vxn_scene_submit(sc._h, k / 30.0, vx.VXA_FP32, 0, 1, 0)
     if mode.startswith("stream"):
@@ -39,7 +44,9 @@ for mode in ("stream", "stream3", "submit_only"):
     el = (time.perf_counter() - t0) * 1e3 / steps
     st = _abi.vxa_stats()
     lib.vxa_stats_read(ctx, C.byref(st))
-    print(f"{mode:12s} wall {el:.4f} ms/step   frame kernels {st.gpu_ms / st.frames:.4f} ms/frame ({st.frames} frames)")
+    print(f"{mode:12s} wall {el:.4f} ms/step   frame kernels {st.gpu_ms / st.frames:.4f} ms/frame ({st.frames} frames)"
+          + (f"   host: submit {t_sub * 1e3 / steps:.4f} ms, wait {t_wait * 1e3 / steps:.4f} ms per step"
+             if mode.startswith("stream") else ""))
 
 # D2H bandwidth of one RGB8 frame into page-locked host memory (torch, for reference)
 import torch
