@@ -28,9 +28,6 @@ constexpr int kBlock = 128;
 #ifndef VXA_MIN_BLOCKS
 #define VXA_MIN_BLOCKS 8
 #endif
-#ifndef VXA_STCS
-#define VXA_STCS 0
-#endif
 #ifndef VXA_ZERO_SPLIT
 #define VXA_ZERO_SPLIT 1
 #endif
@@ -580,17 +577,6 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             }
         }
         if (best.have) ++n_leaf;
-#if VXA_STCS
-        // output streams past the caches (evict-first): the frame is written
-        // once and read by the host copy, the L2 keeps the model's node words
-        __stcs(p.fb + pix, rgba);
-        if (p.rgb != nullptr) { // streamed frame: the readback's RGB8 bytes too (no pack pass)
-            unsigned char* o = p.rgb + 3 * pix;
-            __stcs(o, static_cast<unsigned char>(rgba));
-            __stcs(o + 1, static_cast<unsigned char>(rgba >> 8));
-            __stcs(o + 2, static_cast<unsigned char>(rgba >> 16));
-        }
-#else
         p.fb[pix] = rgba;
         if (p.rgb != nullptr) { // streamed frame: the readback's RGB8 bytes too (no pack pass)
             uint8_t* o = p.rgb + 3 * pix;
@@ -598,7 +584,6 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             o[1] = static_cast<uint8_t>(rgba >> 8);
             o[2] = static_cast<uint8_t>(rgba >> 16);
         }
-#endif
 
         if constexpr (kAov) {
             PixelAov a;
