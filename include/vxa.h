@@ -232,6 +232,10 @@ int vxa_timer_begin(vxa_ctx* ctx);
 int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms);
 /* Writes a scratch buffer larger than L2 on the context stream. */
 int vxa_flush_l2(vxa_ctx* ctx);
+/* Holds the context stream for about `microseconds` (one spinning thread):
+ * enqueued before vxa_timer_begin it gives the host time to enqueue the timed
+ * work, so host submission latency stays out of a device-timed region. */
+int vxa_stream_delay(vxa_ctx* ctx, uint32_t microseconds);
 /* Raw cudaStream_t of the context (for callers that record their own events). */
 void* vxa_stream(vxa_ctx* ctx);
 

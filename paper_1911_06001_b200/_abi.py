@@ -172,7 +172,7 @@ VXA_SYMBOLS = [
     "vxa_model_counts",
     "vxa_hbo_create", "vxa_hbo_release", "vxa_hbo_download", "vxa_hbo_upload", "vxa_render", "vxa_submit", "vxa_submit_readback",
     "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
-    "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream",
+    "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream_delay", "vxa_stream",
     "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_tiles_count", "vxa_tiles_pack", "vxa_tiles_unpack", "vxa_traverse",
 ]
 VXN_SYMBOLS = [
@@ -230,6 +230,7 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_timer_begin", i, P)
     _declare(lib, "vxa_timer_end", i, P, C.POINTER(d))
     _declare(lib, "vxa_flush_l2", i, P)
+    _declare(lib, "vxa_stream_delay", i, P, C.c_uint32)
     _declare(lib, "vxa_stream", P, P)
     _declare(lib, "vxa_fb_export", i, P, C.c_int32, C.c_int32, P)
     _declare(lib, "vxa_fb_import", i, P, C.c_int32, C.c_int32, P)

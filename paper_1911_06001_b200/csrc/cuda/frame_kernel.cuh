@@ -28,6 +28,9 @@ constexpr int kBlock = 128;
 #ifndef VXA_MIN_BLOCKS
 #define VXA_MIN_BLOCKS 8
 #endif
+#ifndef VXA_PDL
+#define VXA_PDL 0
+#endif
 #ifndef VXA_ZERO_SPLIT
 #define VXA_ZERO_SPLIT 1
 #endif
@@ -365,6 +368,12 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     // opaque to the optimiser: kept in a register instead of being re-derived
     // from %tid / the CTA window (6 instructions) on every push
     asm volatile("" : "+r"(stack.base));
+#if VXA_PDL
+    // launched as a programmatic dependent of the culling pre-pass: everything
+    // above overlapped its tail; the lists, the order and the tile counter are
+    // read only after it completed (a no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     const uint16_t* const list = s_list[warp];
 
     while (true) {
@@ -614,49 +623,20 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     }
 }
 
-// Pre-pass for large scenes: one warp per super-tile of this rank cone-tests
-// every instance against the super-tile's cone and writes the survivors (in
-// instance order) to its list; the frame kernel's 8x4 tiles then test only
-// their super-tile's list (tiles x instances / 32 rounds -> super-tiles x
-// instances / 32 + tiles x list / 32).
-template <typename Real>
-__global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__ FrameParams<Real> p,
-                                                        uint16_t* __restrict__ list, uint32_t* __restrict__ count) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t st = blockIdx.x * 4u + (threadIdx.x >> 5);
-    const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
-    if (st >= n_mine) return;
-    const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
-    const uint32_t sy = super_row(p, s);
-    const int x0 = static_cast<int>((s - sy * p.n_super_x) * kSuper), y0 = static_cast<int>(sy * kSuper);
-    const float w = static_cast<float>(min(kSuper, p.width - x0)), h = static_cast<float>(min(kSuper, p.height - y0));
-    const TileCone cone = region_cone(p, x0, y0, w, h);
-    uint16_t* out = list + static_cast<size_t>(st) * p.super_cap;
-    uint32_t cnt = 0;
-    for (uint32_t base = 0; base < p.n_inst; base += 32) {
-        const uint32_t i = base + lane;
-        const bool c = i < p.n_inst && cone_candidate(__ldg(p.cull + i), cone);
-        const uint32_t m = __ballot_sync(0xffffffffu, c);
-        const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
-        if (c && pos < p.super_cap) out[pos] = static_cast<uint16_t>(i);
-        cnt += __popc(m);
-    }
-    if (lane == 0) count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
-}
-
 // Longest-first order of the rank's super-tiles for the frame kernel's work
-// queue: a counting sort (one block) by descending candidate count from the
-// pre-pass (overflowed lists first, empty ones last). Only the schedule
+// queue: a counting sort by descending candidate count (overflowed lists first,
+// empty ones last), run by the pre-pass's last block. Only the schedule
 // changes -- every pixel's arithmetic is the same -- so the grid's tail is made
-// of cheap tiles instead of whatever the screen order puts last.
-static __global__ void __launch_bounds__(1024) super_order_kernel(const uint32_t* __restrict__ count, uint32_t n,
-                                                          uint32_t* __restrict__ order) {
+// of cheap tiles instead of whatever the screen order puts last. `count` was
+// written by other blocks of the same grid: read through L2 (__ldcg), not the
+// read-only path.
+__device__ __forceinline__ void order_by_count(const uint32_t* count, uint32_t n, uint32_t* order) {
     constexpr uint32_t kBuckets = 66; // overflow, 64 .. 0 candidates
     __shared__ uint32_t start[kBuckets];
     const auto bucket = [](uint32_t c) { return c == 0xffffffffu ? 0u : 65u - min(c, 64u); };
     for (uint32_t b = threadIdx.x; b < kBuckets; b += blockDim.x) start[b] = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[bucket(__ldg(count + i))], 1u);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[bucket(__ldcg(count + i))], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t acc = 0;
@@ -667,7 +647,56 @@ static __global__ void __launch_bounds__(1024) super_order_kernel(const uint32_t
         }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(__ldg(count + i))], 1u)] = i;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(__ldcg(count + i))], 1u)] = i;
+}
+
+// Pre-pass for large scenes: one warp per super-tile of this rank cone-tests
+// every instance against the super-tile's cone and writes the survivors (in
+// instance order) to its list; the frame kernel's 8x4 tiles then test only
+// their super-tile's list (tiles x instances / 32 rounds -> super-tiles x
+// instances / 32 + tiles x list / 32). With p.super_order set, the grid's last
+// block to finish (a ticket on `done`, which it resets) then writes the
+// longest-first super-tile order.
+template <typename Real>
+__global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__ FrameParams<Real> p,
+                                                        uint16_t* __restrict__ list, uint32_t* __restrict__ count,
+                                                        uint32_t* __restrict__ done) {
+    const uint32_t lane = threadIdx.x & 31u;
+#if VXA_PDL
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
+    const uint32_t st = blockIdx.x * 4u + (threadIdx.x >> 5);
+    const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
+    if (st < n_mine) {
+        const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
+        const uint32_t sy = super_row(p, s);
+        const int x0 = static_cast<int>((s - sy * p.n_super_x) * kSuper), y0 = static_cast<int>(sy * kSuper);
+        const float w = static_cast<float>(min(kSuper, p.width - x0)), h = static_cast<float>(min(kSuper, p.height - y0));
+        const TileCone cone = region_cone(p, x0, y0, w, h);
+        uint16_t* out = list + static_cast<size_t>(st) * p.super_cap;
+        uint32_t cnt = 0;
+        for (uint32_t base = 0; base < p.n_inst; base += 32) {
+            const uint32_t i = base + lane;
+            const bool c = i < p.n_inst && cone_candidate(__ldg(p.cull + i), cone);
+            const uint32_t m = __ballot_sync(0xffffffffu, c);
+            const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
+            if (c && pos < p.super_cap) out[pos] = static_cast<uint16_t>(i);
+            cnt += __popc(m);
+        }
+        if (lane == 0) count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
+    }
+    if (p.super_order == nullptr) return;
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence(); // this block's counts are visible before its ticket
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    order_by_count(count, n_mine, const_cast<uint32_t*>(p.super_order));
+    if (threadIdx.x == 0) *done = 0; // ready for the next frame
 }
 
 } // namespace vxa

@@ -16,15 +16,29 @@ void* pick(bool aov, bool hbo, bool compact) { return compact ? pick_k<true>(aov
 
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l) {
     void* args[] = {const_cast<FrameParams<float>*>(&p)};
+#if VXA_PDL
+    if (p.super_list != nullptr) { // behind the pre-pass: programmatic dependent launch
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(l.grid);
+        cfg.blockDim = dim3(kBlock);
+        cfg.dynamicSmemBytes = frame_smem_bytes_f32(p.max_depth);
+        cfg.stream = l.stream;
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr.val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelExC(&cfg, pick(aov, hbo, p.compact != 0), args);
+    }
+#endif
     return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f32(p.max_depth), l.stream);
 }
 
-cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, cudaStream_t s) {
+cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, uint32_t* done,
+                              cudaStream_t s) {
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (n_mine == 0) return cudaSuccess;
-    super_cull_kernel<float><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
-    if (p.super_order != nullptr)
-        super_order_kernel<<<1, 1024, 0, s>>>(count, n_mine, const_cast<uint32_t*>(p.super_order));
+    super_cull_kernel<float><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count, done);
     return cudaGetLastError();
 }
 

@@ -14,12 +14,11 @@ void* pick(bool aov, bool hbo, bool /*compact: FP64 keeps the general words*/) {
 }
 } // namespace
 
-cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint32_t* count, cudaStream_t s) {
+cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint32_t* count, uint32_t* done,
+                              cudaStream_t s) {
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (n_mine == 0) return cudaSuccess;
-    super_cull_kernel<double><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count);
-    if (p.super_order != nullptr)
-        super_order_kernel<<<1, 1024, 0, s>>>(count, n_mine, const_cast<uint32_t*>(p.super_order));
+    super_cull_kernel<double><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count, done);
     return cudaGetLastError();
 }
 

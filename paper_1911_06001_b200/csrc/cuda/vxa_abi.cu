@@ -181,6 +181,7 @@ struct vxa_ctx {
     DevBuf<uint16_t> super_list;  // per-super-tile candidate lists (large scenes)
     DevBuf<uint32_t> super_count;
     DevBuf<uint32_t> super_order; // longest-first super-tile order (VXA_LPT)
+    DevBuf<uint32_t> super_done;  // pre-pass block tickets (the last block sorts; reset by it)
     int aux_launches = 0;         // pre-pass kernels since the last stats reset
     unsigned char* inst_host[2] = {nullptr, nullptr};
     size_t inst_host_cap = 0;
@@ -521,8 +522,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
             VXA_CUDA(ctx->super_order.ensure(std::max<size_t>(mine_super, 1)));
             p.super_order = ctx->super_order.ptr;
         }
-        e = launch_super_cull(p, ctx->super_list.ptr, ctx->super_count.ptr, ctx->stream);
-        ctx->aux_launches += p.super_order != nullptr ? 2 : 1; // pre-pass (+ its order kernel)
+        e = launch_super_cull(p, ctx->super_list.ptr, ctx->super_count.ptr, ctx->super_done.ptr, ctx->stream);
+        ++ctx->aux_launches;
     }
     if (e == cudaSuccess) {
         if constexpr (sizeof(Real) == 8)
@@ -625,6 +626,8 @@ int init_ctx(vxa_ctx* ctx) {
     VXA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     VXA_CUDA(cudaStreamCreateWithFlags(&ctx->upload_stream, cudaStreamNonBlocking));
     VXA_CUDA(ctx->tile_counter.ensure(1));
+    VXA_CUDA(ctx->super_done.ensure(1));
+    VXA_CUDA(cudaMemset(ctx->super_done.ptr, 0, sizeof(uint32_t)));
     VXA_CUDA(ctx->counters.ensure(8));
     VXA_CUDA(cudaMemset(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long)));
     for (int s = 0; s < 2; ++s) {
@@ -672,6 +675,7 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->super_list.release();
     ctx->super_count.release();
     ctx->super_order.release();
+    ctx->super_done.release();
     ctx->aov.release();
     ctx->hbo.release();
     ctx->rgb.release();
@@ -1298,6 +1302,27 @@ int vxa_timer_end(vxa_ctx* ctx, double* elapsed_ms) {
     float ms = 0.f;
     VXA_CUDA(cudaEventElapsedTime(&ms, ctx->t_a, ctx->t_b));
     *elapsed_ms = ms;
+    return VXA_OK;
+}
+
+namespace {
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void delay_kernel(uint32_t ns) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+} // namespace
+
+int vxa_stream_delay(vxa_ctx* ctx, uint32_t microseconds) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    delay_kernel<<<1, 1, 0, ctx->stream>>>(1000u * std::min<uint32_t>(microseconds, 1000000u));
+    VXA_CUDA(cudaGetLastError());
     return VXA_OK;
 }
 

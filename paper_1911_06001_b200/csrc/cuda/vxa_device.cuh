@@ -172,7 +172,7 @@ template <typename Real> struct FrameParams {
     const uint16_t* super_list;
     const uint32_t* super_count;
     uint32_t super_cap;
-    // Processing order of the rank-local super-tiles (super_order_kernel: most
+    // Processing order of the rank-local super-tiles (super_cull_kernel's last block: most
     // candidates first, so the grid's tail is cheap tiles), or null: natural order.
     const uint32_t* super_order;
     const uint32_t* top_words; // compact words of the scene's single model, or null

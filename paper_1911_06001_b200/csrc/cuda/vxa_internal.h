@@ -36,8 +36,10 @@ struct FrameLaunch {
 // Node words the FP32 frame kernel stages in shared memory (0 = off; build variant).
 constexpr uint32_t kSmemTopWords = VXA_SMEM_TOP;
 // Per-super-tile candidate lists for large scenes (frame_kernel.cuh: super_cull_kernel).
-cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, cudaStream_t s);
-cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint32_t* count, cudaStream_t s);
+cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, uint32_t* done,
+                              cudaStream_t s);
+cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint32_t* count, uint32_t* done,
+                              cudaStream_t s);
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l);
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l);
 int frame_blocks_per_sm_f32(bool aov, bool hbo, bool compact, uint32_t max_depth);
