@@ -509,13 +509,19 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 if (mode == kOne) {
                     found = one_left, cand = only, one_left = false;
                 } else if (mode == kListSorted) {
-                    // (t_center, index) minimum over the remaining hit bits
+                    // (t_center, index) minimum over the remaining hit bits. A lone
+                    // first candidate needs no sphere values: nothing to order, and
+                    // its t_boundary only matters once there is a best hit.
                     int kb = -1;
                     Real tcb = Real(0);
-                    for (unsigned long long it = rem; it; it &= it - 1) {
-                        const int k = __ffsll(it) - 1;
-                        const SphereRes<Real> sr = sphere_of(p, list[k], dw);
-                        if (kb < 0 || sr.tc < tcb) kb = k, tcb = sr.tc, cand_tb = sr.tb;
+                    if (!best.have && rem != 0 && (rem & (rem - 1)) == 0) {
+                        kb = __ffsll(rem) - 1;
+                    } else {
+                        for (unsigned long long it = rem; it; it &= it - 1) {
+                            const int k = __ffsll(it) - 1;
+                            const SphereRes<Real> sr = sphere_of(p, list[k], dw);
+                            if (kb < 0 || sr.tc < tcb) kb = k, tcb = sr.tc, cand_tb = sr.tb;
+                        }
                     }
                     if (kb >= 0) found = true, cand = list[kb], rem &= ~(1ull << kb);
                 } else if (mode == kListIdOrder) {
