@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --headstart-us 0"
 timeout 300 $CMD > gpurun_out/b_ll.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo ncu=$?

@@ -254,3 +254,48 @@ def test_c_abi_misuse_is_reported_not_fatal(gpu):
     without = np.zeros_like(with_ghost)
     assert lib.vxa_render(ctx, C.byref(f), C.byref(inst[1]), 1, without.ctypes.data, None, None) == 0
     assert (with_ghost == without).all()
+
+
+def test_back_to_back_frames_with_growing_instance_tables(gpu):
+    """Frames submitted without waiting, alternating a 64-instance and a 700-instance
+    scene on one context: the double-buffered device instance tables grow while
+    earlier frames are in flight, and every frame equals its synchronous render."""
+    lib = vx.vxa()
+    ctx = vx.context()
+    vxl = vx.voxanim()
+    model = vx.Model.procedural(6, shell=True)
+    small = vx.Scene(vx.config.C4, [model], 0, 320, 180)
+    big = vx.Scene(vx.config.CROWD, [model], 700, 320, 180)
+    bufs = [np.zeros((180, 320, 3), np.uint8) for _ in range(2)]
+    for b in bufs:
+        assert lib.vxa_host_register(ctx, b.ctypes.data, b.nbytes) == 0
+    t = C.c_uint64()
+    tickets, scenes = [], []
+    for k in range(8):
+        sc = big if k % 2 else small
+        assert vxl.vxn_scene_stream(sc._h, k / 30.0, vx.VXA_FP32, bufs[k % 2].ctypes.data, C.byref(t)) == 0
+        tickets.append(t.value)
+        scenes.append(sc)
+        if k >= 1:
+            assert lib.vxa_wait_readback(ctx, tickets[k - 1]) == 0
+            got = bufs[(k - 1) % 2].copy()
+            ref_sc = scenes[k - 1]
+            # the synchronous frame of the same scene and time, rendered after the stream caught up
+            assert lib.vxa_wait_readback(ctx, tickets[k]) == 0
+            ref_sc.evaluate((k - 1) / 30.0)
+            want = ref_sc.render(precision=vx.VXA_FP32)[0]
+            assert (got == want).all(), k - 1
+    for b in bufs:
+        lib.vxa_host_unregister(ctx, b.ctypes.data)
+
+
+def test_stream_delay_holds_the_stream(gpu):
+    """vxa_stream_delay (bench head start) keeps the context stream busy for the
+    requested time and nothing else."""
+    lib = vx.vxa()
+    ctx = vx.context()
+    ms = C.c_double()
+    assert lib.vxa_timer_begin(ctx) == 0
+    assert lib.vxa_stream_delay(ctx, 300) == 0
+    assert lib.vxa_timer_end(ctx, C.byref(ms)) == 0
+    assert 0.29 <= ms.value < 5.0, ms.value
