@@ -28,6 +28,11 @@ constexpr int kBlock = 128;
 #ifndef VXA_MIN_BLOCKS
 #define VXA_MIN_BLOCKS 8
 #endif
+// Build variants measured in DESIGN.md §7 (defaults = the measured best):
+// VXA_PDL      launch the frame kernel as a programmatic dependent of the culling
+//              pre-pass (griddepcontrol) -- no change measured, off;
+// VXA_ZERO_SPLIT  a second traversal instantiation for rays with a zero local
+//              direction component, so the common loop has no zero conventions.
 #ifndef VXA_PDL
 #define VXA_PDL 0
 #endif
@@ -35,10 +40,10 @@ constexpr int kBlock = 128;
 #define VXA_ZERO_SPLIT 1
 #endif
 constexpr int kWarps = kBlock / 32;
-constexpr uint32_t kListCap = 64;
+constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
 struct BlockStack : SmemStack<kBlock * sizeof(uint2)> {
     uint32_t base_top; // shared address of the staged top node words (VXA_SMEM_TOP)
-}; // per-warp tile candidate list (bit positions of a u64 mask)
+};
 
 // Super-tile row of super-tile s: s / n_super_x by a multiply-high when the
 // host found the magic exact for every super-tile of the frame (vxa_abi.cu).

@@ -41,11 +41,12 @@ constexpr uint32_t kMixed = 1u << 16;
 constexpr int kTileW = VXA_TILE_W, kTileH = 32 / VXA_TILE_W;
 constexpr int kSuper = 64;
 constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
-// Scenes with more instances than this get the per-super-tile culling pre-pass.
-// Longest-first super-tile order after the culling pre-pass (1) or screen order (0).
+// Work-queue order of the super-tiles when the culling pre-pass runs: longest
+// first by candidate count (1) or screen order (0); DESIGN.md §7.
 #ifndef VXA_LPT
 #define VXA_LPT 1
 #endif
+// Scenes with more instances than this get the per-super-tile culling pre-pass.
 #ifndef VXA_SUPER_MIN
 #define VXA_SUPER_MIN 32
 #endif
