@@ -276,6 +276,25 @@ def ncu_compute(workload):
             "source": "profiles/ncu_frame_kernel.json (ncu --set full)"}
 
 
+def exchange_gpu_ids(rank: int, world: int, device: int) -> list:
+    """UUIDs of every rank's GPU, exchanged through a TCP store beside the process group's
+    rendezvous (before any backend is chosen)."""
+    import datetime
+
+    import torch
+    import torch.distributed as dist
+
+    store = dist.TCPStore(os.environ.get("MASTER_ADDR", "127.0.0.1"), int(os.environ.get("MASTER_PORT", "29500")) + 1,
+                          world, rank == 0, timeout=datetime.timedelta(seconds=120))
+    store.set(f"gpu{rank}", str(torch.cuda.get_device_properties(device).uuid))
+    ids = [store.get(f"gpu{r}").decode() for r in range(world)]
+    store.set(f"done{rank}", "1")
+    if rank == 0:  # the server outlives every client's last read
+        for r in range(world):
+            store.get(f"done{r}")
+    return ids
+
+
 def exchange_handle(dist, rank, handle: bytes) -> bytes:
     """Broadcast rank 0's 64-byte CUDA IPC framebuffer handle to every rank."""
     obj = [handle if rank == 0 else None]
@@ -379,6 +398,19 @@ def run_ours(args):
         # a launcher that gives each process one visible GPU: LOCAL_RANK is not an ordinal there
         if torch.cuda.device_count() <= local:
             device = local = 0
+        # more ranks than physical GPUs (e.g. --gpus 2 on a one-GPU box): NCCL cannot put two
+        # ranks on one device, so run the shared-device path (gloo barriers, CUDA IPC) -- a
+        # correctness run of the multi-rank path, labelled as such, not a scaling measurement
+        try:
+            ids = exchange_gpu_ids(rank, world, device)
+        except Exception as e:  # no side channel: assume one GPU per rank, as before
+            print(f"bench: GPU id exchange failed ({e}); assuming one GPU per rank", file=sys.stderr)
+            ids = [str(r) for r in range(world)]
+        if len(set(ids)) < world:
+            args.same_device = True
+            device = local = 0
+            if rank == 0:
+                print(f"bench: {world} ranks share fewer than {world} GPUs: shared-device mode", file=sys.stderr)
     os.environ["VOXANIM_DEVICE"] = str(device)
     import paper_1911_06001_b200 as vx
     from paper_1911_06001_b200 import _abi
@@ -405,7 +437,9 @@ def run_ours(args):
             raise RuntimeError(f"{what}: {lib.vxa_last_error().decode()}")
 
     # multi-GPU: map rank 0's framebuffer into every rank (NVLink peer stores)
-    composition = "NVLink peer stores into rank 0's framebuffer (CUDA IPC)" if world > 1 else "single device"
+    composition = ("single device" if world == 1 else
+                   "CUDA IPC stores into rank 0's framebuffer (ranks share one device)" if args.same_device else
+                   "NVLink peer stores into rank 0's framebuffer (CUDA IPC)")
     if world > 1:
         handle = (C.c_char * 64)()
         if rank == 0:
@@ -691,7 +725,10 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
                        "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False,
-                       "partition": f"64x64 super-tiles round-robin over {world} GPU(s)",
+                       "partition": (f"64x64 super-tiles round-robin over {world} ranks sharing one GPU "
+                                     f"(multi-rank correctness run, not a scaling measurement)"
+                                     if world > 1 and args.same_device else
+                                     f"64x64 super-tiles round-robin over {world} GPU(s)"),
                        "composition": composition,
                        "l2": "flushed between timed steps (256 MB write)" if not args.no_flush else "warm",
                        "timed_region": f"device events around each step (instance-table upload, culling pre-pass, "

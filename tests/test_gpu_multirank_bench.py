@@ -16,13 +16,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("compose,port", [("ipc", 29531), ("gather", 29532)])
-def test_two_ranks_compose_the_single_device_frame(gpu, compose, port):
+@pytest.mark.parametrize("compose,port,flag", [("ipc", 29531, True), ("gather", 29532, True), ("ipc", 29533, False)])
+def test_two_ranks_compose_the_single_device_frame(gpu, compose, port, flag):
     """ipc: peer stores into rank 0's framebuffer; gather: the fallback without
-    CUDA IPC (tiles packed per rank, collective gather, unpacked on rank 0)."""
+    CUDA IPC (tiles packed per rank, collective gather, unpacked on rank 0).
+    Without --same-device the bench finds the ranks share one GPU (GPU ids
+    exchanged before the backend is chosen) and takes the same path."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--same-device", "--no-cpu-baseline", "--no-extras"]
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-extras"] + (["--same-device"] if flag else [])
     env = dict(os.environ)
     if compose == "gather":
         env["VOXANIM_COMPOSE"] = "gather"
@@ -32,6 +34,7 @@ def test_two_ranks_compose_the_single_device_frame(gpu, compose, port):
     assert len(lines) == 1, res.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2
-    assert d["config"]["composition"].startswith("NVLink peer stores" if compose == "ipc" else "collective gather")
+    assert d["config"]["composition"].startswith("CUDA IPC stores" if compose == "ipc" else "collective gather")
+    assert "sharing one GPU" in d["config"]["partition"]
     assert d["multi_gpu_frame_identical"] is True
     assert d["e2e"] is not None and d["e2e"]["value"] > 0
