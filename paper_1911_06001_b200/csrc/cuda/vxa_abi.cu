@@ -719,12 +719,19 @@ int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t
 }
 
 // Radius, in unit-cube coordinates about the cube centre, of a sphere holding
-// every leaf: the farthest corner of any occupied cell at level min(depth, 5)
-// (a cell bounds its whole subtree) or of a leaf above that level. Returned
-// squared with a small margin; the FP32 kernel skips the traversal of rays whose
-// line misses it (a shell's box corners). Walks at most 4681 nodes.
+// every leaf: the farthest corner of any leaf, or of any occupied cell of the
+// deepest level the walk reaches (a cell bounds its whole subtree). The walk
+// goes level by level until a level holds more than kContentCells cells (or the
+// caller's node array ends: device-built models pass their top levels only).
+// Returned squared with a small margin; the FP32 kernel skips the traversal of
+// rays whose line misses it -- a shell's box corners, and the thin annulus
+// between the shell and a coarse bound.
+#ifndef VXA_CONTENT_CELLS
+#define VXA_CONTENT_CELLS 4194304u // cells per level (64 MB of walk state at most)
+#endif
 float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
-    const int K = static_cast<int>(std::min<uint32_t>(depth, 5u));
+    const int K = static_cast<int>(depth);
+    constexpr size_t kContentCells = VXA_CONTENT_CELLS;
     struct Cell {
         uint32_t idx, x, y, z;
     };
@@ -740,9 +747,15 @@ float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
         return acc;
     };
     for (int L = 0; L < K; ++L) {
+        bool inside = true;
+        for (const Cell& c : cur) inside = inside && c.idx < node_count;
+        if (!inside) { // the nodes below are not here (top levels only): bound by the cells
+            for (const Cell& c : cur) r2 = std::max(r2, corner2(c.x, c.y, c.z, L));
+            break;
+        }
         next.clear();
+        bool full = false;
         for (const Cell& c : cur) {
-            if (c.idx >= node_count) return 1.0f; // not a well-formed model: no bound
             const uint8_t* r = raw + 12 * size_t{c.idx};
             uint32_t cb;
             std::memcpy(&cb, r, 4);
@@ -755,6 +768,14 @@ float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
                 else
                     next.push_back({cb + static_cast<uint32_t>(__builtin_popcount(internal & ((1u << o) - 1u))), x, y, z});
             }
+            if (next.size() > kContentCells) {
+                full = true;
+                break;
+            }
+        }
+        if (full) { // the next level would not fit: bound by this level's cells
+            for (const Cell& c : cur) r2 = std::max(r2, corner2(c.x, c.y, c.z, L));
+            break;
         }
         cur.swap(next);
     }
