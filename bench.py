@@ -86,6 +86,7 @@ class ClockSampler:
         self.device = device
         self.samples = []
         self._stop = threading.Event()
+        self._first = threading.Event()  # set once a sample exists (NVML start-up can take ~1 s)
         self._t = None
 
     # NVML clocks-event reason bits (nvml.h: nvmlClocksEventReason*)
@@ -103,6 +104,7 @@ class ClockSampler:
                 bits = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.samples.append([str(sm), str(mx)] +
                                     ["Active" if bits & self.NVML_BITS[n] else "Not Active" for n in self.NAMES])
+                self._first.set()
                 self._stop.wait(0.005)
         finally:
             pynvml.nvmlShutdown()
@@ -120,6 +122,7 @@ class ClockSampler:
                 out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
                 if out:
                     self.samples.append([x.strip() for x in out.split(",")])
+                    self._first.set()
             except Exception:
                 pass
             self._stop.wait(0.05)
@@ -127,6 +130,8 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._poll, daemon=True)
         self._t.start()
+        # the timed region starts only once the sampler is running, so even a short run is covered
+        self._first.wait(timeout=20)
         return self
 
     def __exit__(self, *exc):
