@@ -51,6 +51,36 @@ __device__ __forceinline__ uint32_t compact3(uint32_t v) {
     return v;
 }
 
+// Content bound of the built model: the largest squared distance, in unit-cube
+// coordinates about the cube centre, of any leaf's farthest corner (the FP32
+// frame kernel's content-sphere test, vxa_abi.cu: content_r2), from one byte of
+// V_{depth-1} per cube. Exact in FP32: coordinates are multiples of 2^-depth
+// (depth <= 10), their squares and sums fit the mantissa. Maximum through the
+// float bits (non-negative floats order like unsigned ints).
+__global__ void leaf_extent(const uint8_t* __restrict__ v, uint64_t cubes, uint32_t depth,
+                            unsigned int* __restrict__ out) {
+    const float sz = ldexpf(1.0f, -static_cast<int>(depth));
+    float best = 0.0f;
+    for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < cubes; i += uint64_t{gridDim.x} * blockDim.x) {
+        const uint32_t b = v[i];
+        if (b == 0) continue;
+        const uint32_t c = static_cast<uint32_t>(i);
+        const uint32_t cx = compact3(c >> 2), cy = compact3(c >> 1), cz = compact3(c);
+        for (uint32_t o = 0; o < 8; ++o) {
+            if (!((b >> o) & 1u)) continue;
+            const uint32_t q[3] = {2 * cx + ((o >> 2) & 1u), 2 * cy + ((o >> 1) & 1u), 2 * cz + (o & 1u)};
+            float acc = 0.0f;
+            for (int a = 0; a < 3; ++a) {
+                const float lo = static_cast<float>(q[a]) * sz - 0.5f, hi = static_cast<float>(q[a] + 1) * sz - 0.5f;
+                acc += fmaxf(lo * lo, hi * hi);
+            }
+            best = fmaxf(best, acc);
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, d));
+    if ((threadIdx.x & 31u) == 0 && best > 0.0f) atomicMax(out, __float_as_uint(best));
+}
+
 // V_{depth-1}: for each cube c of the 2^(depth-1) lattice, the occupancy of
 // its 8 voxels as the octant mask. Voxels (2x+i, 2y+j, 2z..2z+1) are two
 // adjacent bits of the x-major bitset (bit (x*n + y)*n + z, z even).
@@ -301,7 +331,7 @@ cudaError_t build_svo(cudaStream_t s, const uint64_t* grid_dev, uint32_t depth, 
         std::vector<size_t> off(depth + 1, 0);
         for (uint32_t L = 0; L < depth; ++L)
             off[L + 1] = off[L] + align_up(std::max<uint64_t>(8, uint64_t{1} << (3 * L)));
-        if (cudaError_t e = scratch.pyramid.ensure(off[depth] + 8 * size_t{depth}); e != cudaSuccess) return e;
+        if (cudaError_t e = scratch.pyramid.ensure(off[depth] + 8 * size_t{depth} + 8); e != cudaSuccess) return e;
         for (uint32_t L = 0; L < depth; ++L) V[L] = static_cast<uint8_t*>(scratch.pyramid.p) + off[L];
     }
     auto* counts = reinterpret_cast<unsigned long long*>(V[depth - 1] + align_up(std::max<uint64_t>(
@@ -317,8 +347,12 @@ cudaError_t build_svo(cudaStream_t s, const uint64_t* grid_dev, uint32_t depth, 
         parent_masks<<<grid_for(cubes), kThreads, 0, s>>>(reinterpret_cast<const uint64_t*>(V[L]), cubes, V[L - 1]);
     }
     tr.mark(s, "pyramid");
-    // level sizes: N_0 = 1 (the root always exists), N_{L+1} = set bits of V_L
-    cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * depth, s);
+    // level sizes: N_0 = 1 (the root always exists), N_{L+1} = set bits of V_L;
+    // then the leaves' extent (content bound) behind them
+    cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * depth + 8, s);
+    auto* extent = reinterpret_cast<unsigned int*>(counts + depth);
+    leaf_extent<<<grid_for(top), kThreads, 0, s>>>(V[depth - 1], top, depth, extent);
+    out.extent_dev = extent;
     for (uint32_t L = 0; L < depth; ++L) {
         const uint64_t bytes = uint64_t{1} << (3 * L);
         count_bits<<<grid_for(bytes / 4 + 1), kThreads, 0, s>>>(V[L], bytes, counts + L);

@@ -729,6 +729,13 @@ int vxa_device_info(vxa_ctx* ctx, int* device, int* sm_count, char* name, size_t
 #ifndef VXA_CONTENT_CELLS
 #define VXA_CONTENT_CELLS 4194304u // cells per level (64 MB of walk state at most)
 #endif
+// Squared content-sphere radius from the squared farthest leaf extent, with the
+// margin the FP32 kernel's test relies on.
+float content_bound(double r2) {
+    const double rho = std::sqrt(r2) * (1.0 + 1e-5) + 1e-5;
+    return static_cast<float>(rho * rho);
+}
+
 float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
     const int K = static_cast<int>(depth);
     constexpr size_t kContentCells = VXA_CONTENT_CELLS;
@@ -779,8 +786,7 @@ float content_r2(const uint8_t* raw, uint32_t node_count, uint32_t depth) {
         }
         cur.swap(next);
     }
-    const double rho = std::sqrt(r2) * (1.0 + 1e-5) + 1e-5;
-    return static_cast<float>(rho * rho);
+    return content_bound(r2);
 }
 
 int vxa_upload_model(vxa_ctx* ctx, const void* nodes, uint32_t node_count, const void* attrs, uint32_t attr_count,
@@ -987,11 +993,12 @@ int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, ui
     m.dev.depth = depth;
     m.dev.node_count = static_cast<uint32_t>(b.node_count);
     {
-        // the top levels are the first records (BFS order): at most 4681 nodes above level 5
-        const size_t top = std::min<uint64_t>(b.node_count, 4681);
-        std::vector<uint8_t> head(12 * top);
-        VXA_CUDA(cudaMemcpy(head.data(), m.raw, head.size(), cudaMemcpyDeviceToHost));
-        m.dev.content_r2 = content_r2(head.data(), static_cast<uint32_t>(top), depth);
+        // content bound: the farthest leaf corner, reduced on the device by the builder
+        unsigned int bits = 0;
+        VXA_CUDA(cudaMemcpy(&bits, b.extent_dev, sizeof(bits), cudaMemcpyDeviceToHost));
+        float r2;
+        std::memcpy(&r2, &bits, sizeof(r2));
+        m.dev.content_r2 = content_bound(static_cast<double>(r2));
     }
     m.attr_count = b.attr_count;
     m.bytes = (8 + 12 + (m.cwords ? 4 : 0)) * b.node_count + 4 * b.attr_count;

@@ -112,6 +112,9 @@ struct BuiltModel {
     uint32_t* cwords = nullptr;  // compact render words (null when bases exceed 24 bits)
     uint2* words = nullptr;      // wide render words (filled by the caller's repack)
     uint64_t node_count = 0, attr_count = 0;
+    // device scalar (in the builder's scratch): float bits of the squared leaf
+    // extent about the cube centre (unit-cube coordinates); valid once s is done
+    const unsigned int* extent_dev = nullptr;
 };
 // Enqueues the build on s (returns after the level sizes are known; the
 // emission passes are still in flight). On error out.block may be set.

@@ -72,6 +72,25 @@ def test_built_model_renders_like_uploaded(gpu):
     assert (a == b).all() and (a == o).all()
 
 
+@pytest.mark.parametrize("prim,depth", [("sphere", 7), ("box_shell", 6), ("menger", 6)])
+def test_built_model_content_bound_renders_like_uploaded_fp32(gpu, prim, depth):
+    """The FP32 kernel skips traversals of rays missing the model's content
+    sphere. Device-built models get it from the builder's leaf extent reduction,
+    uploaded ones from the host walk: both conservative, so the FP32 frames of the
+    same model agree pixel for pixel, in the C1 view and the 64-instance C4 layout."""
+    words, gd = vx.grid_primitive(prim, depth)
+    built = vx.Model.from_grid(words, gd, device=True)
+    uploaded = vx.Model.from_bytes(built.serialize())
+    for cfg, w, h in ((vx.config.C1, 0, 0), (vx.config.C4, 480, 270)):
+        sa = vx.Scene(cfg, [built], 0, w, h)
+        sb = vx.Scene(cfg, [uploaded], 0, w, h)
+        sa.evaluate(0.7)
+        sb.evaluate(0.7)
+        a = sa.render(precision=vx.VXA_FP32)[0]
+        b = sb.render(precision=vx.VXA_FP32)[0]
+        assert (a == b).all(), (prim, cfg)
+
+
 def test_c_abi_build_download_and_errors(gpu):
     lib = vx.vxa()
     ctx = vx.context()
