@@ -340,18 +340,59 @@ def cpu_baseline(model, workload, seconds, max_frames=5):
             "ms_per_frame": round(total_ms / frames, 3)}
 
 
+def oracle_bytes(model, workload, ks):
+    """Algorithmic bytes per ray counted by the ORACLE: the
+    reference's own per-pixel internal-node visits (traverse_debug, replayed in
+    shade_pixel's candidate order and skip rule by oracle/ref_harness.cpp's dump)
+    x 8 B + 4 B per attribute fetch (hit) + 4 B framebuffer store, over full
+    frames at the animation times of timed steps ks."""
+    import numpy as np
+    from oracle import ref
+
+    cfg, shell, depth, W, H, animated = WORKLOADS[workload]
+    rscene = ref.RefScene(cfg, [ref.RefModel.from_bytes(model.serialize())], 0, W, H)
+    fetches = hits = trav = n = 0
+    for k in ks:
+        rscene.evaluate(frame_time(k, animated))
+        aov, _ = rscene.dump(threads=ref.hardware_threads())
+        fetches += int(aov["node_fetches"].astype(np.int64).sum())
+        hits += int((aov["object_id"] >= 0).sum())
+        trav += int(aov["traversals"].astype(np.int64).sum())
+        n += aov.size
+    return {"bytes_per_ray": (8.0 * fetches + 4.0 * hits + 4.0 * n) / n, "node_fetches_per_ray": fetches / n,
+            "leaf_hits_per_ray": hits / n, "traversals_per_ray": trav / n,
+            "sample": f"{len(ks)} full {W}x{H} frames at t = " + ", ".join(f"{frame_time(k, animated):.4f}" for k in ks)
+                      + " s of the timed steps, reference traverse_debug visits (oracle/_ref dump)"}
+
+
 # ---------------------------------------------------------------------------- reference arm
+
+def reference_model(ref, workload):
+    """The workload's model for the reference arm, loaded by the reference's own
+    load_svo. The reference cannot build the depth-11 shell itself (its
+    build_from_grid needs a 2048^3 grid and a pointer tree of tens of GB), so a
+    CHILD process runs this repo's procedural builder -- pinned byte-identical to
+    the reference build_from_grid of the same grid (tests/test_builder.py) -- and
+    writes the .svo; this process only ever loads oracle/_ref."""
+    import tempfile
+
+    cfg, shell, depth, W, H, animated = WORKLOADS[workload]
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, f"model_d{depth}.svo")
+        code = (f"import sys; sys.path.insert(0, {ROOT!r}); import paper_1911_06001_b200 as vx; "
+                f"vx.Model.procedural({depth}, shell={shell}).save({path!r})")
+        subprocess.run([sys.executable, "-c", code], check=True)
+        return ref.RefModel.load(path)
+
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_1911_06001_b200 as vx  # host code only: the procedural depth-11 model
     from oracle import ref
 
     cfg, shell, depth, W, H, animated = WORKLOADS[args.workload]
-    model = vx.Model.procedural(depth, shell=shell)
-    rmodel = ref.RefModel.from_bytes(model.serialize())
+    rmodel = reference_model(ref, args.workload)
     rscene = ref.RefScene(cfg, [rmodel], 0, W, H)
     threads = ref.hardware_threads()
     # First warm-up step: one full reference frame; it sizes the sample so the
@@ -477,6 +518,24 @@ def run_ours(args):
         gather_buf = torch.zeros(n_max.value * 64 * 64, dtype=torch.int32, device=dev)
         gather_host = args.same_device  # gloo: the collective runs on host tensors
 
+    # Frame completion without a host barrier (peer-store composition): rank 0
+    # exports a flag block; every frame is opened by rank 0's go flag and closed
+    # when every rank's done flag has landed in rank 0's HBM (vxa_frame_open /
+    # vxa_frame_close). Ranks on distinct GPUs wait on the device (1-thread flag
+    # kernels, system-scope acquire/release over NVLink); ranks sharing a GPU
+    # must not run kernels that wait on one another, so there the same protocol
+    # polls the flags from the host.
+    sync = None
+    if world > 1 and gather_buf is None:
+        h = (C.c_char * 64)()
+        if rank == 0:
+            check(lib.vxa_sync_export(ctx, world, h), "sync_export")
+        got = exchange_handle(dist, rank, bytes(h))
+        if rank != 0:
+            check(lib.vxa_sync_import(ctx, rank, world, (C.c_char * 64).from_buffer_copy(got)), "sync_import")
+        sync = _abi.VXA_SYNC_HOST if args.same_device else _abi.VXA_SYNC_DEVICE
+        check(lib.vxa_sync_configure(ctx, sync, 20000), "sync_configure")
+
     def gather_compose():
         """The frame's super-tiles of every rank into rank 0's framebuffer (gather mode)."""
         import torch
@@ -508,8 +567,33 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    for k in range(args.warmup):
+    def frame(k, timed=False):
+        """One frame of this rank. N > 1 with flags: rank 0 opens it (go) and closes
+        it when every rank's tiles have landed; rank r waits for go, renders, and
+        signals done. The events bracket rank 0's whole frame (go .. last done)
+        and rank r's own part. Gather mode: host-synchronised collective."""
+        if sync is not None:
+            if rank == 0:
+                if timed:
+                    check(lib.vxa_timer_begin(ctx), "timer")
+                check(lib.vxa_frame_open(ctx), "frame_open")
+            else:
+                check(lib.vxa_frame_open(ctx), "frame_open")
+                if timed:
+                    check(lib.vxa_timer_begin(ctx), "timer")
+            submit(k)
+            check(lib.vxa_frame_close(ctx), "frame_close")
+            return
+        if timed:
+            check(lib.vxa_timer_begin(ctx), "timer")
         submit(k)
+        if gather_buf is not None:
+            check(lib.vxa_synchronize(ctx), "sync")
+            gather_compose()
+            barrier()  # gather mode: the frame is complete when the collective is
+
+    for k in range(args.warmup):
+        frame(k)
     check(lib.vxa_synchronize(ctx), "sync")
     barrier()
 
@@ -521,16 +605,11 @@ def run_ours(args):
                 check(lib.vxa_flush_l2(ctx), "flush")
             # the stream idles ~0.5 ms before the timed region opens, so the host has enqueued the
             # step's upload and kernels by then: the device time is the step's, not the host's
-            # submission latency (which the e2e number carries)
-            if args.headstart_us > 0:
+            # submission latency (which the e2e number carries). N > 1: rank 0's delay; the
+            # other ranks' frames start at its go flag.
+            if args.headstart_us > 0 and rank == 0:
                 check(lib.vxa_stream_delay(ctx, args.headstart_us), "delay")
-            check(lib.vxa_timer_begin(ctx), "timer")
-            submit(args.warmup + k)
-            if world > 1:
-                check(lib.vxa_synchronize(ctx), "sync")
-                if gather_buf is not None:
-                    gather_compose()
-                barrier()  # the frame is complete in rank 0's framebuffer only when every rank is done
+            frame(args.warmup + k, timed=True)
             ms = C.c_double()
             check(lib.vxa_timer_end(ctx, C.byref(ms)), "timer")
             step_ms.append(ms.value)
@@ -568,11 +647,10 @@ def run_ours(args):
     if world > 1:
         import numpy as np
 
+        barrier()
         k_chk = args.warmup + args.steps + 1
-        submit(k_chk)
+        frame(k_chk)
         check(lib.vxa_synchronize(ctx), "sync")
-        if gather_buf is not None:
-            gather_compose()
         barrier()
         if rank == 0:
             composed = np.empty((H, W, 3), np.uint8)
@@ -588,34 +666,52 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e and world > 1:
         # every rank: host update + its super-tiles (peer stores into rank 0); rank 0
-        # then reads the composed RGB8 frame into page-locked host memory
+        # packs the composed frame once every rank's done flag is in and reads the RGB8
+        # image into page-locked host memory on its copy stream while the next frame
+        # renders (vxa_framebuffer_readback); no host barrier between frames
         import numpy as np
 
-        host_img = np.empty((H, W, 3), np.uint8)
+        bufs = [np.empty((H, W, 3), np.uint8) for _ in range(2)]
         if rank == 0:
-            check(lib.vxa_host_register(ctx, host_img.ctypes.data, host_img.nbytes), "host_register")
+            for b in bufs:
+                check(lib.vxa_host_register(ctx, b.ctypes.data, b.nbytes), "host_register")
         lib.vxa_stats_reset(ctx)
         barrier()
+        tickets = []
+        ticket = C.c_uint64()
         t0 = time.perf_counter()
         for k in range(args.e2e_steps):
-            submit(k)
-            check(lib.vxa_synchronize(ctx), "sync")
-            if gather_buf is not None:
-                gather_compose()
-            barrier()
+            frame(k)
             if rank == 0:
-                check(lib.vxa_read_framebuffer(ctx, host_img.ctypes.data, W, H), "read_framebuffer")
-            barrier()
+                check(lib.vxa_framebuffer_readback(ctx, W, H, bufs[k % 2].ctypes.data, C.byref(ticket)), "readback")
+                tickets.append(ticket.value)
+                if len(tickets) >= 2:
+                    check(lib.vxa_wait_readback(ctx, tickets[-2]), "wait_readback")
+        if rank == 0:
+            check(lib.vxa_wait_readback(ctx, tickets[-1]), "wait_readback")
+        check(lib.vxa_synchronize(ctx), "sync")
         el = max_over_ranks(time.perf_counter() - t0)
         st2 = _abi.vxa_stats()
         lib.vxa_stats_read(ctx, C.byref(st2))
         if rank == 0:
-            lib.vxa_host_unregister(ctx, host_img.ctypes.data)
+            for b in bufs:
+                lib.vxa_host_unregister(ctx, b.ctypes.data)
         e2e = {"value": round(rays * args.e2e_steps / el / 1e6, 3), "unit": "Mrays/s",
                "h2d_bytes_per_step": int(st2.h2d_bytes // args.e2e_steps) * world,
                "d2h_bytes_per_step": W * H * 3, "ms_per_step": round(el * 1e3 / args.e2e_steps, 3),
                "path": "every rank: evaluate_animation + vxa_submit of its super-tiles (NVLink peer stores into "
-                       "rank 0); rank 0: RGB8 pack + D2H into a page-locked host image"}
+                       "rank 0) between vxa_frame_open/close; rank 0: RGB8 pack of the composed frame + D2H "
+                       "into a page-locked host image on its copy stream (overlapping the next frame)"
+                       if sync is not None else
+                       "every rank: evaluate_animation + vxa_submit; collective tile gather to rank 0; "
+                       "rank 0: RGB8 pack + D2H"}
+    sync_timeout = None
+    if sync is not None:
+        to = C.c_int32()
+        check(lib.vxa_sync_status(ctx, C.byref(to)), "sync_status")
+        sync_timeout = bool(max_over_ranks(float(to.value)))
+        if sync_timeout:
+            print(f"rank {rank}: a frame flag wait timed out", file=sys.stderr)
     if not args.no_e2e and world == 1:
         import numpy as np
 
@@ -686,16 +782,17 @@ def run_ours(args):
             hbo = C.c_uint32(0)
             if opt:
                 check(lib.vxa_hbo_create(ctx, 1920, 1080, C.byref(hbo)), "hbo_create")
-            for k in range(5):
+            # BASELINE config 2: the whole 120-frame sequence at 30 fps (t = k/30, k = 0..119)
+            steps_x = 120
+            for k in range(steps_x - 5, steps_x):
                 vxl.vxn_scene_submit(sc._h, frame_time(k, anim), prec, 0, 1, hbo.value)
             lib.vxa_synchronize(ctx)
             lib.vxa_stats_reset(ctx)
             tot = 0.0
-            steps_x = 60
             for k in range(steps_x):
                 lib.vxa_flush_l2(ctx)
                 lib.vxa_timer_begin(ctx)
-                if vxl.vxn_scene_submit(sc._h, frame_time(5 + k, anim) if anim else -1.0, prec, 0, 1, hbo.value) != 0:
+                if vxl.vxn_scene_submit(sc._h, frame_time(k, anim) if anim else -1.0, prec, 0, 1, hbo.value) != 0:
                     raise RuntimeError(vxl.vxn_last_error().decode())
                 msx = C.c_double()
                 lib.vxa_timer_end(ctx, C.byref(msx))
@@ -707,13 +804,42 @@ def run_ours(args):
             msf = tot / steps_x
             extras[name] = {"ms_per_frame": round(msf, 4), "fps": round(1000 / msf, 1),
                             "mrays_per_s": round(1920 * 1080 / msf / 1e3, 1), "frames": steps_x,
+                            "sequence": "t = k/30 s, k = 0..119" if anim else "static",
                             "pixels_reused_per_frame": int(stx.pixels_reused // steps_x),
                             "traversals_per_frame": int(stx.svo_traversals // steps_x)}
+        # the FP64 parity kernel (bit-exact vs the reference) on the headline workload
+        if args.precision == "fp32" and args.workload == "c4":
+            for k in range(3):
+                vxl.vxn_scene_submit(scene._h, frame_time(k, animated), _abi.VXA_FP64, 0, 1, 0)
+            lib.vxa_synchronize(ctx)
+            lib.vxa_stats_reset(ctx)
+            tot, nf = 0.0, 20
+            for k in range(nf):
+                lib.vxa_flush_l2(ctx)
+                lib.vxa_stream_delay(ctx, args.headstart_us)
+                lib.vxa_timer_begin(ctx)
+                if vxl.vxn_scene_submit(scene._h, frame_time(args.warmup + k, animated), _abi.VXA_FP64, 0, 1, 0) != 0:
+                    raise RuntimeError(vxl.vxn_last_error().decode())
+                msx = C.c_double()
+                lib.vxa_timer_end(ctx, C.byref(msx))
+                tot += msx.value
+            msf = tot / nf
+            extras["c4_fp64"] = {"ms_per_frame": round(msf, 4), "fps": round(1000 / msf, 1),
+                                 "mrays_per_s": round(W * H / msf / 1e3, 1), "frames": nf, "dtype": "f64",
+                                 "note": "FP64 parity kernel (reference operation order, bit-exact image, AOVs "
+                                         "and FrameStats), same workload, timing and L2 flush as value"}
         extras["animated_vs_static"] = round(extras["c2_animated_1080p"]["ms_per_frame"] /
                                              extras["c3_static_1080p"]["ms_per_frame"], 4)
         extras["model_build"] = model_build_bench(lib, ctx)
         extras["crowd_4096_4k"] = crowd_bench(lib, ctx, vxl, prec)
 
+    orc = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            orc = oracle_bytes(model, args.workload,
+                               [args.warmup + k * args.steps // 3 for k in range(3)] if animated else [0])
+        except Exception as e:  # reported beside the kernel-counted bytes, not required
+            print(f"bench: oracle byte count unavailable: {e}", file=sys.stderr)
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -722,6 +848,25 @@ def run_ours(args):
             base = {"value": None, "unit": "Mrays/s", "cores": None, "kind": "reference",
                     "sample": f"unavailable: {e}"}
 
+    # the roofline's algorithmic bytes: oracle-counted per ray (the reference's
+    # visits) x the rays of one launch; the kernel's own (pruned) counts beside it
+    alg_bytes_o = orc["bytes_per_ray"] * pixels_mine if orc else alg_bytes
+    achieved_o = alg_bytes_o / (kernel_ms / 1e3) / 1e9
+    launches = int(st.kernel_launches)
+    if dist is not None:  # every rank's kernels in the timed region
+        import torch
+
+        t = torch.tensor([launches], dtype=torch.int64, device="cpu" if args.same_device else f"cuda:{local}")
+        dist.all_reduce(t)
+        launches = int(t.item())
+    timed_region = (f"CUDA events on the context stream around each step: culling pre-pass + frame kernel "
+                    f"(the instance-table H2D is issued on the upload stream during the {args.headstart_us} us "
+                    f"stream delay that precedes the region, so host enqueue latency and the upload stay out; "
+                    f"e2e carries them)")
+    if world > 1:
+        timed_region += ("; N > 1: rank 0's events open before its go flag and close after every rank's done "
+                         "flag, so they enclose every rank's frame and the flag exchange; value uses the max "
+                         "over ranks")
     if rank == 0:
         cfg, shell, depth, _, _, _ = WORKLOADS[args.workload]
         line = {
@@ -737,14 +882,26 @@ def run_ours(args):
                                      f"64x64 super-tiles round-robin over {world} GPU(s)"),
                        "composition": composition,
                        "l2": "flushed between timed steps (256 MB write)" if not args.no_flush else "warm",
-                       "timed_region": f"device events around each step (instance-table upload, culling pre-pass, "
-                                       f"frame kernel), opened after a {args.headstart_us} us stream delay so host "
-                                       f"enqueue latency is not device time",
+                       "timed_region": timed_region,
+                       "frame_sync": (None if world == 1 else
+                                      "device flags (vxa_frame_open/close: go/done flags in rank 0's HBM, 1-thread "
+                                      "release/acquire kernels over NVLink, no host barrier)"
+                                      if sync == _abi.VXA_SYNC_DEVICE else
+                                      "host-polled flags (vxa_frame_open/close; ranks share one GPU)"
+                                      if sync == _abi.VXA_SYNC_HOST else
+                                      "host synchronisation + collective gather + barrier per frame"),
                        "model_bytes_device": None},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 5), "traffic": traffic,
+            "roofline": {"bound": "hbm", "achieved": round(achieved_o, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved_o / peak, 5), "traffic": traffic,
                          "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": round(alg_bytes),
+                         "algorithmic_bytes_per_launch": round(alg_bytes_o),
+                         "algorithmic_bytes_source": ("oracle-counted (SURVEY.md §8(d)): " + orc["sample"]
+                                                      if orc else "kernel-counted (no oracle sample at N > 1)"),
+                         "algorithmic_bytes_oracle": round(alg_bytes_o) if orc else None,
+                         "oracle_per_ray": ({k: round(v, 4) for k, v in orc.items() if k != "sample"}
+                                            if orc else None),
+                         "algorithmic_bytes_kernel_counted": round(alg_bytes),
+                         "achieved_kernel_counted": round(achieved, 2),
                          "kernel_ms": round(kernel_ms, 4),
                          "per_ray": {"node_fetches": round(st.node_fetches / frames / pixels_mine, 4),
                                      "leaf_hits": round(st.leaf_hits / frames / pixels_mine, 4),
@@ -754,21 +911,41 @@ def run_ours(args):
             "cpu_baseline": base,
             "e2e": e2e,
             "extras": extras,
-            "gpu_launches": int(st.kernel_launches),
+            "gpu_launches": launches,
             "multi_gpu_frame_identical": multi_ok,
+            "frame_sync_timed_out": sync_timeout,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
-    return 0
+    return 1 if sync_timeout else 0
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without a launcher: start N ranks under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     args = parse()
+    rank, world, _ = dist_env()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     return run_ours(args)
 
 

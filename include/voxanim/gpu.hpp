@@ -44,10 +44,17 @@ void render_frame_into(const Scene& scene, const RenderOptions& opts, const Rend
 // Process-wide CUDA context (device from VOXANIM_DEVICE, default 0).
 vxa_ctx* context();
 
-// Device handle of a model, uploading it on first use. The cache is keyed by
-// the model's storage (node/attribute buffers, sizes, depth) plus a content
-// signature, so distinct models never alias.
+// Device handle of a model, uploading it on first use. Scene models
+// (shared_ptr<const SvoModel>, scene.hpp:20) are keyed by their owner (a
+// weak_ptr holds the control block, so the key is never reused by another
+// model; the device copy is released once the model is destroyed) plus a
+// storage/content check; a bare reference (traverse API) is keyed by its
+// storage (node/attribute buffers, sizes, depth) plus a content signature.
+std::uint32_t model_handle(const std::shared_ptr<const SvoModel>& model);
 std::uint32_t model_handle(const SvoModel& model);
+// Starts assembling a frame's instance table: handles returned from here on are
+// not evicted by the model cache until the next call.
+std::uint64_t begin_model_frame();
 
 // voxanim::build_from_grid on the device (vxa_build_model): the same SvoModel,
 // byte for byte, built in HBM and copied back; the device copy is kept in the

@@ -248,6 +248,39 @@ void* vxa_stream(vxa_ctx* ctx);
 int vxa_fb_export(vxa_ctx* ctx, int32_t width, int32_t height, void* ipc_handle_out);
 int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_handle); /* NULL: detach */
 
+/* Frame completion across ranks without a host barrier. The reference's frame
+ * is complete when every row-band thread has joined (renderer.cpp:268-287);
+ * across GPUs the same point is "every rank's super-tiles are in rank 0's
+ * framebuffer". Rank 0 exports a small flag block {go, done[world]} in its HBM
+ * (vxa_sync_export, 64-byte CUDA IPC handle); every other rank imports it.
+ * Per frame, every rank calls vxa_frame_open before submitting and
+ * vxa_frame_close after it (the same number of times on every rank; frames are
+ * numbered by the calls):
+ *   rank 0: open stores go = frame; close waits until done[r] == frame for all r;
+ *   rank r: open waits until go == frame; close stores done[r] = frame.
+ * mode VXA_SYNC_DEVICE: the stores and waits are 1-thread kernels on the
+ * context stream (system-scope release stores / acquire loads over NVLink),
+ * so the host never blocks and rank 0's stream ends the frame only when the
+ * whole frame has landed; a wait gives up after timeout_ms and latches an
+ * error that vxa_sync_status reports. Only for ranks on distinct GPUs: kernels
+ * that wait on one another must never share a device.
+ * mode VXA_SYNC_HOST: the waits are host polls of the flags (ranks sharing one
+ * device: a correctness run of the same protocol). */
+#define VXA_SYNC_DEVICE 0
+#define VXA_SYNC_HOST 1
+int vxa_sync_export(vxa_ctx* ctx, int32_t world, void* ipc_handle_out);
+int vxa_sync_import(vxa_ctx* ctx, int32_t rank, int32_t world, const void* ipc_handle);
+int vxa_sync_configure(vxa_ctx* ctx, int32_t mode, uint32_t timeout_ms);
+int vxa_frame_open(vxa_ctx* ctx);
+int vxa_frame_close(vxa_ctx* ctx);
+/* 0 when no wait has timed out (synchronises the context stream). */
+int vxa_sync_status(vxa_ctx* ctx, int32_t* timed_out);
+/* Streaming readback of the resident (composed) framebuffer: its RGB8 pack on
+ * the context stream (after everything enqueued so far, e.g. vxa_frame_close)
+ * and the D2H into rgb_out on the copy stream; same tickets as
+ * vxa_submit_readback. */
+int vxa_framebuffer_readback(vxa_ctx* ctx, int32_t width, int32_t height, uint8_t* rgb_out, uint64_t* ticket);
+
 /* Screen partition used when tile_world > 1: the rank that renders pixel
  * (x, y) of a width-wide frame split over `world` devices (64x64 super-tiles,
  * round-robin). Pure function, no device needed. */

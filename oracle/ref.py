@@ -55,6 +55,7 @@ def lib() -> C.CDLL:
             "vref_last_error": (C.c_char_p,),
             "vref_model_deserialize": (P, P, C.c_size_t),
             "vref_model_dense_sphere": (P, u32),
+            "vref_model_load": (P, C.c_char_p),
             "vref_model_shell_grid": (P, u32),
             "vref_model_random": (P, u64, u32, d),
             "vref_model_from_grid": (P, P, u32, u32, u32),
@@ -110,6 +111,11 @@ class RefModel:
     def from_bytes(cls, data: bytes):
         buf = C.create_string_buffer(data, len(data))
         return cls(lib().vref_model_deserialize(buf, len(data)))
+
+    @classmethod
+    def load(cls, path: str):
+        """The reference load_svo (svo.cpp) of a .svo file."""
+        return cls(lib().vref_model_load(path.encode()))
 
     @classmethod
     def dense_sphere(cls, depth):

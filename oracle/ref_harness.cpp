@@ -390,6 +390,11 @@ VREF_API vref_model* vref_model_deserialize(const uint8_t* bytes, size_t n) {
     return guard([&] { return wrap(deserialize(std::span<const std::uint8_t>(bytes, n))); }, (vref_model*)nullptr);
 }
 
+// The reference's own file loader (svo.cpp: load_svo -> deserialize).
+VREF_API vref_model* vref_model_load(const char* path) {
+    return guard([&] { return wrap(load_svo(path)); }, (vref_model*)nullptr);
+}
+
 VREF_API vref_model* vref_model_dense_sphere(uint32_t depth) {
     return guard([&] { return wrap(build_from_grid(gen_primitive(PrimitiveKind::Sphere, depth), depth)); },
                  (vref_model*)nullptr);

@@ -15,6 +15,7 @@ LIB_DIR = os.environ.get("VOXANIM_LIB_DIR") or os.path.join(os.path.dirname(os.p
 
 VXA_OK, VXA_ERR_INVALID, VXA_ERR_MODEL, VXA_ERR_CUDA, VXA_ERR_OOM, VXA_ERR_NO_DEVICE = range(6)
 VXA_FP32, VXA_FP64 = 0, 1
+VXA_SYNC_DEVICE, VXA_SYNC_HOST = 0, 1
 
 
 class vxa_camera(C.Structure):
@@ -174,6 +175,8 @@ VXA_SYMBOLS = [
     "vxa_wait_readback", "vxa_synchronize", "vxa_stats_read", "vxa_stats_reset", "vxa_read_framebuffer",
     "vxa_host_register", "vxa_host_unregister", "vxa_timer_begin", "vxa_timer_end", "vxa_flush_l2", "vxa_stream_delay", "vxa_stream",
     "vxa_fb_export", "vxa_fb_import", "vxa_tile_owner", "vxa_tiles_count", "vxa_tiles_pack", "vxa_tiles_unpack", "vxa_traverse",
+    "vxa_sync_export", "vxa_sync_import", "vxa_sync_configure", "vxa_frame_open", "vxa_frame_close", "vxa_sync_status",
+    "vxa_framebuffer_readback",
 ]
 VXN_SYMBOLS = [
     "vxn_last_error", "vxn_model_procedural", "vxn_model_dense_sphere", "vxn_model_random", "vxn_model_full_cube",
@@ -239,6 +242,13 @@ def load_vxa(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxa_tiles_count", i, i, i, i, i, C.POINTER(u32))
     _declare(lib, "vxa_tiles_pack", i, P, i, i, i, i, P)
     _declare(lib, "vxa_tiles_unpack", i, P, i, i, i, i, P)
+    _declare(lib, "vxa_sync_export", i, P, C.c_int32, P)
+    _declare(lib, "vxa_sync_import", i, P, C.c_int32, C.c_int32, P)
+    _declare(lib, "vxa_sync_configure", i, P, C.c_int32, u32)
+    _declare(lib, "vxa_frame_open", i, P)
+    _declare(lib, "vxa_frame_close", i, P)
+    _declare(lib, "vxa_sync_status", i, P, C.POINTER(C.c_int32))
+    _declare(lib, "vxa_framebuffer_readback", i, P, C.c_int32, C.c_int32, P, C.POINTER(u64))
     return lib
 
 

@@ -425,6 +425,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 if (cnt <= kListCap) list_n = cnt;
             }
         }
+        // warp-uniform: no lane of the tile leaves the frame (the RGB8 store gathers across lanes)
+        const bool tile_inside = tx0 + kTileW <= p.width && ty0 + kTileH <= p.height;
         if (px >= p.width || py >= p.height) continue;
         const size_t pix = static_cast<size_t>(py) * static_cast<size_t>(p.width) + static_cast<size_t>(px);
 
@@ -599,10 +601,29 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         if (best.have) ++n_leaf;
         p.fb[pix] = rgba;
         if (p.rgb != nullptr) { // streamed frame: the readback's RGB8 bytes too (no pack pass)
-            uint8_t* o = p.rgb + 3 * pix;
-            o[0] = static_cast<uint8_t>(rgba);
-            o[1] = static_cast<uint8_t>(rgba >> 8);
-            o[2] = static_cast<uint8_t>(rgba >> 16);
+            if (kTileW == 8 && tile_inside && (p.width & 3) == 0) {
+                // A tile row is 8 pixels = 24 contiguous RGB8 bytes = six 4-byte words
+                // (4-aligned: 3 (y W + x0) with W % 4 == 0 and x0 % 8 == 0). Lane j < 6
+                // of each row gathers the two pixels its word covers (bytes 4j .. 4j+3
+                // = pixels 4j/3 and 4j/3 + 1) and stores the word: 24 lanes x 4 B.
+                const uint32_t r = lane >> 3, j = lane & 7u;
+                const uint32_t q0 = (4u * j) / 3u;
+                const uint32_t src0 = (r << 3) + min(q0, 7u), src1 = (r << 3) + min(q0 + 1u, 7u);
+                const uint32_t v0 = __shfl_sync(0xffffffffu, rgba, src0);
+                const uint32_t v1 = __shfl_sync(0xffffffffu, rgba, src1);
+                const uint32_t j3 = j - 3u * (j / 3u);
+                const uint32_t sel = j3 == 0 ? 0x4210u : (j3 == 1 ? 0x5421u : 0x6542u);
+                if (j < 6u) {
+                    const size_t row = static_cast<size_t>(ty0 + static_cast<int>(r)) * static_cast<size_t>(p.width) +
+                                       static_cast<size_t>(tx0);
+                    *reinterpret_cast<uint32_t*>(p.rgb + 3 * row + 4 * j) = __byte_perm(v0, v1, sel);
+                }
+            } else {
+                uint8_t* o = p.rgb + 3 * pix;
+                o[0] = static_cast<uint8_t>(rgba);
+                o[1] = static_cast<uint8_t>(rgba >> 8);
+                o[2] = static_cast<uint8_t>(rgba >> 16);
+            }
         }
 
         if constexpr (kAov) {
@@ -625,6 +646,9 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         }
     }
 
+    // multi-GPU: this thread's peer stores are performed system-wide before the
+    // rank's completion flag (vxa_frame_close) can be written
+    if (p.fence_sys) __threadfence_system();
     // warp-aggregated counters: traversals, reuse, node fetches, leaf hits
     const uint32_t vals[4] = {n_trav, n_reuse, n_fetch, n_leaf};
 #pragma unroll

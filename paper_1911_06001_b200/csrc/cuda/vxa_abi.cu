@@ -169,6 +169,20 @@ struct vxa_ctx {
     uint32_t* peer_fb = nullptr; // rank 0's framebuffer mapped via CUDA IPC
     int32_t peer_w = 0, peer_h = 0;
 
+    // Frame completion flags (vxa_frame_open/close): rank 0 owns the block
+    // {go, pad, done[kSyncRanks]} in its HBM, other ranks map it via CUDA IPC.
+    static constexpr int kSyncRanks = 64;
+    DevBuf<unsigned int> sync_own;     // rank 0: the flag block
+    unsigned int* sync_peer = nullptr; // rank r: rank 0's block, peer-mapped
+    unsigned int* sync_flags = nullptr; // the block this rank addresses (own or peer)
+    DevBuf<unsigned int> sync_err;     // latched by a wait that timed out
+    int32_t sync_rank = 0, sync_world = 1;
+    int32_t sync_mode = VXA_SYNC_DEVICE;
+    uint64_t sync_timeout_ns = 10ull * 1000 * 1000 * 1000;
+    uint32_t sync_seq = 0; // frames opened so far
+    cudaStream_t poll_stream = nullptr; // VXA_SYNC_HOST flag reads
+    unsigned int* sync_host = nullptr;  // pinned, kSyncRanks + 2 words
+
     DevBuf<uint32_t> tile_counter;
     DevBuf<unsigned long long> counters;
     unsigned long long* counters_host = nullptr; // pinned, 8 counters
@@ -450,6 +464,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     ctx->n_rays += my_pixels;
     if (p.sphere_pass) ctx->n_sphere_tests += my_pixels * n;
     p.fb = target;
+    p.fence_sys = target != ctx->fb.ptr ? 1u : 0u; // peer stores: fenced before vxa_frame_close's flag
     p.rgb = ctx->next_rgb; // set by vxa_submit_readback for this frame only
     if (p.rgb != nullptr && ctx->next_rgb_free != nullptr) VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->next_rgb_free, 0));
     p.max_depth = 1;
@@ -477,6 +492,10 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
             p.top_n = std::min<uint32_t>(kSmemTopWords, nodes) & ~3u;
         }
     }
+    // VOXANIM_CONTENT_BOUND=off disables the FP32 content-sphere skip (tests: the
+    // bound must never change a frame); read per frame
+    if (const char* env = std::getenv("VOXANIM_CONTENT_BOUND"); env && std::strcmp(env, "off") == 0)
+        for (uint32_t k = 0; k < n; ++k) tab[k].model.content_r2 = 1.0f;
     // VOXANIM_NODE_WORDS=wide forces the general words (tests, A/B timing); read per frame
     if (const char* env = std::getenv("VOXANIM_NODE_WORDS"); env && std::strcmp(env, "wide") == 0) p.compact = 0;
     p.tile_counter = ctx->tile_counter.ptr;
@@ -666,6 +685,11 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->build.pyramid.release();
     ctx->build.levels.release();
     if (ctx->peer_fb) cudaIpcCloseMemHandle(ctx->peer_fb);
+    if (ctx->sync_peer) cudaIpcCloseMemHandle(ctx->sync_peer);
+    ctx->sync_own.release();
+    ctx->sync_err.release();
+    if (ctx->sync_host) cudaFreeHost(ctx->sync_host);
+    if (ctx->poll_stream) cudaStreamDestroy(ctx->poll_stream);
     for (auto& [h, b] : ctx->hbos) cudaFree(b.rec);
     ctx->fb.release();
     ctx->tile_counter.release();
@@ -978,6 +1002,11 @@ int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, ui
             m.raw, static_cast<uint32_t>(b.node_count), m.words, nullptr);
         e = cudaGetLastError();
     }
+    // the builder's leaf extent (content bound, below): read under the same synchronisation
+    if (e == cudaSuccess && ctx->counters_host == nullptr)
+        e = cudaMallocHost(&ctx->counters_host, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->counters_host, b.extent_dev, sizeof(unsigned int), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
         cudaStreamSynchronize(ctx->stream);
@@ -995,7 +1024,7 @@ int vxa_build_model(vxa_ctx* ctx, const uint64_t* grid_words, uint32_t depth, ui
     {
         // content bound: the farthest leaf corner, reduced on the device by the builder
         unsigned int bits = 0;
-        VXA_CUDA(cudaMemcpy(&bits, b.extent_dev, sizeof(bits), cudaMemcpyDeviceToHost));
+        std::memcpy(&bits, ctx->counters_host, sizeof(bits));
         float r2;
         std::memcpy(&r2, &bits, sizeof(r2));
         m.dev.content_r2 = content_bound(static_cast<double>(r2));
@@ -1395,6 +1424,198 @@ int vxa_fb_import(vxa_ctx* ctx, int32_t width, int32_t height, const void* ipc_h
     ctx->peer_fb = static_cast<uint32_t*>(p);
     ctx->peer_w = width;
     ctx->peer_h = height;
+    return VXA_OK;
+}
+
+namespace {
+// ---- frame completion flags (vxa_frame_open / vxa_frame_close) -------------
+// One thread each. The store is a system-scope release after a full fence, so
+// every write this device made before it (the frame kernel's peer stores into
+// rank 0's framebuffer, themselves fenced at system scope by their threads)
+// is visible to a thread that acquires the flag. The wait spins with
+// system-scope acquire loads (the flags are written over NVLink) and gives up
+// after timeout_ns, latching err: a lost rank never hangs the device.
+__global__ void sync_store_kernel(unsigned int* flag, unsigned int v) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned int load_acquire_sys(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// flags[0 .. n) must all reach v (frame numbers increase by one per frame;
+// the difference is compared as a signed value, so wrap-around is harmless).
+__global__ void sync_wait_kernel(const unsigned int* flags, int n, unsigned int v, unsigned long long timeout_ns,
+                                 unsigned int* err) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int i = 0; i < n; ++i) {
+        unsigned int ns = 32;
+        while (static_cast<int>(load_acquire_sys(flags + i) - v) < 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) {
+                atomicOr(err, 1u);
+                return;
+            }
+            __nanosleep(ns);
+            ns = ns < 1024 ? 2 * ns : ns;
+        }
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+// VXA_SYNC_HOST: poll flags[0 .. n) from the host until all reach v.
+int host_poll(vxa_ctx* ctx, const unsigned int* flags, int n, unsigned int v) {
+    const auto t0 = std::chrono::steady_clock::now();
+    while (true) {
+        VXA_CUDA(cudaMemcpyAsync(ctx->sync_host, flags, sizeof(unsigned int) * n, cudaMemcpyDeviceToHost,
+                                 ctx->poll_stream));
+        VXA_CUDA(cudaStreamSynchronize(ctx->poll_stream));
+        bool all = true;
+        for (int i = 0; i < n && all; ++i) all = static_cast<int>(ctx->sync_host[i] - v) >= 0;
+        if (all) return VXA_OK;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms * 1e6 > static_cast<double>(ctx->sync_timeout_ns))
+            return fail(VXA_ERR_CUDA, "vxa_frame sync: timed out waiting for another rank");
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
+int sync_common(vxa_ctx* ctx, int32_t rank, int32_t world) {
+    if (world < 2 || world > vxa_ctx::kSyncRanks || rank < 0 || rank >= world)
+        return fail(VXA_ERR_INVALID, "sync: rank/world out of range");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    VXA_CUDA(ctx->sync_err.ensure(1));
+    VXA_CUDA(cudaMemset(ctx->sync_err.ptr, 0, sizeof(unsigned int)));
+    if (ctx->poll_stream == nullptr) VXA_CUDA(cudaStreamCreateWithFlags(&ctx->poll_stream, cudaStreamNonBlocking));
+    if (ctx->sync_host == nullptr)
+        VXA_CUDA(cudaMallocHost(&ctx->sync_host, sizeof(unsigned int) * (vxa_ctx::kSyncRanks + 2)));
+    ctx->sync_rank = rank;
+    ctx->sync_world = world;
+    ctx->sync_seq = 0;
+    return VXA_OK;
+}
+} // namespace
+
+int vxa_sync_export(vxa_ctx* ctx, int32_t world, void* ipc_handle_out) {
+    if (ctx == nullptr || ipc_handle_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (int rc = sync_common(ctx, 0, world); rc != VXA_OK) return rc;
+    VXA_CUDA(ctx->sync_own.ensure(vxa_ctx::kSyncRanks + 2));
+    VXA_CUDA(cudaMemset(ctx->sync_own.ptr, 0, sizeof(unsigned int) * (vxa_ctx::kSyncRanks + 2)));
+    cudaIpcMemHandle_t h;
+    VXA_CUDA(cudaIpcGetMemHandle(&h, ctx->sync_own.ptr));
+    std::memcpy(ipc_handle_out, &h, sizeof(h));
+    ctx->sync_flags = ctx->sync_own.ptr;
+    return VXA_OK;
+}
+
+int vxa_sync_import(vxa_ctx* ctx, int32_t rank, int32_t world, const void* ipc_handle) {
+    if (ctx == nullptr || ipc_handle == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (rank == 0) return fail(VXA_ERR_INVALID, "sync: rank 0 exports the flag block");
+    if (int rc = sync_common(ctx, rank, world); rc != VXA_OK) return rc;
+    if (ctx->sync_peer) {
+        cudaIpcCloseMemHandle(ctx->sync_peer);
+        ctx->sync_peer = nullptr;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof(h));
+    void* p = nullptr;
+    VXA_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->sync_peer = static_cast<unsigned int*>(p);
+    ctx->sync_flags = ctx->sync_peer;
+    return VXA_OK;
+}
+
+int vxa_sync_configure(vxa_ctx* ctx, int32_t mode, uint32_t timeout_ms) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (mode != VXA_SYNC_DEVICE && mode != VXA_SYNC_HOST) return fail(VXA_ERR_INVALID, "sync: unknown mode");
+    ctx->sync_mode = mode;
+    if (timeout_ms > 0) ctx->sync_timeout_ns = static_cast<uint64_t>(timeout_ms) * 1000000ull;
+    return VXA_OK;
+}
+
+int vxa_frame_open(vxa_ctx* ctx) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (ctx->sync_flags == nullptr) return fail(VXA_ERR_INVALID, "sync: no flag block (vxa_sync_export/import)");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const unsigned int v = ++ctx->sync_seq;
+    if (ctx->sync_rank == 0) {
+        sync_store_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sync_flags, v);
+        ++ctx->aux_launches;
+    } else if (ctx->sync_mode == VXA_SYNC_DEVICE) {
+        sync_wait_kernel<<<1, 1, 0, ctx->stream>>>(ctx->sync_flags, 1, v, ctx->sync_timeout_ns, ctx->sync_err.ptr);
+        ++ctx->aux_launches;
+    } else {
+        if (int rc = host_poll(ctx, ctx->sync_flags, 1, v); rc != VXA_OK) return rc;
+    }
+    VXA_CUDA(cudaGetLastError());
+    return VXA_OK;
+}
+
+int vxa_frame_close(vxa_ctx* ctx) {
+    if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (ctx->sync_flags == nullptr) return fail(VXA_ERR_INVALID, "sync: no flag block (vxa_sync_export/import)");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const unsigned int v = ctx->sync_seq;
+    unsigned int* done = ctx->sync_flags + 2; // done[r] at word 2 + r
+    if (ctx->sync_rank != 0) {
+        sync_store_kernel<<<1, 1, 0, ctx->stream>>>(done + ctx->sync_rank, v);
+        ++ctx->aux_launches;
+    } else if (ctx->sync_mode == VXA_SYNC_DEVICE) {
+        sync_wait_kernel<<<1, 1, 0, ctx->stream>>>(done + 1, ctx->sync_world - 1, v, ctx->sync_timeout_ns,
+                                                   ctx->sync_err.ptr);
+        ++ctx->aux_launches;
+    } else {
+        if (int rc = host_poll(ctx, done + 1, ctx->sync_world - 1, v); rc != VXA_OK) return rc;
+    }
+    VXA_CUDA(cudaGetLastError());
+    return VXA_OK;
+}
+
+int vxa_sync_status(vxa_ctx* ctx, int32_t* timed_out) {
+    if (ctx == nullptr || timed_out == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    *timed_out = 0;
+    if (ctx->sync_err.ptr == nullptr) return VXA_OK;
+    unsigned int e = 0;
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    VXA_CUDA(cudaMemcpy(&e, ctx->sync_err.ptr, sizeof(e), cudaMemcpyDeviceToHost));
+    *timed_out = e ? 1 : 0;
+    return VXA_OK;
+}
+
+int vxa_framebuffer_readback(vxa_ctx* ctx, int32_t width, int32_t height, uint8_t* rgb_out, uint64_t* ticket) {
+    if (ctx == nullptr || rgb_out == nullptr || ticket == nullptr) return fail(VXA_ERR_INVALID, "null argument");
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+    if (width != ctx->fb_w || height != ctx->fb_h || ctx->fb.ptr == nullptr)
+        return fail(VXA_ERR_INVALID, "framebuffer size mismatch");
+    VXA_CUDA(cudaSetDevice(ctx->device));
+    const size_t npix = static_cast<size_t>(width) * height;
+    const int slot = static_cast<int>(ctx->rb_next & 1u);
+    VXA_CUDA(ctx->rb_rgb[slot].ensure(npix * 3 + 16));
+    VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->rb_done[slot], 0)); // the slot's previous D2H
+    const size_t quads = (npix + 3) / 4;
+    pack_rgb<<<static_cast<unsigned>((quads + 255) / 256), 256, 0, ctx->stream>>>(ctx->fb.ptr, ctx->rb_rgb[slot].ptr,
+                                                                                  npix);
+    VXA_CUDA(cudaGetLastError());
+    ++ctx->aux_launches;
+    VXA_CUDA(cudaEventRecord(ctx->rb_packed[slot], ctx->stream));
+    if (int rc = flush_readback(ctx); rc != VXA_OK) return rc;
+    ctx->rb_pending = true;
+    ctx->rb_pending_slot = slot;
+    ctx->rb_pending_out = rgb_out;
+    ctx->rb_pending_bytes = npix * 3;
+    ctx->d2h += npix * 3;
+    *ticket = ctx->rb_next++;
     return VXA_OK;
 }
 

@@ -198,6 +198,7 @@ template <typename Real> struct FrameParams {
     uint32_t n_tiles; // warp tiles owned by this rank
     uint32_t max_depth; // deepest model of the frame (FP32 shared-memory stack height)
     uint32_t compact;   // every model has compact 4-byte words (FP32 kernel)
+    uint32_t fence_sys; // fb is another GPU's framebuffer: every thread fences its stores at system scope
     // outputs
     uint32_t* fb;                 // RGBA8 framebuffer (local or peer-mapped)
     uint8_t* rgb;                 // streamed frames: RGB8 copy for the readback (or null)

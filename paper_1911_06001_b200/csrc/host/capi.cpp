@@ -255,6 +255,7 @@ void export_frame(const voxanim::Scene& sc, vxa_frame_desc* f) {
 void export_instances(const voxanim::Scene& sc, vxa_instance* inst) {
     const voxanim::SvoModel* last = nullptr;
     std::uint32_t last_handle = 0;
+    voxanim::gpu::begin_model_frame();
     for (std::size_t i = 0; i < sc.objects.size(); ++i) {
         const voxanim::SceneObject& o = sc.objects[i];
         vxa_instance& v = inst[i];
@@ -263,7 +264,7 @@ void export_instances(const voxanim::Scene& sc, vxa_instance* inst) {
         if (o.model) {
             if (o.model.get() != last) {
                 last = o.model.get();
-                last_handle = voxanim::gpu::model_handle(*o.model);
+                last_handle = voxanim::gpu::model_handle(o.model);
             }
             v.model = last_handle;
         }

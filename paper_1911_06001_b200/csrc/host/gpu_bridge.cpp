@@ -2,7 +2,9 @@
 // model cache and status -> exception translation.
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -17,6 +19,13 @@ vxa_ctx* g_ctx = nullptr;
 int g_precision = -1; // -1: read VOXANIM_PRECISION on first use
 
 struct CachedModel {
+    // Scene models (shared_ptr<const SvoModel>, scene.hpp:20): keyed by the
+    // owner's control block, which this weak_ptr keeps allocated, so a later
+    // model can never reuse the key; the entry is released once the model is
+    // gone. Raw references (traverse API) use the storage key below only.
+    std::weak_ptr<const SvoModel> owner;
+    bool owned;
+    std::uint64_t frame; // frame generation that last used the handle (never evicted within it)
     const void* nodes;
     const void* attrs;
     std::size_t node_count, attr_count;
@@ -28,6 +37,7 @@ struct CachedModel {
 
 std::list<CachedModel> g_cache; // most recently used first
 std::uint64_t g_cache_bytes = 0;
+std::uint64_t g_frame = 1; // current frame generation (begin_model_frame)
 
 std::uint64_t mix64(std::uint64_t h, std::uint64_t v) {
     h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
@@ -103,35 +113,105 @@ void set_default_precision(Precision p) {
     g_precision = static_cast<int>(p);
 }
 
-std::uint32_t model_handle(const SvoModel& m) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    vxa_ctx* ctx = ctx_locked();
-    const std::uint64_t sig = signature(m);
-    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
-        if (it->nodes == m.nodes.data() && it->attrs == m.attributes.data() && it->node_count == m.nodes.size() &&
-            it->attr_count == m.attributes.size() && it->depth == m.depth && it->signature == sig) {
-            g_cache.splice(g_cache.begin(), g_cache, it);
-            return g_cache.front().handle;
+namespace {
+
+bool same_storage(const CachedModel& c, const SvoModel& m, std::uint64_t sig) {
+    return c.nodes == m.nodes.data() && c.attrs == m.attributes.data() && c.node_count == m.nodes.size() &&
+           c.attr_count == m.attributes.size() && c.depth == m.depth && c.signature == sig;
+}
+
+// Releases the device copies of scene models that no longer exist.
+void purge_expired(vxa_ctx* ctx) {
+    for (auto it = g_cache.begin(); it != g_cache.end();) {
+        if (it->owned && it->owner.expired()) {
+            vxa_release_model(ctx, it->handle);
+            g_cache_bytes -= it->bytes;
+            it = g_cache.erase(it);
+        } else {
+            ++it;
         }
     }
+}
+
+std::uint32_t upload_locked(vxa_ctx* ctx, const SvoModel& m, std::uint64_t sig,
+                            const std::shared_ptr<const SvoModel>* owner) {
     std::uint32_t handle = 0;
     check(vxa_upload_model(ctx, m.nodes.data(), static_cast<std::uint32_t>(m.nodes.size()), m.attributes.data(),
                            static_cast<std::uint32_t>(m.attributes.size()), m.depth, &handle),
           "vxa_upload_model");
     std::uint64_t bytes = 0;
     vxa_model_info(ctx, handle, &bytes, nullptr);
-    g_cache.push_front({m.nodes.data(), m.attributes.data(), m.nodes.size(), m.attributes.size(), m.depth, sig, handle,
-                        bytes});
+    g_cache.push_front({owner ? std::weak_ptr<const SvoModel>(*owner) : std::weak_ptr<const SvoModel>(), owner != nullptr,
+                        g_frame, m.nodes.data(), m.attributes.data(), m.nodes.size(), m.attributes.size(), m.depth, sig,
+                        handle, bytes});
     g_cache_bytes += bytes;
-    // Evict least recently used models beyond the budget (never the new one).
+    // Evict least recently used models beyond the budget: never the new one, nor
+    // one a frame being assembled already holds (same generation).
     const std::uint64_t budget = cache_budget();
-    while (g_cache_bytes > budget && g_cache.size() > 1) {
-        const CachedModel& victim = g_cache.back();
-        vxa_release_model(ctx, victim.handle);
-        g_cache_bytes -= victim.bytes;
-        g_cache.pop_back();
+    for (auto it = std::prev(g_cache.end()); g_cache_bytes > budget && it != g_cache.begin();) {
+        auto victim = it--;
+        if (victim->frame == g_frame) continue;
+        vxa_release_model(ctx, victim->handle);
+        g_cache_bytes -= victim->bytes;
+        g_cache.erase(victim);
     }
     return handle;
+}
+
+} // namespace
+
+std::uint64_t begin_model_frame() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return ++g_frame;
+}
+
+std::uint32_t model_handle(const std::shared_ptr<const SvoModel>& model) {
+    if (!model) throw ValidationError("null model");
+    std::lock_guard<std::mutex> lk(g_mu);
+    vxa_ctx* ctx = ctx_locked();
+    purge_expired(ctx);
+    const SvoModel& m = *model;
+    const std::uint64_t sig = signature(m);
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+        if (!it->owned || it->owner.owner_before(model) || model.owner_before(it->owner)) continue;
+        if (same_storage(*it, m, sig)) {
+            it->frame = g_frame;
+            g_cache.splice(g_cache.begin(), g_cache, it);
+            return g_cache.front().handle;
+        }
+        // the same owner with different contents (edited in place): re-upload
+        vxa_release_model(ctx, it->handle);
+        g_cache_bytes -= it->bytes;
+        g_cache.erase(it);
+        break;
+    }
+    // a device copy made for the same storage before the model was shared (e.g.
+    // build_from_grid's, or a traverse call's) is adopted by its owner
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+        if (!it->owned && same_storage(*it, m, sig)) {
+            it->owner = model;
+            it->owned = true;
+            it->frame = g_frame;
+            g_cache.splice(g_cache.begin(), g_cache, it);
+            return g_cache.front().handle;
+        }
+    }
+    return upload_locked(ctx, m, sig, &model);
+}
+
+std::uint32_t model_handle(const SvoModel& m) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    vxa_ctx* ctx = ctx_locked();
+    purge_expired(ctx);
+    const std::uint64_t sig = signature(m);
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+        if (!it->owned && same_storage(*it, m, sig)) {
+            it->frame = g_frame;
+            g_cache.splice(g_cache.begin(), g_cache, it);
+            return g_cache.front().handle;
+        }
+    }
+    return upload_locked(ctx, m, sig, nullptr);
 }
 
 SvoModel build_from_grid(const VoxelGrid& grid, std::uint32_t depth) {
@@ -164,8 +244,8 @@ SvoModel build_from_grid(const VoxelGrid& grid, std::uint32_t depth) {
     }
     std::uint64_t bytes = 0;
     vxa_model_info(ctx, handle, &bytes, nullptr);
-    g_cache.push_front({m.nodes.data(), m.attributes.data(), m.nodes.size(), m.attributes.size(), m.depth, signature(m),
-                        handle, bytes});
+    g_cache.push_front({std::weak_ptr<const SvoModel>(), false, g_frame, m.nodes.data(), m.attributes.data(),
+                        m.nodes.size(), m.attributes.size(), m.depth, signature(m), handle, bytes});
     g_cache_bytes += bytes;
     return m;
 }

@@ -183,6 +183,7 @@ void render_frame_into(const Scene& scene, const RenderOptions& opts, const Rend
 
     std::vector<vxa_instance> inst(scene.objects.size());
     std::unordered_map<const SvoModel*, std::uint32_t> handles;
+    begin_model_frame();
     for (std::size_t i = 0; i < scene.objects.size(); ++i) {
         const SceneObject& o = scene.objects[i];
         vxa_instance& v = inst[i];
@@ -190,7 +191,7 @@ void render_frame_into(const Scene& scene, const RenderOptions& opts, const Rend
         v.id = o.id;
         if (o.model) {
             auto [it, fresh] = handles.try_emplace(o.model.get(), 0u);
-            if (fresh) it->second = model_handle(*o.model);
+            if (fresh) it->second = model_handle(o.model);
             v.model = it->second;
         }
         std::copy(o.transform.rotation.m.begin(), o.transform.rotation.m.end(), v.rotation);

@@ -91,6 +91,31 @@ def test_built_model_content_bound_renders_like_uploaded_fp32(gpu, prim, depth):
         assert (a == b).all(), (prim, cfg)
 
 
+@pytest.mark.parametrize("prim,depth", [("sphere", 7), ("box_shell", 6), ("menger", 6), ("full", 5)])
+def test_built_model_content_bound_never_changes_a_frame(gpu, prim, depth, monkeypatch):
+    """The content bound is only a skip: FP32 frames of device-built models with
+    the content-sphere test on and off (VOXANIM_CONTENT_BOUND=off) agree pixel for
+    pixel -- incl. models whose leaves reach the cube's corners (box shell, full
+    cube: the bound must not cut them) -- in the C1 view and the C4 layout."""
+    if prim == "full":
+        n = 1 << depth
+        words = np.full((n ** 3 + 63) // 64, np.iinfo(np.uint64).max, np.uint64)
+        gd = depth
+    else:
+        words, gd = vx.grid_primitive(prim, depth)
+    built = vx.Model.from_grid(words, gd, device=True)
+    for cfg, w, h in ((vx.config.C1, 0, 0), (vx.config.C4, 480, 270)):
+        sc = vx.Scene(cfg, [built], 0, w, h)
+        sc.evaluate(0.7)
+        monkeypatch.delenv("VOXANIM_CONTENT_BOUND", raising=False)
+        on = sc.render(precision=vx.VXA_FP32)[0]
+        monkeypatch.setenv("VOXANIM_CONTENT_BOUND", "off")
+        off = sc.render(precision=vx.VXA_FP32)[0]
+        monkeypatch.delenv("VOXANIM_CONTENT_BOUND")
+        assert (on == off).all(), (prim, cfg)
+        assert (on != 0).any()
+
+
 def test_c_abi_build_download_and_errors(gpu):
     lib = vx.vxa()
     ctx = vx.context()

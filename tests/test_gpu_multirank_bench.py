@@ -38,3 +38,19 @@ def test_two_ranks_compose_the_single_device_frame(gpu, compose, port, flag):
     assert "sharing one GPU" in d["config"]["partition"]
     assert d["multi_gpu_frame_identical"] is True
     assert d["e2e"] is not None and d["e2e"]["value"] > 0
+    # ranks sharing one GPU run the flag protocol with host polls (never device waits)
+    assert d["config"]["frame_sync"].startswith("host-polled flags" if compose == "ipc" else "host synchronisation")
+    assert d["frame_sync_timed_out"] in (None, False)
+
+
+def test_bench_launches_its_own_ranks(gpu):
+    """`bench.py --gpus 2` without a launcher starts two ranks itself (torch.distributed.run
+    on 127.0.0.1) and reports n_gpus 2 and the composed frame's identity."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--same-device", "--steps", "3",
+           "--warmup", "3", "--no-cpu-baseline", "--no-extras", "--e2e-steps", "5"]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=dict(os.environ))
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["multi_gpu_frame_identical"] is True
