@@ -35,6 +35,11 @@ CONFIG_SIZES = {1: (512, 512), 2: (1920, 1080), 3: (1920, 1080), 4: (3840, 2160)
 
 # classify() codes
 MATCH, TIE, BUG, T_OUT_OF_TOL = 0, 1, 2, 3
+# classify_rules() codes: 0 match, 1..10 the tie rules (oracle/ref_harness.cpp: Rule), 100 bug, 101 t out of tolerance
+RULES = {0: "match", 1: "entry_face", 2: "sphere_graze", 3: "box_graze", 4: "zero_dir_face", 5: "oracle_voxel_grazed",
+         6: "gpu_voxel_near_miss", 7: "behind_origin", 8: "same_entry_t", 9: "instance_tie", 10: "miss_graze",
+         100: "bug", 101: "t_out_of_tolerance"}
+RULE_BUG, RULE_T_OUT = 100, 101
 
 _LIB = None
 P = C.c_void_p
@@ -79,6 +84,7 @@ def lib() -> C.CDLL:
             "vref_render_rows": (i, P, i, i, i, P, C.POINTER(d)),
             "vref_explain": (i, P, i, i, P, P, C.c_char_p, C.c_size_t),
             "vref_classify": (i, P, i, i, P, P, d, P),
+            "vref_classify_rules": (i, P, i, i, P, P, d, P),
             "vref_traverse": (i, P, P, u32, P, i),
             "vref_dda_random": (i, u64, u32, d, P, u32, P, P, P),
             "vref_primary_ray": (i, P, i, i, C.POINTER(d)),
@@ -248,6 +254,16 @@ class RefScene:
         _ok(lib().vref_classify(self._h, a, b, o.ctypes.data, g.ctypes.data, t_rel, cls.ctypes.data), "classify")
         return cls
 
+    def classify_rules(self, oracle_aov, gpu_aov, t_rel=1e-6, rows=None):
+        """Per-pixel rule code (RULES) of each FP32-vs-oracle difference."""
+        a, b = rows if rows else (0, self.height)
+        o = np.ascontiguousarray(oracle_aov, AOV_DTYPE)
+        g = np.ascontiguousarray(gpu_aov, AOV_DTYPE)
+        out = np.zeros((b - a, self.width), np.uint8)
+        _ok(lib().vref_classify_rules(self._h, a, b, o.ctypes.data, g.ctypes.data, t_rel, out.ctypes.data),
+            "classify_rules")
+        return out
+
     def explain(self, px, py, oracle_rec, gpu_rec):
         o = np.ascontiguousarray(np.array([oracle_rec], AOV_DTYPE))
         g = np.ascontiguousarray(np.array([gpu_rec], AOV_DTYPE))
@@ -263,6 +279,15 @@ class RefScene:
     def __del__(self):
         if getattr(self, "_h", None) and _LIB is not None:
             _LIB.vref_scene_free(self._h)
+
+
+def rule_histogram(rules, hit_mask=None) -> dict:
+    """{rule name: pixel count} of the non-matching pixels (+ the hit-pixel total)."""
+    vals, counts = np.unique(rules, return_counts=True)
+    h = {RULES.get(int(v), str(int(v))): int(c) for v, c in zip(vals, counts) if v != 0}
+    if hit_mask is not None:
+        h["hit_pixels"] = int(hit_mask.sum())
+    return h
 
 
 def traverse(model: RefModel, rays, with_fetches=False):

@@ -322,60 +322,148 @@ bool instance_t(const SceneObject& obj, const Ray& world, double& t) {
     return true;
 }
 
-// 0: equal; 1: documented slab-test tie; 2: unexplained (a bug); 3: same hit but t out of tolerance.
-int classify_pixel(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
+// Per-pixel classification of an FP32 result against the oracle's, by rule
+// (the tie rules are geometric: each names the FP64 near-coincidence that lets
+// an FP32 traversal legitimately pick the other answer). Every rule's share is
+// reported per frame (vref_classify_rules) so no rule can silently absorb bugs.
+enum Rule : int {
+    kMatch = 0,
+    kTieEntryFace = 1,    // same voxel, entered through another face at an edge/corner (entry planes within tau)
+    kTieSphereGraze = 2,  // a bounding sphere grazed (|d^2 - r^2| small): candidate sets may differ
+    kTieBoxGraze = 3,     // an instance's root box grazed
+    kTieZeroDirFace = 4,  // a zero-direction axis running along a voxel face (half-open convention)
+    kTieOracleGrazed = 5, // the oracle's voxel is only grazed (t_out - t_in <= tau)
+    kTieGpuNearMiss = 6,  // the GPU's voxel is a near miss / graze (|t_in - t_out| <= tau)
+    kTieBehindOrigin = 7, // the GPU's voxel ends within tau behind the origin
+    kTieSameEntry = 8,    // both voxels (different ones) entered at the same parameter (within tau)
+    kTieInstance = 9,     // two instances' FP64 hits within tau (nearest (t, id) selection)
+    kTieMissGraze = 10,   // GPU missed; the oracle's voxel is nearly grazed (within 4 tau)
+    kRuleCount = 11,
+    kBug = 100,           // unexplained difference
+    kTOutOfTol = 101,     // same hit, t outside the stated FP32 tolerance
+};
+
+// The t tolerance of a matching hit: t_rel relative, plus the FP32 resolution of
+// the entry plane's position (cell size and origin rounded to 2^-24 relative)
+// divided by the incidence |d_a| -- a grazing entry is ill-conditioned -- with
+// that term capped at 2^-12 relative (1 / 4096 of t): a t error larger than that
+// is not rounding, whatever the incidence.
+double t_tolerance(const Scene& scene, const Ray& ray, const AovRec& o, double t_rel) {
+    const SceneObject* obj = scene.find_object(o.object_id);
+    const Ray loc = transform_ray_world_to_local(ray, obj->transform);
+    const int ax = o.entry_axis;
+    const double da = std::abs(loc.direction[ax]);
+    const double ha = bounds_from_scale(obj->transform.scale).half_extent[ax];
+    const double scale = std::max(1.0, std::abs(o.t));
+    double tol = t_rel * scale;
+    if (da > 0.0) tol += std::min(std::ldexp(std::abs(loc.origin[ax]) + 2.0 * ha, -22) / da, std::ldexp(scale, -12));
+    return tol;
+}
+
+// Replays node_child (svo.cpp:27-39) along the voxel's octant path: true iff a
+// leaf sits exactly there, with its parent node and attribute index.
+bool leaf_at(const SvoModel& m, const uint32_t v[3], uint32_t level, uint32_t& parent, uint32_t& attr) {
+    if (level < 1 || level > m.depth || m.nodes.empty()) return false;
+    uint32_t node = 0;
+    for (uint32_t l = 0; l < level; ++l) {
+        const uint32_t sh = level - 1 - l;
+        const unsigned oct = (((v[0] >> sh) & 1u) << 2) | (((v[1] >> sh) & 1u) << 1) | ((v[2] >> sh) & 1u);
+        const ChildRef c = node_child(m, node, oct);
+        if (c.absent()) return false;
+        if (c.is_leaf()) {
+            if (l + 1 != level) return false;
+            parent = node;
+            attr = c.index;
+            return true;
+        }
+        node = c.index;
+    }
+    return false;
+}
+
+int classify_rule(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
     const bool ho = o.object_id >= 0, hg = g.object_id >= 0;
-    if (!ho && !hg) return 0;
-    if (ho && hg && o.object_id == g.object_id && o.voxel[0] == g.voxel[0] && o.voxel[1] == g.voxel[1] &&
-        o.voxel[2] == g.voxel[2] && o.level == g.level && o.node_index == g.node_index && o.attr_index == g.attr_index) {
-        // FP32 t tolerance: t_rel relative, plus the FP32 resolution of the entry
-        // plane's position (cell size and origin rounded to 2^-24 relative)
-        // divided by the incidence |d_a| -- a grazing entry is ill-conditioned.
+    if (!ho && !hg) return kMatch;
+    const bool same_voxel = ho && hg && o.object_id == g.object_id && o.voxel[0] == g.voxel[0] &&
+                            o.voxel[1] == g.voxel[1] && o.voxel[2] == g.voxel[2] && o.level == g.level;
+    if (same_voxel) {
+        // the leaf's parent node and attribute are functions of its path: the same
+        // voxel with another node or attribute index is a bug, never a tie
+        if (o.node_index != g.node_index || o.attr_index != g.attr_index) return kBug;
+        if (std::abs(o.t - g.t) > t_tolerance(scene, ray, o, t_rel)) return kTOutOfTol;
+        if (o.entry_axis == g.entry_axis) return kMatch;
         const SceneObject* obj = scene.find_object(o.object_id);
-        const Ray loc = transform_ray_world_to_local(ray, obj->transform);
-        const int ax = o.entry_axis;
-        const double da = std::abs(loc.direction[ax]);
-        const double ha = bounds_from_scale(obj->transform.scale).half_extent[ax];
-        double tol = t_rel * std::max(1.0, std::abs(o.t));
-        if (da > 0.0) tol += std::ldexp(std::abs(loc.origin[ax]) + 2.0 * ha, -22) / da;
-        if (std::abs(o.t - g.t) > tol) return 3;
-        if (o.entry_axis == g.entry_axis) return 0;
-        // same voxel entered through a different face: an edge/corner entry tie
         const Interval iv = voxel_interval(*obj, ray, o.voxel, o.level);
-        return std::abs(iv.axis_in[o.entry_axis] - iv.axis_in[g.entry_axis]) <= tau(o.t) ? 1 : 2;
+        return std::abs(iv.axis_in[o.entry_axis] - iv.axis_in[g.entry_axis]) <= tau(o.t) ? kTieEntryFace : kBug;
     }
     const double tref = ho ? o.t : g.t;
     const double tt = tau(tref);
     const SceneObject* oo = ho ? scene.find_object(o.object_id) : nullptr;
     const SceneObject* og = hg ? scene.find_object(g.object_id) : nullptr;
-    // sphere / box grazes of either instance
+    if (hg) {
+        // Whatever the GPU hit must be a real answer for this ray: an existing
+        // leaf of its instance's model (with that leaf's parent node and
+        // attribute), on the ray, entered at the GPU's t. The tie rules below
+        // only decide whether choosing it over the oracle's leaf is explained by
+        // an FP64 near-coincidence.
+        if (og == nullptr || !og->model) return kBug;
+        uint32_t parent = 0, attr = 0;
+        if (!leaf_at(*og->model, g.voxel, g.level, parent, attr)) return kBug;
+        if (parent != g.node_index || attr != g.attr_index) return kBug;
+        // (a ray running along a face on a zero-direction axis belongs to either
+        // side: the half-open convention's tie, checked below)
+        if (!on_zero_dir_face(*og, ray, g.voxel, g.level)) {
+            const Interval v = voxel_interval(*og, ray, g.voxel, g.level);
+            if (v.in - v.out > tt) return kBug; // the ray does not pass through it
+            if (v.out < -tt) return kBug;       // wholly behind the origin
+            const double t_in = std::max(v.in, 0.0);
+            if (std::abs(g.t - t_in) > tt + t_rel * std::max(1.0, t_in) + std::ldexp(std::max(1.0, t_in), -12))
+                return kBug;
+        }
+    }
+    if (ho && hg && o.object_id == g.object_id && o.level != g.level) {
+        // a leaf never contains another leaf: the GPU's voxel being an ancestor or a
+        // descendant of the oracle's (a traversal stopping early or late) is a bug
+        const uint32_t lo = std::min(o.level, g.level), hi = std::max(o.level, g.level);
+        const uint32_t* vlo = o.level < g.level ? o.voxel : g.voxel;
+        const uint32_t* vhi = o.level < g.level ? g.voxel : o.voxel;
+        if ((vhi[0] >> (hi - lo)) == vlo[0] && (vhi[1] >> (hi - lo)) == vlo[1] && (vhi[2] >> (hi - lo)) == vlo[2])
+            return kBug;
+    }
     for (const SceneObject* obj : {oo, og})
-        if (obj && (sphere_grazed(*obj, ray, tref) || box_grazed(*obj, ray, tref))) return 1;
+        if (obj && sphere_grazed(*obj, ray, tref)) return kTieSphereGraze;
+    for (const SceneObject* obj : {oo, og})
+        if (obj && box_grazed(*obj, ray, tref)) return kTieBoxGraze;
     if ((oo && on_zero_dir_face(*oo, ray, o.voxel, o.level)) || (og && on_zero_dir_face(*og, ray, g.voxel, g.level)))
-        return 1;
+        return kTieZeroDirFace;
     Interval vo, vg;
     if (oo) {
         vo = voxel_interval(*oo, ray, o.voxel, o.level);
-        if (vo.out - vo.in <= tt) return 1; // V_o grazed
+        if (vo.out - vo.in <= tt) return kTieOracleGrazed;
     }
     if (og) {
         vg = voxel_interval(*og, ray, g.voxel, g.level);
-        if (std::abs(vg.in - vg.out) <= tt) return 1; // V_g near-miss or graze
-        if (vg.out < 0.0 && vg.out > -tt) return 1;  // behind-origin boundary
+        if (std::abs(vg.in - vg.out) <= tt) return kTieGpuNearMiss;
+        if (vg.out < 0.0 && vg.out > -tt) return kTieBehindOrigin;
+        // a GPU voxel the ray does not pass through at all is a bug whatever else holds
+        if (vg.in > vg.out) return kBug;
     }
     if (oo && og) {
         const double ti = std::max(vo.in, 0.0), tg = std::max(vg.in, 0.0);
-        if (std::abs(ti - tg) <= tt) return 1; // both voxels entered at the same parameter
+        if (std::abs(ti - tg) <= tt) return kTieSameEntry;
         if (o.object_id != g.object_id) {
             double t64 = 0.0;
-            if (instance_t(*og, ray, t64) && std::abs(t64 - o.t) <= tt) return 1; // nearest-instance tie
+            if (instance_t(*og, ray, t64) && std::abs(t64 - o.t) <= tt) return kTieInstance;
         }
     }
-    if (!hg && oo) {
-        // GPU missed: the oracle's voxel must be (nearly) grazed or a neighbour gap
-        if (vo.out - vo.in <= 4 * tt) return 1;
-    }
-    return 2;
+    if (!hg && oo && vo.out - vo.in <= 4 * tt) return kTieMissGraze;
+    return kBug;
+}
+
+// 0: equal; 1: documented slab-test tie; 2: unexplained (a bug); 3: same hit but t out of tolerance.
+int classify_pixel(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
+    const int r = classify_rule(scene, ray, o, g, t_rel);
+    return r == kMatch ? 0 : r == kBug ? 2 : r == kTOutOfTol ? 3 : 1;
 }
 
 } // namespace
@@ -667,6 +755,24 @@ VREF_API int vref_classify(const vref_scene* s, int row_begin, int row_end, cons
 }
 
 // Human-readable breakdown of one pixel's classification (debugging aid).
+// Rule codes (classify_rule) per pixel of rows [row_begin, row_end).
+VREF_API int vref_classify_rules(const vref_scene* s, int row_begin, int row_end, const AovRec* oracle,
+                                 const AovRec* gpu, double t_rel, uint8_t* out) {
+    return guard(
+        [&] {
+            const Scene& scene = s->s;
+            const int W = scene.camera.width;
+            for (int py = row_begin; py < row_end; ++py)
+                for (int px = 0; px < W; ++px) {
+                    const size_t i = static_cast<size_t>(py - row_begin) * W + px;
+                    out[i] = static_cast<uint8_t>(
+                        classify_rule(scene, generate_primary_ray(scene.camera, px, py), oracle[i], gpu[i], t_rel));
+                }
+            return 0;
+        },
+        -1);
+}
+
 VREF_API int vref_explain(const vref_scene* s, int px, int py, const AovRec* o, const AovRec* g, char* buf, size_t n) {
     return guard(
         [&] {

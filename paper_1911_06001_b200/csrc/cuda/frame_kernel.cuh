@@ -278,12 +278,20 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
             // general copy, every other ray a loop without the zero conventions
             if (fr.zero)
                 hit = traverse_fast<kAov, true>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+            else if constexpr (VXA_POSLOOP)
+                hit = traverse_pos<kAov>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
             else
                 hit = traverse_fast<kAov, false>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
 #else
-            hit = traverse_fast<kAov>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+            if (VXA_POSLOOP && !fr.zero)
+                hit = traverse_pos<kAov>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
+            else
+                hit = traverse_fast<kAov>(nodes, static_cast<int>(in.model.depth), fr, h, stack);
 #endif
         }
+        else if (VXA_POSLOOP && !fr.zero)
+            hit = traverse_pos<kAov>(WideNodes{in.model.words, in.model.side}, static_cast<int>(in.model.depth), fr, h,
+                                     stack);
         else
             hit = traverse_fast<kAov>(WideNodes{in.model.words, in.model.side}, static_cast<int>(in.model.depth), fr, h,
                                       stack);

@@ -78,7 +78,11 @@ __global__ void __launch_bounds__(128) traverse_kernel(DevModel m, const Travers
         LocalStack lstack;
         if (fast_setup(r, d, U_lo, U_hi, Ur_lo, Ur_hi, h2, zf, zb)) {
             FastHit h;
-            hit = traverse_fast<true>(WideNodes{m.words, m.side}, static_cast<int>(m.depth), r, h, lstack);
+            // the frame kernel's dispatch: position-space loop unless a direction component is zero
+            if (VXA_POSLOOP && !r.zero)
+                hit = traverse_pos<true>(WideNodes{m.words, m.side}, static_cast<int>(m.depth), r, h, lstack);
+            else
+                hit = traverse_fast<true>(WideNodes{m.words, m.side}, static_cast<int>(m.depth), r, h, lstack);
             o.node_fetches = h.fetches;
             if (hit) {
                 t = h.t, axis = h.axis, attr = h.attr, parent = h.parent, level = h.level;

@@ -107,6 +107,11 @@ struct WideNodes {
 #ifndef VXA_SMEM_TOP
 #define VXA_SMEM_TOP 0
 #endif
+// FP32 core for rays without a zero direction component: position-space planes
+// (traverse_pos, 1) or the cell-index planes of traverse_fast (0); DESIGN.md §7.
+#ifndef VXA_POSLOOP
+#define VXA_POSLOOP 1
+#endif
 
 struct CompactNodes {
     const uint32_t* w;
@@ -497,8 +502,12 @@ struct FastRay {
     // Unit-cube form of each mirrored axis: positions are measured in root
     // cells (x' = (x + h) / 2h), so node planes sit at exact dyadic positions
     // c * 2^-L and the scale 2h only multiplies t (folded into inv).
-    float A[3];   // (-h - o_m) / 2h, rounded
-    float Ar[3];  // its FP64 rounding residual, times inv
+    // Rays with a zero direction component (traverse_fast<.., true>):
+    //   A = (-h - o_m) / 2h rounded, Ar = its FP64 rounding residual times inv.
+    // Every other ray (traverse_pos): positions P = 1 + x' in [1, 2] and
+    //   A = B = (A_64 - 1) inv rounded once from FP64, so t(P) = fma(P, inv, B); Ar unused.
+    float A[3];
+    float Ar[3];
     float inv[3]; // 2h / |d|
     // Pruning bound: subtrees entered at t >= t_lim cannot hold a hit that
     // beats the caller's best (t_lim = nextafter(best t), +inf for none).
@@ -554,8 +563,11 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         r.zbits[a] = zbits[a];
+        if (d[a] == 0.0f) r.zero |= axis_bit(a);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
         if (d[a] == 0.0f) {
-            r.zero |= axis_bit(a);
             r.A[a] = 0.0f;
             r.Ar[a] = 0.0f;
             r.inv[a] = 0.0f;
@@ -565,11 +577,22 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
         } else {
             const bool m = d[a] < 0.0f;
             if (m) r.mirror |= axis_bit(a);
-            r.A[a] = m ? -A_hi[a] : A_lo[a];
+            const float A = m ? -A_hi[a] : A_lo[a];
+            const float Ar = m ? -Ar_hi[a] : Ar_lo[a];
             r.inv[a] = __fdiv_rn(h2[a], fabsf(d[a]));
-            r.Ar[a] = __fmul_rn(m ? -Ar_hi[a] : Ar_lo[a], r.inv[a]);
-            te = fmaxf(te, plane_t(0.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
-            tx = fminf(tx, plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
+            if (VXA_POSLOOP && r.zero == 0) {
+                // position form: t(P) = fma(P, inv, B), B folded in FP64 and rounded once
+                r.A[a] = __double2float_rn(((static_cast<double>(A) - 1.0) + static_cast<double>(Ar)) *
+                                           static_cast<double>(r.inv[a]));
+                r.Ar[a] = 0.0f;
+                te = fmaxf(te, __fmaf_rn(1.0f, r.inv[a], r.A[a]));
+                tx = fminf(tx, __fmaf_rn(2.0f, r.inv[a], r.A[a]));
+            } else {
+                r.A[a] = A;
+                r.Ar[a] = __fmul_rn(Ar, r.inv[a]);
+                te = fmaxf(te, plane_t(0.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
+                tx = fminf(tx, plane_t(1.0f, 1.0f, r.A[a], r.Ar[a], r.inv[a]));
+            }
         }
     }
     // a leaf's t is never below its ancestors' entry (shared, monotone planes),
@@ -752,6 +775,159 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
                 if (r.zero & axis_bit(a)) tm[a] = zero_mid(r, a, level);
         }
         fcur = first_child(t0, tm);
+    }
+    out.fetches = fetches;
+    return false;
+}
+
+// Position-space FP32 core for rays without a zero direction component (the
+// same decisions as traverse_fast, fewer instructions and registers). Each
+// mirrored axis is measured in root cells shifted by one, P in [1, 2]: a node
+// at level L spans [1 + c 2^-L, 1 + (c + 1) 2^-L), so its low corner is any
+// interior position with the mantissa bits below 23 - L cleared and its
+// midplane sets bit 22 - L -- a pop rebuilds an ancestor's planes with two
+// bit operations per axis (no floor). A plane's parameter is
+// t = fma(P, inv, B): one rounding of an exact product plus B (FastRay), so
+// every plane still has one value at every level (watertight), and a pop
+// reproduces the descent's values bit for bit.
+// State: the node's midplane positions pm, midplane and far-plane parameters
+// tm / t1 (no near planes: the entry parameter of the child being stepped is
+// carried as `ten` -- the next sibling's entry is max(ten, t_exit) exactly,
+// because it differs from the current child only on the exit axis, whose near
+// plane is below its exit plane), the node word, the next octant, the level
+// and the `live` mask of ancestors with children left (as in traverse_fast).
+template <bool kTrackIdx, class Nodes, class Stack>
+__device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& r, FastHit& out, Stack& stack) {
+    uint32_t sidx[kTrackIdx ? kMaxDepth : 1];
+    float pm[3], tm[3], t1[3];
+    float ten; // entry parameter of the child fcur (first_node: the node's own entry)
+    {
+        float t0[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            pm[a] = 1.5f;
+            t0[a] = __fmaf_rn(1.0f, r.inv[a], r.A[a]);
+            tm[a] = __fmaf_rn(1.5f, r.inv[a], r.A[a]);
+            t1[a] = __fmaf_rn(2.0f, r.inv[a], r.A[a]);
+        }
+        ten = fmaxf(fmaxf(t0[0], t0[1]), t0[2]);
+    }
+    typename Nodes::Word fw = nodes.load(0);
+    uint32_t fidx = 0, fetches = 1;
+    // first_node: octant bit iff the midplane is crossed before the entry
+    uint32_t fcur = (tm[0] < ten ? 4u : 0u) | (tm[1] < ten ? 2u : 0u) | (tm[2] < ten ? 1u : 0u);
+    int level = 0;
+    const int depth = min(model_depth, static_cast<int>(kMaxDepth));
+    uint32_t live = 0;
+
+    while (true) {
+        if (fcur >= kExit) {
+            // pop to the deepest live ancestor, its planes rebuilt from the position bits
+            if (live == 0) break;
+            int lv;
+            asm("bfind.u32 %0, %1;" : "=r"(lv) : "r"(live));
+            live ^= 1u << lv;
+            fw = Nodes::unpack(stack.load(lv), fcur);
+            level = lv;
+            if constexpr (kTrackIdx) fidx = sidx[level];
+            const uint32_t keep = 0xffffffffu << (23 - lv); // sign, exponent and the level-lv cell bits
+            const uint32_t mid = 0x400000u >> lv;           // 2^-(lv+1)
+            const float size = __int_as_float((127 - lv) << 23);
+            const uint32_t q = fcur;
+            float c0[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float lo = __uint_as_float(__float_as_uint(pm[a]) & keep);
+                pm[a] = __uint_as_float(__float_as_uint(lo) | mid);
+                const float t0 = __fmaf_rn(lo, r.inv[a], r.A[a]);
+                tm[a] = __fmaf_rn(pm[a], r.inv[a], r.A[a]);
+                t1[a] = __fmaf_rn(lo + size, r.inv[a], r.A[a]);
+                c0[a] = (q & axis_bit(a)) ? tm[a] : t0;
+            }
+            ten = fmaxf(fmaxf(c0[0], c0[1]), c0[2]); // entry of the saved next child
+            // (falls through: the ancestor's saved next child is stepped now)
+        }
+        const uint32_t q = fcur;
+        float c1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) c1[a] = (q & axis_bit(a)) ? t1[a] : tm[a];
+        // next_node: the exit axis is the first axis attaining min c1 (x first)
+        const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
+        {
+            const uint32_t xb = c1[0] == t_exit ? 4u : (c1[1] == t_exit ? 2u : 1u);
+            fcur = (q | xb) + ((q & xb) << 3); // >= kExit iff the exit axis bit is already set
+        }
+        const float t_enter = ten;
+        ten = fmaxf(ten, t_exit);
+        const uint32_t oct = q ^ r.mirror;
+        const uint32_t bit = 1u << oct;
+        const uint32_t valid = Nodes::valid(fw);
+        if (!(valid & bit)) continue;
+        if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
+        bool is_leaf;
+        uint32_t leafm;
+        if constexpr (Nodes::kLastLevelLeaves) {
+            is_leaf = level + 1 == depth;
+            leafm = is_leaf ? valid : 0u;
+        } else {
+            leafm = Nodes::leaves(fw, level, depth);
+            is_leaf = (leafm & bit) != 0;
+        }
+        if (is_leaf) {
+            out.attr = nodes.attr_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & leafm, bit);
+            out.t = fmaxf(t_enter, 0.0f);
+            out.parent = fidx;
+            out.level = static_cast<uint32_t>(level + 1);
+            // entry axis: argmax of the child's near planes, ties to the lower axis
+            // (traversal.cpp:214-222); the node's near planes from its low corner
+            const uint32_t keep = 0xffffffffu << (23 - level);
+            float c0[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float lo = __uint_as_float(__float_as_uint(pm[a]) & keep);
+                c0[a] = (q & axis_bit(a)) ? tm[a] : __fmaf_rn(lo, r.inv[a], r.A[a]);
+            }
+            uint32_t entry = 0;
+            float te = c0[0];
+            if (c0[1] > te) entry = 1, te = c0[1];
+            if (c0[2] > te) entry = 2;
+            out.axis = entry;
+            out.fetches = fetches;
+            const uint32_t top = (2u << level) - 1u; // 2^(level+1) - 1
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const uint32_t cell = (__float_as_uint(pm[a]) & 0x7fffffu) >> (23 - level);
+                const uint32_t v = 2u * cell + ((q >> (2 - a)) & 1u);
+                out.vox[a] = (r.mirror & axis_bit(a)) ? top - v : v;
+            }
+            return true;
+        }
+        if constexpr (!Nodes::kLastLevelLeaves) {
+            if (level + 1 >= depth) continue;
+        }
+        // push: save the parent only while it has children left
+        const uint32_t child =
+            Nodes::child_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & ~leafm, bit);
+        if (fcur < kExit) {
+            live |= 1u << level;
+            stack.store(level, Nodes::pack(fw, fcur));
+        }
+        if constexpr (kTrackIdx) {
+            sidx[level] = fidx;
+            fidx = child;
+        }
+        const float quarter = __int_as_float((125 - level) << 23); // 2^-(level+2): child half-size
+        ++level;
+        fw = nodes.load(child);
+        ++fetches;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            pm[a] = __fmaf_rn((q & axis_bit(a)) ? 1.0f : -1.0f, quarter, pm[a]);
+            tm[a] = __fmaf_rn(pm[a], r.inv[a], r.A[a]);
+            t1[a] = c1[a];
+        }
+        ten = t_enter; // the child's entry = its first child's entry
+        fcur = (tm[0] < ten ? 4u : 0u) | (tm[1] < ten ? 2u : 0u) | (tm[2] < ten ? 1u : 0u);
     }
     out.fetches = fetches;
     return false;

@@ -44,6 +44,10 @@ def check_fp64(s, o, culling=True, sorting=True):
 
 def check_fp32(s, o, o_aov, o_img, culling=True, sorting=True, max_tie_frac=5e-3):
     rgb, aov, st = s.render(culling, sorting, precision=vx.VXA_FP32, aov=True)
+    # the production instantiation (no AOV stores) renders the same image as the
+    # AOV one the classifier checks
+    prod = s.render(culling, sorting, precision=vx.VXA_FP32)[0]
+    assert (prod == rgb).all(), f"{int((prod != rgb).any(axis=2).sum())} pixels differ between FP32 kernels"
     cls = o.classify(o_aov, aov, T_REL)
     n_hit = max(1, int((o_aov["object_id"] >= 0).sum()))
     bugs = int((cls == ref.BUG).sum())
