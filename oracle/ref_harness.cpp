@@ -239,9 +239,24 @@ constexpr double kInf = std::numeric_limits<double>::infinity();
 
 double tau(double t) { return 8.0 * std::ldexp(1.0, -23) * std::max(1.0, std::abs(t)); }
 
+// FP32 error of a plane parameter on local axis a of the instance: the plane's
+// position is resolved to 2^-22 of (|o_a| + 2 h_a) (origin and cell size
+// rounded to FP32), which moves t by that over the incidence |d_a| -- large on a
+// grazing axis. Capped at 2^-12 of t: more than that is not rounding.
+double plane_err(const SceneObject& obj, const Ray& world, int a, double t) {
+    if (a < 0) return 0.0;
+    const Ray loc = transform_ray_world_to_local(world, obj.transform);
+    const double da = std::abs(loc.direction[a]);
+    const double cap = std::ldexp(std::max(1.0, std::abs(t)), -12);
+    if (da == 0.0) return 0.0;
+    const double h = bounds_from_scale(obj.transform.scale).half_extent[a];
+    return std::min(std::ldexp(std::abs(loc.origin[a]) + 2.0 * h, -22) / da, cap);
+}
+
 struct Interval {
     double in = kInf, out = -kInf;
     double axis_in[3] = {-kInf, -kInf, -kInf}; // entry parameter of each axis' slab
+    int in_axis = -1, out_axis = -1;           // the axes whose planes give in / out
 };
 
 // FP64 slab test of the voxel box (level `level` of the instance's octree)
@@ -262,8 +277,8 @@ Interval voxel_interval(const SceneObject& obj, const Ray& world, const uint32_t
         double t0 = (lo - o) / d, t1 = (hi - o) / d;
         if (t0 > t1) std::swap(t0, t1);
         iv.axis_in[a] = t0;
-        iv.in = std::max(iv.in, t0);
-        iv.out = std::min(iv.out, t1);
+        if (t0 > iv.in) iv.in = t0, iv.in_axis = a;
+        if (t1 < iv.out) iv.out = t1, iv.out_axis = a;
     }
     return iv;
 }
@@ -343,21 +358,13 @@ enum Rule : int {
     kTOutOfTol = 101,     // same hit, t outside the stated FP32 tolerance
 };
 
-// The t tolerance of a matching hit: t_rel relative, plus the FP32 resolution of
-// the entry plane's position (cell size and origin rounded to 2^-24 relative)
-// divided by the incidence |d_a| -- a grazing entry is ill-conditioned -- with
-// that term capped at 2^-12 relative (1 / 4096 of t): a t error larger than that
-// is not rounding, whatever the incidence.
-double t_tolerance(const Scene& scene, const Ray& ray, const AovRec& o, double t_rel) {
+// The t tolerance of a matching hit: t_rel relative, plus the FP32 error of the
+// entry planes the two answers used (plane_err: a grazing entry is
+// ill-conditioned), each capped at 2^-12 of t.
+double t_tolerance(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
     const SceneObject* obj = scene.find_object(o.object_id);
-    const Ray loc = transform_ray_world_to_local(ray, obj->transform);
-    const int ax = o.entry_axis;
-    const double da = std::abs(loc.direction[ax]);
-    const double ha = bounds_from_scale(obj->transform.scale).half_extent[ax];
-    const double scale = std::max(1.0, std::abs(o.t));
-    double tol = t_rel * scale;
-    if (da > 0.0) tol += std::min(std::ldexp(std::abs(loc.origin[ax]) + 2.0 * ha, -22) / da, std::ldexp(scale, -12));
-    return tol;
+    return t_rel * std::max(1.0, std::abs(o.t)) +
+           std::max(plane_err(*obj, ray, o.entry_axis, o.t), plane_err(*obj, ray, g.entry_axis, o.t));
 }
 
 // Replays node_child (svo.cpp:27-39) along the voxel's octant path: true iff a
@@ -381,6 +388,9 @@ bool leaf_at(const SvoModel& m, const uint32_t v[3], uint32_t level, uint32_t& p
     return false;
 }
 
+// Every near-coincidence test below allows tau (8 FP32 ulp of t) plus the FP32
+// plane errors (plane_err) of the axes whose planes the compared parameters come
+// from -- an FP32 traversal can only disagree with FP64 by that much.
 int classify_rule(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
     const bool ho = o.object_id >= 0, hg = g.object_id >= 0;
     if (!ho && !hg) return kMatch;
@@ -390,16 +400,20 @@ int classify_rule(const Scene& scene, const Ray& ray, const AovRec& o, const Aov
         // the leaf's parent node and attribute are functions of its path: the same
         // voxel with another node or attribute index is a bug, never a tie
         if (o.node_index != g.node_index || o.attr_index != g.attr_index) return kBug;
-        if (std::abs(o.t - g.t) > t_tolerance(scene, ray, o, t_rel)) return kTOutOfTol;
+        if (std::abs(o.t - g.t) > t_tolerance(scene, ray, o, g, t_rel)) return kTOutOfTol;
         if (o.entry_axis == g.entry_axis) return kMatch;
         const SceneObject* obj = scene.find_object(o.object_id);
         const Interval iv = voxel_interval(*obj, ray, o.voxel, o.level);
-        return std::abs(iv.axis_in[o.entry_axis] - iv.axis_in[g.entry_axis]) <= tau(o.t) ? kTieEntryFace : kBug;
+        const double tol = tau(o.t) + plane_err(*obj, ray, o.entry_axis, o.t) + plane_err(*obj, ray, g.entry_axis, o.t);
+        return std::abs(iv.axis_in[o.entry_axis] - iv.axis_in[g.entry_axis]) <= tol ? kTieEntryFace : kBug;
     }
     const double tref = ho ? o.t : g.t;
     const double tt = tau(tref);
     const SceneObject* oo = ho ? scene.find_object(o.object_id) : nullptr;
     const SceneObject* og = hg ? scene.find_object(g.object_id) : nullptr;
+    const auto err2 = [&](const SceneObject* obj, const Interval& v) {
+        return plane_err(*obj, ray, v.in_axis, tref) + plane_err(*obj, ray, v.out_axis, tref);
+    };
     if (hg) {
         // Whatever the GPU hit must be a real answer for this ray: an existing
         // leaf of its instance's model (with that leaf's parent node and
@@ -414,11 +428,13 @@ int classify_rule(const Scene& scene, const Ray& ray, const AovRec& o, const Aov
         // side: the half-open convention's tie, checked below)
         if (!on_zero_dir_face(*og, ray, g.voxel, g.level)) {
             const Interval v = voxel_interval(*og, ray, g.voxel, g.level);
-            if (v.in - v.out > tt) return kBug; // the ray does not pass through it
-            if (v.out < -tt) return kBug;       // wholly behind the origin
+            const double tol = tt + err2(og, v);
+            if (v.in - v.out > tol) return kBug; // the ray does not pass through it
+            if (v.out < -tol) return kBug;       // wholly behind the origin
             const double t_in = std::max(v.in, 0.0);
-            if (std::abs(g.t - t_in) > tt + t_rel * std::max(1.0, t_in) + std::ldexp(std::max(1.0, t_in), -12))
-                return kBug;
+            if (std::abs(g.t - t_in) > tt + t_rel * std::max(1.0, t_in) + plane_err(*og, ray, v.in_axis, t_in) +
+                                           plane_err(*og, ray, g.entry_axis, t_in))
+                return kBug; // not entered at the GPU's t
         }
     }
     if (ho && hg && o.object_id == g.object_id && o.level != g.level) {
@@ -439,24 +455,26 @@ int classify_rule(const Scene& scene, const Ray& ray, const AovRec& o, const Aov
     Interval vo, vg;
     if (oo) {
         vo = voxel_interval(*oo, ray, o.voxel, o.level);
-        if (vo.out - vo.in <= tt) return kTieOracleGrazed;
+        if (vo.out - vo.in <= tt + err2(oo, vo)) return kTieOracleGrazed;
     }
     if (og) {
         vg = voxel_interval(*og, ray, g.voxel, g.level);
-        if (std::abs(vg.in - vg.out) <= tt) return kTieGpuNearMiss;
-        if (vg.out < 0.0 && vg.out > -tt) return kTieBehindOrigin;
+        const double tol = tt + err2(og, vg);
+        if (std::abs(vg.in - vg.out) <= tol) return kTieGpuNearMiss;
+        if (vg.out < 0.0 && vg.out > -tol) return kTieBehindOrigin;
         // a GPU voxel the ray does not pass through at all is a bug whatever else holds
         if (vg.in > vg.out) return kBug;
     }
     if (oo && og) {
         const double ti = std::max(vo.in, 0.0), tg = std::max(vg.in, 0.0);
-        if (std::abs(ti - tg) <= tt) return kTieSameEntry;
+        const double tol = tt + plane_err(*oo, ray, vo.in_axis, tref) + plane_err(*og, ray, vg.in_axis, tref);
+        if (std::abs(ti - tg) <= tol) return kTieSameEntry;
         if (o.object_id != g.object_id) {
             double t64 = 0.0;
-            if (instance_t(*og, ray, t64) && std::abs(t64 - o.t) <= tt) return kTieInstance;
+            if (instance_t(*og, ray, t64) && std::abs(t64 - o.t) <= tol) return kTieInstance;
         }
     }
-    if (!hg && oo && vo.out - vo.in <= 4 * tt) return kTieMissGraze;
+    if (!hg && oo && vo.out - vo.in <= 4 * tt + err2(oo, vo)) return kTieMissGraze;
     return kBug;
 }
 
@@ -798,9 +816,15 @@ VREF_API int vref_explain(const vref_scene* s, int px, int py, const AovRec* o, 
                         loc.origin.y, loc.origin.z);
                     double t64 = 0;
                     if (instance_t(*obj, ray, t64)) add("    fp64 traverse t %.17g\n", t64);
+                    uint32_t par = 0, at = 0;
+                    const bool leaf = obj->model && leaf_at(*obj->model, r->voxel, r->level, par, at);
+                    add("    leaf_at %d parent %u attr %u  t - max(in,0) = %.3g  sphere_grazed %d box_grazed %d zero_face %d\n",
+                        leaf ? 1 : 0, par, at, r->t - std::max(iv.in, 0.0), sphere_grazed(*obj, ray, r->t) ? 1 : 0,
+                        box_grazed(*obj, ray, r->t) ? 1 : 0, on_zero_dir_face(*obj, ray, r->voxel, r->level) ? 1 : 0);
                 }
             }
-            add("  tau %.3g class %d\n", tau(o->object_id >= 0 ? o->t : g->t), classify_pixel(scene, ray, *o, *g, 1e-6));
+            add("  tau %.3g class %d rule %d\n", tau(o->object_id >= 0 ? o->t : g->t),
+                classify_pixel(scene, ray, *o, *g, 1e-6), classify_rule(scene, ray, *o, *g, 1e-6));
             std::snprintf(buf, n, "%s", out.c_str());
             return 0;
         },

@@ -3,7 +3,7 @@
 * build_from_grid (ours) == build_from_grid (reference), byte for byte, on the
   reference's own random-grid generator (tests/support/oracles.hpp:265-279);
 * the sparse procedural builder == the reference's dense route
-  (gen_primitive(Sphere) -> build_from_grid) for depth <= 8, solid and shell;
+  (gen_primitive(Sphere) -> build_from_grid) for depth <= 9 solid, <= 10 shell;
 * node / leaf counts of the benchmark models (SURVEY.md §8(d));
 * the .svo stream: our serialize is accepted by the reference deserialize and
   re-serialises identically; corrupted streams are rejected with the same
@@ -25,6 +25,19 @@ def test_procedural_solid_matches_reference_dense_build(depth):
 @pytest.mark.parametrize("depth", range(1, 9))
 def test_procedural_shell_matches_reference_dense_build(depth):
     assert vx.Model.procedural(depth, shell=True).serialize() == ref.RefModel.shell_grid(depth).serialize()
+
+
+@pytest.mark.parametrize("depth,shell", [(9, True), (9, False), (10, True)])
+def test_procedural_matches_reference_dense_build_deep(depth, shell):
+    """The headline models' builder pinned beyond depth 8: at depth 9 (solid and
+    shell) and depth 10 (the C2/C3 shell, 1,333,345 nodes; the reference's
+    build_from_grid of the 1024^3 grid takes ~20 s here) the sparse procedural
+    builder is byte-identical to the reference's gen_primitive -> build_from_grid
+    (svo.cpp:80-132, ingest.cpp:195-211). The depth-11 C4 model is built by the
+    same code one level further (the reference cannot build it: 2048^3 grid)."""
+    ours = vx.Model.procedural(depth, shell=shell).serialize()
+    theirs = (ref.RefModel.shell_grid(depth) if shell else ref.RefModel.dense_sphere(depth)).serialize()
+    assert ours == theirs
 
 
 @pytest.mark.parametrize("depth", [1, 3, 6])
