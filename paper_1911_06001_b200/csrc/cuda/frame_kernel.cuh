@@ -64,9 +64,16 @@ template <typename Real> struct Best {
 // opposing the unmirrored local direction (traversal.cpp:214-222, renderer.cpp:89).
 template <typename Real> __device__ __forceinline__ void best_normal(const FrameParams<Real>& p, const Best<Real>& b, Real n[3]) {
     const DevInstance<Real>& in = p.inst[b.inst];
-    Real nl[3] = {Real(0), Real(0), Real(0)};
-    nl[b.axis] = b.pos_dir ? Real(-1) : Real(1);
-    for (int k = 0; k < 3; ++k) n[k] = in.R[3 * k] * nl[0] + in.R[3 * k + 1] * nl[1] + in.R[3 * k + 2] * nl[2];
+    if constexpr (sizeof(Real) == 8) {
+        // the reference's Mat3 * Vec3 (math.hpp:121-125), operand order kept
+        Real nl[3] = {Real(0), Real(0), Real(0)};
+        nl[b.axis] = b.pos_dir ? Real(-1) : Real(1);
+        for (int k = 0; k < 3; ++k) n[k] = in.R[3 * k] * nl[0] + in.R[3 * k + 1] * nl[1] + in.R[3 * k + 2] * nl[2];
+    } else {
+        // FP32: +-column `axis` of R, selected (the products with the one-hot local
+        // normal are exact; the compact hit buffer expands records the same way)
+        for (int k = 0; k < 3; ++k) n[k] = b.pos_dir ? -in.R[3 * k + b.axis] : in.R[3 * k + b.axis];
+    }
 }
 
 template <typename Real> struct SphereRes {
@@ -485,12 +492,23 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         bool reused = false;
         bool single_trace = false;
         HitRec prev;
+        HitRec16 prev16;
+        const bool compact_hbo = sizeof(Real) == 4 && p.hbo_compact != 0;
         if constexpr (kHbo) {
             if (!p.camera_dirty && n_hits == 1) {
                 const DevInstance<Real>& o = p.inst[only];
                 // a dirty object is never reused: its record is not even read
-                if (!o.dirty) prev = reinterpret_cast<const HitRec*>(p.hbo)[pix];
-                if (!o.dirty && prev.kind == kSingle && prev.object_id == o.id) {
+                bool same = false;
+                if (!o.dirty) {
+                    if (compact_hbo) {
+                        prev16 = reinterpret_cast<const HitRec16*>(p.hbo)[pix];
+                        same = (prev16.meta & 3u) == kSingle && prev16.object_id == o.id;
+                    } else {
+                        prev = reinterpret_cast<const HitRec*>(p.hbo)[pix];
+                        same = prev.kind == kSingle && prev.object_id == o.id;
+                    }
+                }
+                if (same) {
                     reused = true;
                 } else {
                     single_trace = true; // "trace just this SVO"
@@ -573,7 +591,29 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 
         // ---- shade + store
         uint32_t rgba;
-        if constexpr (kHbo) {
+        if (kHbo && compact_hbo) {
+            // 16-byte records: a reused record's normal is the object's current R
+            // times its stored local normal (the object is not dirty)
+            HitRec16 rec;
+            if (reused && n_hits == 1) {
+                rec = prev16;
+            } else {
+                rec.color = best.have ? __ldg(p.inst[best.inst].model.attrs + best.attr) : 0xff000000u;
+                rec.t = best.have ? static_cast<float>(best.t) : 0.0f;
+                rec.object_id = best.have ? best.id : -1;
+                rec.meta = kind | (best.axis << 2) | (best.pos_dir ? 16u : 0u);
+            }
+            if ((rec.meta & 3u) == kMiss) {
+                rgba = p.background;
+            } else {
+                Best<Real> b = best;
+                if (reused && n_hits == 1) b.inst = only, b.axis = (rec.meta >> 2) & 3u, b.pos_dir = (rec.meta & 16u) != 0;
+                Real nrm[3];
+                best_normal(p, b, nrm);
+                rgba = shade_rgba(rec.color, nrm, dw);
+            }
+            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec16*>(p.hbo)[pix] = rec; // a reused record is unchanged
+        } else if constexpr (kHbo) {
             HitRec rec;
             if (reused && n_hits == 1) {
                 rec = prev;

@@ -102,6 +102,80 @@ __global__ void pack_rgb(const uint32_t* __restrict__ fb, uint8_t* __restrict__ 
     }
 }
 
+// ---- compact device hit buffers (FP32 frames) --------------------------------
+// Local normal (axis, sign) of a world normal n of an object with rotation R:
+// n_local = R^T n, the axis of largest magnitude.
+__device__ __forceinline__ uint32_t local_normal_meta(const float* R, const double n[3]) {
+    float best = -1.0f;
+    uint32_t axis = 0, neg = 0;
+    for (uint32_t a = 0; a < 3; ++a) {
+        const float v = R[a] * static_cast<float>(n[0]) + R[3 + a] * static_cast<float>(n[1]) +
+                        R[6 + a] * static_cast<float>(n[2]);
+        if (fabsf(v) > best) best = fabsf(v), axis = a, neg = v < 0.0f ? 1u : 0u;
+    }
+    return (axis << 2) | (neg << 4);
+}
+
+// 48-byte records -> 16-byte ones against the frame's instance table (first
+// instance with the record's id, the reference's find_object rule).
+__global__ void hbo_compress(const HitRec* __restrict__ in, HitRec16* __restrict__ out, size_t n,
+                             const DevInstance<float>* __restrict__ inst, uint32_t n_inst) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const HitRec r = in[i];
+    HitRec16 c;
+    c.color = r.color;
+    c.t = static_cast<float>(r.t);
+    c.object_id = r.object_id;
+    c.meta = r.kind & 3u;
+    if (r.kind != 0) {
+        for (uint32_t k = 0; k < n_inst; ++k)
+            if (inst[k].id == r.object_id) {
+                c.meta |= local_normal_meta(inst[k].R, r.normal);
+                break;
+            }
+    }
+    out[i] = c;
+}
+
+// The rotation and id of every instance of an FP32 frame (for later expansion).
+__global__ void hbo_save_table(const DevInstance<float>* __restrict__ inst, uint32_t n_inst, float* __restrict__ tab) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_inst) return;
+    for (int j = 0; j < 9; ++j) tab[10 * k + j] = inst[k].R[j];
+    tab[10 * k + 9] = __int_as_float(inst[k].id);
+}
+
+// 16-byte records -> 48-byte host-layout ones: the normal is +-column `axis` of
+// the object's R (the FP32 kernel's best_normal), as the 48-byte path stores it.
+__global__ void hbo_expand(const HitRec16* __restrict__ in, HitRec* __restrict__ out, size_t n,
+                           const float* __restrict__ tab, uint32_t n_inst) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const HitRec16 c = in[i];
+    HitRec r;
+    r.color = c.color;
+    r.pad0 = 0;
+    r.normal[0] = r.normal[1] = r.normal[2] = 0.0;
+    r.t = static_cast<double>(c.t);
+    r.object_id = c.object_id;
+    r.kind = static_cast<uint8_t>(c.meta & 3u);
+    r.pad1[0] = r.pad1[1] = r.pad1[2] = 0;
+    if (r.kind != 0) {
+        const uint32_t axis = (c.meta >> 2) & 3u;
+        const bool neg = (c.meta & 16u) != 0;
+        for (uint32_t k = 0; k < n_inst; ++k)
+            if (__float_as_int(tab[10 * k + 9]) == c.object_id) {
+                for (int j = 0; j < 3; ++j) {
+                    const float v = tab[10 * k + 3 * j + axis];
+                    r.normal[j] = static_cast<double>(neg ? -v : v);
+                }
+                break;
+            }
+    }
+    out[i] = r;
+}
+
 struct ModelEntry {
     DevModel dev{};
     uint2* words = nullptr;
@@ -203,7 +277,11 @@ struct vxa_ctx {
     int inst_slot = 0;
 
     struct DeviceHbo {
-        HitRec* rec = nullptr;
+        HitRec* rec = nullptr;     // 48-byte host-layout records (FP64 frames, host access)
+        HitRec16* rec16 = nullptr; // 16-byte records of FP32 frames (allocated on first FP32 use)
+        bool compact = false;      // rec16 holds the current records
+        DevBuf<float> tab;         // R (9 floats) + id bits per instance of the last FP32 frame (expansion)
+        uint32_t tab_n = 0;
         int32_t w = 0, h = 0;
     };
     std::map<uint32_t, DeviceHbo> hbos;
@@ -399,7 +477,7 @@ int check_frame(const vxa_frame_desc* f) {
 // Enqueues one frame. aov/hbo are device buffers or null.
 template <typename Real>
 int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov,
-                  HitRec* hbo, bool reset_counters) {
+                  HitRec* hbo, vxa_ctx::DeviceHbo* dev_hbo, bool reset_counters) {
     // one upload: the instance records, then (FP32) the float4 cull table,
     // folded straight into the pinned staging slot
     const size_t inst_bytes = (size_t{n} * sizeof(DevInstance<Real>) + 15) & ~size_t{15};
@@ -435,7 +513,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.background = f->background[0] | (uint32_t{f->background[1]} << 8) | (uint32_t{f->background[2]} << 16) | 0xff000000u;
     p.culling = f->culling ? 1u : 0u;
     p.sorting = f->sorting ? 1u : 0u;
-    p.sphere_pass = (f->culling || f->sorting || hbo != nullptr) ? 1u : 0u;
+    p.sphere_pass = (f->culling || f->sorting || hbo != nullptr || dev_hbo != nullptr) ? 1u : 0u;
     p.camera_dirty = f->camera_dirty ? 1u : 0u;
     p.rank = f->tile_rank;
     p.world = f->tile_world;
@@ -502,6 +580,13 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.counters = ctx->counters.ptr;
     p.aov = aov;
     p.hbo = hbo;
+    p.hbo_compact = 0;
+    const size_t npix_hbo = static_cast<size_t>(W) * H;
+    // VOXANIM_HBO_COMPACT=0 keeps FP32 frames on the 48-byte records (tests)
+    const char* hbo_env = std::getenv("VOXANIM_HBO_COMPACT");
+    const bool want_compact = sizeof(Real) == 4 && !(hbo_env && std::strcmp(hbo_env, "0") == 0);
+    if (dev_hbo != nullptr && want_compact && dev_hbo->rec16 == nullptr)
+        VXA_CUDA(cudaMalloc(&dev_hbo->rec16, npix_hbo * sizeof(HitRec16)));
 
     // the upload runs beside the previous frame's kernel (its own stream and
     // table slot), off the frame-to-frame critical path
@@ -516,12 +601,35 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     if (reset_counters) VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
 
     const bool is64 = sizeof(Real) == 8;
-    const bool a = aov != nullptr, h = hbo != nullptr;
+    const bool a = aov != nullptr, h = hbo != nullptr || dev_hbo != nullptr;
 
     int& occ = ctx->occ[is64][a][h][p.compact][p.max_depth];
     if (occ == 0)
         occ = is64 ? frame_blocks_per_sm_f64(a, h, false, p.max_depth) : frame_blocks_per_sm_f32(a, h, p.compact, p.max_depth);
     FrameLaunch l{ctx->sm_count * occ, ctx->stream};
+    // device hit buffer: bring its records into the format this frame uses
+    // (once per switch; both formats describe the same HitRecords)
+    if (dev_hbo != nullptr) {
+        const unsigned blocks = static_cast<unsigned>((npix_hbo + 255) / 256);
+        if (want_compact) {
+            if (!dev_hbo->compact) {
+                hbo_compress<<<blocks, 256, 0, ctx->stream>>>(dev_hbo->rec, dev_hbo->rec16, npix_hbo,
+                                                              reinterpret_cast<const DevInstance<float>*>(p.inst), n);
+                VXA_CUDA(cudaGetLastError());
+                dev_hbo->compact = true;
+            }
+            p.hbo = dev_hbo->rec16;
+            p.hbo_compact = 1;
+        } else {
+            if (dev_hbo->compact) {
+                hbo_expand<<<blocks, 256, 0, ctx->stream>>>(dev_hbo->rec16, dev_hbo->rec, npix_hbo, dev_hbo->tab.ptr,
+                                                            dev_hbo->tab_n);
+                VXA_CUDA(cudaGetLastError());
+                dev_hbo->compact = false;
+            }
+            p.hbo = dev_hbo->rec;
+        }
+    }
     const int slot_k = ctx->k_count % vxa_ctx::kRing;
     if (ctx->k_begin[slot_k] == nullptr) {
         VXA_CUDA(cudaEventCreate(&ctx->k_begin[slot_k]));
@@ -552,15 +660,23 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     }
     if (e != cudaSuccess) return fail(VXA_ERR_CUDA, std::string("frame kernel launch: ") + cudaGetErrorString(e));
     VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
+    if (dev_hbo != nullptr && p.hbo_compact) {
+        // the instances the records refer to, for a later expansion (download, FP64 frame)
+        VXA_CUDA(dev_hbo->tab.ensure(std::max<size_t>(size_t{10} * n, 10)));
+        if (n) hbo_save_table<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
+            reinterpret_cast<const DevInstance<float>*>(p.inst), n, dev_hbo->tab.ptr);
+        VXA_CUDA(cudaGetLastError());
+        dev_hbo->tab_n = n;
+    }
     VXA_CUDA(cudaEventRecord(ctx->inst_free[slot], ctx->stream)); // this table slot may be overwritten now
     ++ctx->k_count;
     return VXA_OK;
 }
 
 int enqueue_any(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov, HitRec* hbo,
-                bool reset) {
-    if (f->precision == VXA_FP64) return enqueue_frame<double>(ctx, f, in, n, aov, hbo, reset);
-    return enqueue_frame<float>(ctx, f, in, n, aov, hbo, reset);
+                vxa_ctx::DeviceHbo* dev_hbo, bool reset) {
+    if (f->precision == VXA_FP64) return enqueue_frame<double>(ctx, f, in, n, aov, hbo, dev_hbo, reset);
+    return enqueue_frame<float>(ctx, f, in, n, aov, hbo, dev_hbo, reset);
 }
 
 // prefetched: the caller already copied the counters into ctx->counters_host
@@ -690,7 +806,11 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->sync_err.release();
     if (ctx->sync_host) cudaFreeHost(ctx->sync_host);
     if (ctx->poll_stream) cudaStreamDestroy(ctx->poll_stream);
-    for (auto& [h, b] : ctx->hbos) cudaFree(b.rec);
+    for (auto& [h, b] : ctx->hbos) {
+        cudaFree(b.rec);
+        cudaFree(b.rec16);
+        b.tab.release();
+    }
     ctx->fb.release();
     ctx->tile_counter.release();
     ctx->counters.release();
@@ -1083,12 +1203,13 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         VXA_CUDA(cudaMemsetAsync(aov, 0, npix * sizeof(PixelAov), ctx->stream));
     }
     if (f->hbo && f->hbo_device) return fail(VXA_ERR_INVALID, "host and device hit buffers are exclusive");
+    vxa_ctx::DeviceHbo* dev_hbo = nullptr;
     if (f->hbo_device) {
         const auto it = ctx->hbos.find(f->hbo_device);
         if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
         if (it->second.w != f->camera.width || it->second.h != f->camera.height)
             return fail(VXA_ERR_INVALID, "hit buffer dimensions do not match the camera");
-        hbo = it->second.rec;
+        dev_hbo = &it->second;
     }
     if (f->hbo) {
         VXA_CUDA(ctx->hbo.ensure(npix));
@@ -1109,7 +1230,7 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         ctx->next_rgb = ctx->rgb.ptr;
         ctx->next_rgb_free = nullptr;
     }
-    const int erc = enqueue_any(ctx, f, in, n, aov, hbo, true);
+    const int erc = enqueue_any(ctx, f, in, n, aov, hbo, dev_hbo, true);
     ctx->next_rgb = nullptr;
     if (erc != VXA_OK) return erc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
@@ -1179,6 +1300,8 @@ int vxa_hbo_release(vxa_ctx* ctx, uint32_t handle) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaFree(it->second.rec);
+    cudaFree(it->second.rec16);
+    it->second.tab.release();
     ctx->hbos.erase(it);
     return VXA_OK;
 }
@@ -1190,7 +1313,15 @@ int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out) {
     if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
     VXA_CUDA(cudaSetDevice(ctx->device));
     const size_t n = static_cast<size_t>(it->second.w) * it->second.h;
-    VXA_CUDA(cudaMemcpyAsync(out, it->second.rec, n * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
+    const HitRec* src = it->second.rec;
+    if (it->second.compact) { // FP32 frames left 16-byte records: expand them (the buffer stays compact)
+        VXA_CUDA(ctx->hbo.ensure(n));
+        hbo_expand<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
+            it->second.rec16, ctx->hbo.ptr, n, it->second.tab.ptr, it->second.tab_n);
+        VXA_CUDA(cudaGetLastError());
+        src = ctx->hbo.ptr;
+    }
+    VXA_CUDA(cudaMemcpyAsync(out, src, n * sizeof(HitRec), cudaMemcpyDeviceToHost, ctx->stream));
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
     return VXA_OK;
 }
@@ -1204,6 +1335,7 @@ int vxa_hbo_upload(vxa_ctx* ctx, uint32_t handle, const vxa_hit_record* in) {
     const size_t n = static_cast<size_t>(it->second.w) * it->second.h;
     VXA_CUDA(cudaMemcpyAsync(it->second.rec, in, n * sizeof(HitRec), cudaMemcpyHostToDevice, ctx->stream));
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    it->second.compact = false; // the next FP32 frame compresses the uploaded records
     ctx->h2d += n * sizeof(HitRec);
     return VXA_OK;
 }
@@ -1215,15 +1347,15 @@ int vxa_submit(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     if (f->hbo) return fail(VXA_ERR_INVALID, "vxa_submit does not take a host hit buffer");
     if (n > 0 && in == nullptr) return fail(VXA_ERR_INVALID, "null instance array");
     VXA_CUDA(cudaSetDevice(ctx->device));
-    HitRec* hbo = nullptr;
+    vxa_ctx::DeviceHbo* dev_hbo = nullptr;
     if (f->hbo_device) {
         const auto it = ctx->hbos.find(f->hbo_device);
         if (it == ctx->hbos.end()) return fail(VXA_ERR_INVALID, "unknown hit buffer handle");
         if (it->second.w != f->camera.width || it->second.h != f->camera.height)
             return fail(VXA_ERR_INVALID, "hit buffer dimensions do not match the camera");
-        hbo = it->second.rec;
+        dev_hbo = &it->second;
     }
-    return enqueue_any(ctx, f, in, n, nullptr, hbo, false);
+    return enqueue_any(ctx, f, in, n, nullptr, nullptr, dev_hbo, false);
 }
 
 namespace {

@@ -210,7 +210,8 @@ template <typename Real> struct FrameParams {
     uint32_t* tile_counter;       // persistent-thread work counter
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
     void* aov;                    // vxa_pixel_aov* or null
-    void* hbo;                    // vxa_hit_record* (device copy) or null
+    void* hbo;                    // vxa_hit_record* (device copy) or HitRec16* (hbo_compact), or null
+    uint32_t hbo_compact;         // FP32 device hit buffer in the 16-byte format
 };
 
 // Host-layout records written by the kernel (match include/vxa.h).
@@ -240,6 +241,19 @@ struct HitRec {
     uint8_t pad1[3];
 };
 static_assert(sizeof(HitRec) == 48, "voxanim::HitRecord layout");
+
+// Compact device hit-buffer record of the FP32 kernel (vxa_hbo_create buffers):
+// 16 B instead of 48. The world normal is not stored: a record is reused only
+// for the same object while it is not dirty, so its normal is the object's
+// current R times the stored local normal (entry axis, sign) -- exactly what a
+// fresh trace of the same hit computes. Expanded to HitRec on download.
+struct HitRec16 {
+    uint32_t color;
+    float t;
+    int32_t object_id;
+    uint32_t meta; // kind (bits 0-1) | entry axis << 2 | (local direction positive on it) << 4
+};
+static_assert(sizeof(HitRec16) == 16, "compact hit record");
 
 // ---------------------------------------------------------------------------
 // Node access

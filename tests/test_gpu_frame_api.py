@@ -165,6 +165,42 @@ def test_device_hit_buffer_matches_host_hit_buffer(gpu, precision):
     assert lib.vxa_hbo_release(ctx, handle.value) == 0
 
 
+def test_compact_fp32_hit_buffer_equals_full_records(gpu, monkeypatch):
+    """FP32 frames keep device hit buffers in 16-byte records (normal rebuilt from
+    the object's rotation and the stored local axis/sign). Over a mutating
+    sequence that also switches to FP64 frames and back (format conversions both
+    ways) and takes host writes, images, FrameStats and the records the host sees
+    equal those of the 48-byte path (VOXANIM_HBO_COMPACT=0) field for field."""
+    runs = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("VOXANIM_HBO_COMPACT", mode)
+        s, _ = hbo_pair(31)
+        hbo = vx.HitBuffer(96, 64)
+        rng = np.random.default_rng(3)
+        out = []
+        for frame in range(16):
+            mutate(s, frame, rng.uniform(-0.05, 0.05, 2))
+            prec = vx.VXA_FP64 if frame in (6, 7, 12) else vx.VXA_FP32
+            img, _, st = s.render(precision=prec, hbo=hbo)
+            recs = hbo.records()
+            out.append((img, st["pixels_reused"], st["svo_traversals"], recs))
+            if frame == 9:
+                rec = recs[20, 30].copy()
+                rec["kind"], rec["object_id"] = 1, 1
+                hbo.set_record(30, 20, rec)
+            s.mark_clean()
+        runs.append(out)
+    monkeypatch.delenv("VOXANIM_HBO_COMPACT")
+    reused = 0
+    for k, (a, b) in enumerate(zip(*runs)):
+        assert (a[0] == b[0]).all(), k
+        assert a[1] == b[1] and a[2] == b[2], k
+        reused += a[1]
+        for f in ("color", "normal", "t", "object_id", "kind"):
+            assert (a[3][f] == b[3][f]).all(), (k, f)
+    assert reused > 0
+
+
 def test_streaming_readback_matches_synchronous_frames(gpu):
     """vxa_submit_readback (frame k's D2H overlapping frame k+1) delivers the same
     images as synchronous render_frame calls."""

@@ -39,27 +39,47 @@ def check_fp64(s, o, culling=True, sorting=True):
     assert (aov["voxel"] == o_aov["voxel"]).all()
     for k in ("rays", "sphere_tests", "svo_traversals", "pixels_reused"):
         assert st[k] == o_st[k], k
+    o.last_stats = o_st
     return o_aov, o_img
 
 
-def check_fp32(s, o, o_aov, o_img, culling=True, sorting=True, max_tie_frac=5e-3):
+def check_fp32(s, o, o_aov, o_img, culling=True, sorting=True, max_tie_frac=5e-3, max_kind_frac=1e-3):
+    """FP32 production kernel vs the oracle. Every differing pixel must be a
+    documented tie (oracle/ref_harness.cpp classify_rule); matching hits within the
+    t tolerance and +-1 LSB. FP32 FrameStats semantics: rays and sphere_tests are
+    counted on the host (pixels x objects) and equal the reference's; the FP32
+    sphere test is conservative (a margin of 1e-5 relative), so it may admit a
+    grazed sphere the FP64 test rejects, and its t_boundary is lowered by the same
+    margin (a skip can only come later) -- svo_traversals is not below the
+    reference's (up to a tie or two) and exceeds it by at most 1e-4 relative (+8);
+    HitKind may read MultiSphere for SingleSphere on such pixels (full-size frames:
+    <= 1e-5 of the pixels)."""
     rgb, aov, st = s.render(culling, sorting, precision=vx.VXA_FP32, aov=True)
     # the production instantiation (no AOV stores) renders the same image as the
     # AOV one the classifier checks
     prod = s.render(culling, sorting, precision=vx.VXA_FP32)[0]
     assert (prod == rgb).all(), f"{int((prod != rgb).any(axis=2).sum())} pixels differ between FP32 kernels"
-    cls = o.classify(o_aov, aov, T_REL)
+    rules = o.classify_rules(o_aov, aov, T_REL)
+    hist = ref.rule_histogram(rules)
     n_hit = max(1, int((o_aov["object_id"] >= 0).sum()))
-    bugs = int((cls == ref.BUG).sum())
-    t_bad = int((cls == ref.T_OUT_OF_TOL).sum())
-    assert bugs == 0, f"{bugs} unexplained FP32 mismatches"
-    assert t_bad == 0, f"{t_bad} pixels with t outside {T_REL}"
-    ties = int((cls == ref.TIE).sum())
-    assert ties <= max_tie_frac * n_hit + 2, f"{ties} ties of {n_hit} hits"
-    same = cls == ref.MATCH
+    bugs = int((rules == ref.RULE_BUG).sum())
+    t_bad = int((rules == ref.RULE_T_OUT).sum())
+    assert bugs == 0, f"{bugs} unexplained FP32 mismatches {hist}"
+    assert t_bad == 0, f"{t_bad} pixels with t outside the tolerance {hist}"
+    ties = int(((rules > 0) & (rules < 100)).sum())
+    assert ties <= max_tie_frac * n_hit + 2, f"{ties} ties of {n_hit} hits {hist}"
+    same = rules == 0
     diff = np.abs(rgb.astype(int) - o_img.astype(int)).max(axis=2)
     assert (diff[same] <= 1).all(), "RGB outside +-1 LSB on matching pixels"
-    return ties, n_hit
+    o_st = getattr(o, "last_stats", None)
+    if o_st is not None:
+        assert st["rays"] == o_st["rays"] and st["sphere_tests"] == o_st["sphere_tests"]
+        extra = st["svo_traversals"] - o_st["svo_traversals"]
+        assert -2 - 1e-5 * o_st["svo_traversals"] <= extra <= 1e-4 * o_st["svo_traversals"] + 8, \
+            (st["svo_traversals"], o_st["svo_traversals"])
+        kind_bad = int(((aov["kind"] != o_aov["kind"]) & same).sum())
+        assert kind_bad <= max_kind_frac * rules.size + 2, kind_bad
+    return ties, n_hit, hist
 
 
 def test_sorted_tracing_scene(gpu):
@@ -153,8 +173,12 @@ def test_full_size_frame(gpu, cfg, t):
     s.evaluate(t)
     o.evaluate(t)
     o_aov, o_img = check_fp64(s, o)
-    ties, n_hit = check_fp32(s, o, o_aov, o_img)
-    print(f"config {cfg}: {n_hit} hit pixels, {ties} FP32 ties ({100.0 * ties / n_hit:.4f} %)")
+    # tie caps: 3x the largest rate measured over full-size frames (profiles/fp32_evidence_r2.json:
+    # C2 <= 0.017 %, C4 <= 0.165 % of hit pixels; the rate scales with t 2^depth / scale,
+    # the FP32 resolution of a plane position relative to the voxel size)
+    cap = 5e-4 if cfg == vx.config.C2 else 5e-3
+    ties, n_hit, hist = check_fp32(s, o, o_aov, o_img, max_tie_frac=cap, max_kind_frac=1e-5)
+    print(f"config {cfg}: {n_hit} hit pixels, {ties} FP32 ties ({100.0 * ties / n_hit:.4f} %) {hist}")
 
 
 def test_axis_aligned_camera_zero_direction_rays(gpu):
