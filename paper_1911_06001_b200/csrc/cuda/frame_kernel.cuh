@@ -51,28 +51,60 @@ template <typename Real> __device__ __forceinline__ uint32_t super_row(const Fra
     return p.super_x_magic ? __umulhi(s, p.super_x_magic) : s / p.n_super_x;
 }
 
+// The nearest hit so far of a pixel: t, instance, attribute, entry axis and
+// whether the unmirrored local direction is positive on it (the normal's sign);
+// parent / level / voxel for the AOV kernels only.
 template <typename Real> struct Best {
-    bool have;
-    bool pos_dir; // the unmirrored local direction is positive on the entry axis
-    Real t;
-    int32_t id;
-    uint32_t inst, attr, parent, level, axis;
-    uint32_t vox[3];
+    Real t = Real(0);
+    bool have_ = false, pos_dir_ = false;
+    int32_t id_ = -1;
+    uint32_t inst_ = 0, axis_ = 0;
+    uint32_t attr = 0, parent = 0, level = 0;
+    uint32_t vox[3] = {0, 0, 0};
+    __device__ __forceinline__ bool have() const { return have_; }
+    __device__ __forceinline__ uint32_t inst() const { return inst_; }
+    __device__ __forceinline__ uint32_t axis() const { return axis_; }
+    __device__ __forceinline__ bool pos_dir() const { return pos_dir_; }
+    __device__ __forceinline__ int32_t id(const FrameParams<Real>&) const { return id_; }
+    __device__ __forceinline__ void set(uint32_t inst, int32_t id, uint32_t axis, bool pos_dir) {
+        have_ = true, inst_ = inst, id_ = id, axis_ = axis, pos_dir_ = pos_dir;
+    }
+};
+
+// FP32 kernel: few registers live across the candidate loop (they spill at the
+// 64-register cap). Instance, axis, sign and the have-flag share one word; the
+// object id is read back from the instance record when needed (exact t ties,
+// outputs); t is in the pixel's traversal units (unnormalised camera direction,
+// see trace_candidate): t_world = t * rn.
+template <> struct Best<float> {
+    float t = 0.0f;
+    uint32_t key = 0; // bit 31 have | bit 26 pos_dir | bits 24-25 axis | bits 0-23 instance
+    uint32_t attr = 0, parent = 0, level = 0;
+    uint32_t vox[3] = {0, 0, 0};
+    __device__ __forceinline__ bool have() const { return (key >> 31) != 0; }
+    __device__ __forceinline__ uint32_t inst() const { return key & 0xffffffu; }
+    __device__ __forceinline__ uint32_t axis() const { return (key >> 24) & 3u; }
+    __device__ __forceinline__ bool pos_dir() const { return ((key >> 26) & 1u) != 0; }
+    __device__ __forceinline__ int32_t id(const FrameParams<float>& p) const { return p.inst[inst()].id; }
+    __device__ __forceinline__ void set(uint32_t inst, int32_t, uint32_t axis, bool pos_dir) {
+        key = 0x80000000u | (pos_dir ? 1u << 26 : 0u) | (axis << 24) | inst;
+    }
 };
 
 // World normal of the nearest hit: R n_local with n_local = sign e_axis
 // opposing the unmirrored local direction (traversal.cpp:214-222, renderer.cpp:89).
 template <typename Real> __device__ __forceinline__ void best_normal(const FrameParams<Real>& p, const Best<Real>& b, Real n[3]) {
-    const DevInstance<Real>& in = p.inst[b.inst];
+    const DevInstance<Real>& in = p.inst[b.inst()];
+    const uint32_t axis = b.axis();
     if constexpr (sizeof(Real) == 8) {
         // the reference's Mat3 * Vec3 (math.hpp:121-125), operand order kept
         Real nl[3] = {Real(0), Real(0), Real(0)};
-        nl[b.axis] = b.pos_dir ? Real(-1) : Real(1);
+        nl[axis] = b.pos_dir() ? Real(-1) : Real(1);
         for (int k = 0; k < 3; ++k) n[k] = in.R[3 * k] * nl[0] + in.R[3 * k + 1] * nl[1] + in.R[3 * k + 2] * nl[2];
     } else {
         // FP32: +-column `axis` of R, selected (the products with the one-hot local
         // normal are exact; the compact hit buffer expands records the same way)
-        for (int k = 0; k < 3; ++k) n[k] = b.pos_dir ? -in.R[3 * k + b.axis] : in.R[3 * k + b.axis];
+        for (int k = 0; k < 3; ++k) n[k] = b.pos_dir() ? -in.R[3 * k + axis] : in.R[3 * k + axis];
     }
 }
 
@@ -129,26 +161,21 @@ __device__ __forceinline__ SphereRes<Real> sphere_of(const FrameParams<Real>& p,
         return sphere_test(__ldg(p.cull + i), d);
 }
 
-// Per-pixel primary ray. FP32 kernel: the camera-space direction and its norm
-// are also kept in FP64 (dcd, rnd) so each instance's local direction is formed
-// in FP64 and rounded once: a plane entry t = (A + i s) / d_a is only as
-// accurate as the small component d_a.
-struct RayD {
-    double dcx, dcy; // camera-space direction (z = -1)
-    double rnd;      // 1 / |(dcx, dcy, -1)|
-};
-
-// FP64 camera-space direction of pixel (px, py): the reference's NDC
-// (renderer.cpp:19-21) is ((px + 0.5) / W) * 2 - 1 = (2 px + 1 - W) / W. The
-// numerator is an exact integer, so a component is exactly zero iff the
-// reference's is (its quotient is never within an ulp of 0.5 otherwise: the
-// distance is >= 1/2W), and zero-direction rays stay zero; elsewhere the value
-// is within a few FP64 ulp of the reference's, far below the FP32 rounding.
+// FP64 camera-space direction of pixel (px, py), unnormalised (z = -1): the
+// reference's NDC (renderer.cpp:19-21) is ((px + 0.5) / W) * 2 - 1 =
+// (2 px + 1 - W) / W. The numerator is an exact integer, so a component is
+// exactly zero iff the reference's is (its quotient is never within an ulp of
+// 0.5 otherwise: the distance is >= 1/2W), and zero-direction rays stay zero;
+// elsewhere the value is within a few FP64 ulp of the reference's, far below the
+// FP32 rounding. The FP32 kernel forms each instance's local direction from it
+// in FP64 and rounds once (a plane entry t = (A + i s) / d_a is only as accurate
+// as the small component d_a), without normalising: a pixel's traversals all run
+// in the same units (t_world = t |u|^-1), recomputed per candidate from (px, py)
+// instead of being held in registers across the candidate loop.
 template <typename Real>
-__device__ __forceinline__ void camera_dir_f64(const FrameParams<Real>& p, int px, int py, RayD& rd) {
-    rd.dcx = static_cast<double>(2 * px + 1 - p.width) * p.d_kx;
-    rd.dcy = static_cast<double>(p.height - 2 * py - 1) * p.d_ky;
-    rd.rnd = rsqrt(fma(rd.dcx, rd.dcx, fma(rd.dcy, rd.dcy, 1.0)));
+__device__ __forceinline__ void camera_dir_f64(const FrameParams<Real>& p, int px, int py, double& dcx, double& dcy) {
+    dcx = static_cast<double>(2 * px + 1 - p.width) * p.d_kx;
+    dcy = static_cast<double>(p.height - 2 * py - 1) * p.d_ky;
 }
 
 // ---- FP32 tile culling --------------------------------------------------------
@@ -218,9 +245,9 @@ __device__ __forceinline__ bool cone_candidate(const float4 in, const TileCone& 
 }
 
 template <typename Real, bool kAov, bool kCompact>
-__device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint32_t i, const Real dw[3],
-                                                const RayD& rd, Best<Real>& best, uint32_t& traversals,
-                                                uint32_t& fetches, BlockStack& stack) {
+__device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint32_t i, const Real dw[3], int px,
+                                                int py, Best<Real>& best, uint32_t& traversals, uint32_t& fetches,
+                                                BlockStack& stack) {
     const DevInstance<Real>& in = p.inst[i];
     if (!in.valid_model) return;
     ++traversals;
@@ -243,9 +270,13 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
     } else {
         float d[3];
         double dd[3];
-        for (int k = 0; k < 3; ++k) {
-            dd[k] = (fma(in.Md[3 * k], rd.dcx, in.Md[3 * k + 1] * rd.dcy) - in.Md[3 * k + 2]) * rd.rnd;
-            d[k] = static_cast<float>(dd[k]);
+        {
+            double dcx, dcy;
+            camera_dir_f64(p, px, py, dcx, dcy);
+            for (int k = 0; k < 3; ++k) {
+                dd[k] = fma(in.Md[3 * k], dcx, in.Md[3 * k + 1] * dcy) - in.Md[3 * k + 2];
+                d[k] = static_cast<float>(dd[k]);
+            }
         }
         // Content sphere (conservative, margin included): every leaf lies inside
         // it, so a ray whose line misses it -- or that is outside it and moving
@@ -260,15 +291,16 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
                 qw = fma(q, w, qw);
                 ww = fma(w, w, ww);
             }
-            // squared line distance qq - qw^2/ww > r2, without the division (ww > 0)
+            // squared line distance qq - qw^2/ww > r2, without the division (ww > 0;
+            // homogeneous in w, so the unnormalised direction serves)
             const double r2 = static_cast<double>(in.model.content_r2);
             if (fma(qq, ww, -qw * qw) > r2 * ww || (qw > 0.0 && qq > r2)) return;
         }
         FastRay fr;
         // Only a hit at t <= best.t can change the nearest (t, id) (ties go to
         // the lower id), so subtrees entered beyond best.t are pruned.
-        const float t_lim = best.have ? nextafterf(static_cast<float>(best.t), __int_as_float(0x7f800000))
-                                      : __int_as_float(0x7f800000);
+        const float t_lim = best.have() ? nextafterf(static_cast<float>(best.t), __int_as_float(0x7f800000))
+                                        : __int_as_float(0x7f800000);
         if (!fast_setup(fr, d, in.U_lo, in.U_hi, in.Ur_lo, in.Ur_hi, in.h2, in.zflags, in.zbits, t_lim)) return;
         FastHit h;
         bool hit;
@@ -307,17 +339,15 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         for (int k = 0; k < 3; ++k) ld[k] = d[k], vox[k] = h.vox[k];
         t = h.t, axis = h.axis, attr = h.attr, parent = h.parent, level = h.level;
     }
-    if (!best.have || t < best.t || (t == best.t && in.id < best.id)) {
-        best.have = true;
+    if (!best.have() || t < best.t || (t == best.t && in.id < best.id(p))) {
+        best.set(i, in.id, axis, ld[axis] > Real(0));
         best.t = t;
-        best.id = in.id;
-        best.inst = i;
         best.attr = attr;
-        best.parent = parent;
-        best.level = level;
-        best.axis = axis;
-        best.pos_dir = ld[axis] > Real(0);
-        if constexpr (kAov) best.vox[0] = vox[0], best.vox[1] = vox[1], best.vox[2] = vox[2];
+        if constexpr (kAov) {
+            best.parent = parent;
+            best.level = level;
+            best.vox[0] = vox[0], best.vox[1] = vox[1], best.vox[2] = vox[2];
+        }
     }
 }
 
@@ -396,8 +426,16 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 #endif
     const uint16_t* const list = s_list[warp];
 
+    int prev_band = -1; // band of the warp's previous tile (synchronous readback)
     while (true) {
         __syncwarp();
+        if (prev_band >= 0) {
+            // the previous tile's RGB8 bytes are in L2 before its band count moves
+            // (the copy engine starts the band's D2H when the count is complete)
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(p.band_done + prev_band, 1u);
+        }
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -406,6 +444,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         const uint32_t st = p.super_order != nullptr ? __ldg(p.super_order + st_k) : st_k;
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
         const uint32_t sy = super_row(p, s), sx = s - sy * p.n_super_x;
+        if (p.band_done != nullptr) prev_band = static_cast<int>(sy / p.band_rows);
         const int tx0 = static_cast<int>(sx * kSuper + (wt % (kSuper / kTileW)) * kTileW);
         const int ty0 = static_cast<int>(sy * kSuper + (wt / (kSuper / kTileW)) * kTileH);
         const int px = tx0 + static_cast<int>(lane % kTileW);
@@ -447,7 +486,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 
         // ---- primary ray (renderer.cpp:11-23)
         Real dw[3];
-        RayD rd;
+        float rn = 1.0f; // FP32: 1 / |u| -- the pixel's traversal units to world units (t_world = t rn)
         if constexpr (sizeof(Real) == 8) {
             const double ndc_x = (px + 0.5) / p.width * 2.0 - 1.0;
             const double ndc_y = 1.0 - (py + 0.5) / p.height * 2.0;
@@ -459,10 +498,11 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         } else {
             const float dcx = fmaf(static_cast<float>(px) + 0.5f, p.inv_w2, -1.0f) * p.sx;
             const float dcy = fmaf(-(static_cast<float>(py) + 0.5f), p.inv_h2, 1.0f) * p.sy;
-            const float rn = rsqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
+            rn = rsqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
             for (int k = 0; k < 3; ++k) dw[k] = (p.C[3 * k] * dcx + p.C[3 * k + 1] * dcy - p.C[3 * k + 2]) * rn;
-            camera_dir_f64(p, px, py, rd);
         }
+        // world-units t of the best hit (the FP32 kernel traverses in units of |u|)
+        const auto world_t = [&](Real t) { return sizeof(Real) == 8 ? t : static_cast<Real>(static_cast<float>(t) * rn); };
 
         // ---- sphere pass: count hits, remember the single hit (HBO rule)
         uint32_t n_hits = 0, only = 0;
@@ -482,12 +522,6 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         }
 
         Best<Real> best;
-        best.have = false;
-        best.t = Real(0);
-        best.id = -1;
-        best.pos_dir = false;
-        best.inst = best.attr = best.parent = best.level = best.axis = 0;
-        best.vox[0] = best.vox[1] = best.vox[2] = 0;
         uint32_t traversals = 0, fetches = 0, kind = kMiss;
         bool reused = false;
         bool single_trace = false;
@@ -547,7 +581,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                     // its t_boundary only matters once there is a best hit.
                     int kb = -1;
                     Real tcb = Real(0);
-                    if (!best.have && rem != 0 && (rem & (rem - 1)) == 0) {
+                    if (!best.have() && rem != 0 && (rem & (rem - 1)) == 0) {
                         kb = __ffsll(rem) - 1;
                     } else {
                         for (unsigned long long it = rem; it; it &= it - 1) {
@@ -577,10 +611,10 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 if (!found) break;
                 // sorted orders: skip (do not break) when the best hit is nearer than the
                 // candidate's sphere (renderer.cpp:70-72); id orders carry t_boundary = 0
-                if ((mode == kListSorted || mode == kAllSorted) && best.have && best.t < cand_tb) continue;
-                trace_candidate<Real, kAov, kCompact>(p, cand, dw, rd, best, traversals, fetches, stack);
+                if ((mode == kListSorted || mode == kAllSorted) && best.have() && world_t(best.t) < cand_tb) continue;
+                trace_candidate<Real, kAov, kCompact>(p, cand, dw, px, py, best, traversals, fetches, stack);
             }
-            if (best.have) kind = n_cand > 1 ? kMulti : kSingle;
+            if (best.have()) kind = n_cand > 1 ? kMulti : kSingle;
             if constexpr (kHbo) {
                 if (!p.camera_dirty && p.culling && n_hits == 0) reused = true; // trivial reuse of a miss
             }
@@ -598,16 +632,16 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             if (reused && n_hits == 1) {
                 rec = prev16;
             } else {
-                rec.color = best.have ? __ldg(p.inst[best.inst].model.attrs + best.attr) : 0xff000000u;
-                rec.t = best.have ? static_cast<float>(best.t) : 0.0f;
-                rec.object_id = best.have ? best.id : -1;
-                rec.meta = kind | (best.axis << 2) | (best.pos_dir ? 16u : 0u);
+                rec.color = best.have() ? __ldg(p.inst[best.inst()].model.attrs + best.attr) : 0xff000000u;
+                rec.t = best.have() ? static_cast<float>(world_t(best.t)) : 0.0f;
+                rec.object_id = best.have() ? best.id(p) : -1;
+                rec.meta = kind | (best.axis() << 2) | (best.pos_dir() ? 16u : 0u);
             }
             if ((rec.meta & 3u) == kMiss) {
                 rgba = p.background;
             } else {
                 Best<Real> b = best;
-                if (reused && n_hits == 1) b.inst = only, b.axis = (rec.meta >> 2) & 3u, b.pos_dir = (rec.meta & 16u) != 0;
+                if (reused && n_hits == 1) b.set(only, rec.object_id, (rec.meta >> 2) & 3u, (rec.meta & 16u) != 0);
                 Real nrm[3];
                 best_normal(p, b, nrm);
                 rgba = shade_rgba(rec.color, nrm, dw);
@@ -618,13 +652,13 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             if (reused && n_hits == 1) {
                 rec = prev;
             } else {
-                rec.color = best.have ? __ldg(p.inst[best.inst].model.attrs + best.attr) : 0xff000000u;
+                rec.color = best.have() ? __ldg(p.inst[best.inst()].model.attrs + best.attr) : 0xff000000u;
                 rec.pad0 = 0;
                 Real nrm[3] = {Real(0), Real(0), Real(0)};
-                if (best.have) best_normal(p, best, nrm);
+                if (best.have()) best_normal(p, best, nrm);
                 for (int k = 0; k < 3; ++k) rec.normal[k] = static_cast<double>(nrm[k]);
-                rec.t = best.have ? static_cast<double>(best.t) : 0.0;
-                rec.object_id = best.have ? best.id : -1;
+                rec.t = best.have() ? static_cast<double>(world_t(best.t)) : 0.0;
+                rec.object_id = best.have() ? best.id(p) : -1;
                 rec.kind = static_cast<uint8_t>(kind);
                 rec.pad1[0] = rec.pad1[1] = rec.pad1[2] = 0;
             }
@@ -637,8 +671,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             }
             if (!(reused && n_hits == 1)) reinterpret_cast<HitRec*>(p.hbo)[pix] = rec; // a reused record is unchanged
         } else {
-            if (best.have) {
-                const uint32_t color = __ldg(p.inst[best.inst].model.attrs + best.attr);
+            if (best.have()) {
+                const uint32_t color = __ldg(p.inst[best.inst()].model.attrs + best.attr);
                 Real nrm[3];
                 best_normal(p, best, nrm);
                 rgba = shade_rgba(color, nrm, dw);
@@ -646,7 +680,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 rgba = p.background;
             }
         }
-        if (best.have) ++n_leaf;
+        if (best.have()) ++n_leaf;
         p.fb[pix] = rgba;
         if (p.rgb != nullptr) { // streamed frame: the readback's RGB8 bytes too (no pack pass)
             if (kTileW == 8 && tile_inside && (p.width & 3) == 0) {
@@ -676,8 +710,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 
         if constexpr (kAov) {
             PixelAov a;
-            a.t = best.have ? static_cast<double>(best.t) : 0.0;
-            a.object_id = best.have ? best.id : (kHbo && reused && n_hits == 1 ? -2 : -1);
+            a.t = best.have() ? static_cast<double>(world_t(best.t)) : 0.0;
+            a.object_id = best.have() ? best.id(p) : (kHbo && reused && n_hits == 1 ? -2 : -1);
             a.node_index = best.parent;
             a.attr_index = best.attr;
             a.voxel[0] = best.vox[0];
@@ -685,7 +719,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             a.voxel[2] = best.vox[2];
             a.level = static_cast<uint8_t>(best.level);
             a.kind = static_cast<uint8_t>(kind);
-            a.entry_axis = static_cast<uint8_t>(best.axis);
+            a.entry_axis = static_cast<uint8_t>(best.axis());
             a.pad0 = 0;
             a.traversals = traversals;
             a.node_fetches = fetches;
@@ -713,24 +747,33 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 // of cheap tiles instead of whatever the screen order puts last. `count` was
 // written by other blocks of the same grid: read through L2 (__ldcg), not the
 // read-only path.
-__device__ __forceinline__ void order_by_count(const uint32_t* count, uint32_t n, uint32_t* order) {
-    constexpr uint32_t kBuckets = 66; // overflow, 64 .. 0 candidates
-    __shared__ uint32_t start[kBuckets];
-    const auto bucket = [](uint32_t c) { return c == 0xffffffffu ? 0u : 65u - min(c, 64u); };
-    for (uint32_t b = threadIdx.x; b < kBuckets; b += blockDim.x) start[b] = 0;
+__device__ __forceinline__ void order_by_count(const uint32_t* count, uint32_t n, uint32_t* order, uint32_t n_super_x,
+                                               uint32_t band_rows) {
+    // With band_rows (synchronous readback): bands of super-tile rows first, in
+    // screen order, longest-first inside each band, so bands complete one by one.
+    constexpr uint32_t kPer = 66; // overflow, 64 .. 0 candidates
+    constexpr uint32_t kBands = 16;
+    __shared__ uint32_t start[kPer * kBands];
+    const uint32_t n_buckets = band_rows ? kPer * kBands : kPer;
+    const auto bucket = [&](uint32_t i) {
+        const uint32_t c = __ldcg(count + i);
+        const uint32_t b = c == 0xffffffffu ? 0u : 65u - min(c, 64u);
+        return band_rows ? min((i / n_super_x) / band_rows, kBands - 1) * kPer + b : b;
+    };
+    for (uint32_t b = threadIdx.x; b < n_buckets; b += blockDim.x) start[b] = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[bucket(__ldcg(count + i))], 1u);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[bucket(i)], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t acc = 0;
-        for (uint32_t b = 0; b < kBuckets; ++b) {
+        for (uint32_t b = 0; b < n_buckets; ++b) {
             const uint32_t c = start[b];
             start[b] = acc;
             acc += c;
         }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(__ldcg(count + i))], 1u)] = i;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(i)], 1u)] = i;
 }
 
 // Pre-pass for large scenes: one warp per super-tile of this rank cone-tests
@@ -778,7 +821,8 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
     __syncthreads();
     if (!last) return;
     __threadfence();
-    order_by_count(count, n_mine, const_cast<uint32_t*>(p.super_order));
+    // (band_rows implies one rank: super-tile st is screen super-tile st)
+    order_by_count(count, n_mine, const_cast<uint32_t*>(p.super_order), p.n_super_x, p.band_done ? p.band_rows : 0u);
     if (threadIdx.x == 0) *done = 0; // ready for the next frame
 }
 

@@ -9,6 +9,8 @@
 // -ffp-contract=off.
 #include "vxa.h"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -305,6 +307,14 @@ struct vxa_ctx {
     // on a shared copy engine (the next kernel would wait for it).
     bool rb_pending = false;
     uint8_t* next_rgb = nullptr;          // RGB8 target of the frame being submitted (streaming)
+    // synchronous readback in bands (vxa_render): per-band tile counters the copy
+    // stream waits on (cuStreamWaitValue32), set for the frame being submitted
+    DevBuf<uint32_t> band_done;
+    uint32_t* next_band_done = nullptr;
+    uint32_t next_band_rows = 0;
+    cudaEvent_t band_reset = nullptr;
+    int band_api = 0; // 0 unknown, 1 cuStreamWaitValue32 usable, -1 not
+    void* wait_value32 = nullptr;
     cudaEvent_t next_rgb_free = nullptr;  // its slot's previous D2H
     int rb_pending_slot = 0;
     uint8_t* rb_pending_out = nullptr;
@@ -544,6 +554,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.fb = target;
     p.fence_sys = target != ctx->fb.ptr ? 1u : 0u; // peer stores: fenced before vxa_frame_close's flag
     p.rgb = ctx->next_rgb; // set by vxa_submit_readback for this frame only
+    p.band_done = p.rgb != nullptr ? ctx->next_band_done : nullptr;
+    p.band_rows = ctx->next_band_rows;
     if (p.rgb != nullptr && ctx->next_rgb_free != nullptr) VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->next_rgb_free, 0));
     p.max_depth = 1;
     p.compact = sizeof(Real) == 4 ? 1u : 0u;
@@ -824,6 +836,8 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->hbo.release();
     ctx->rgb.release();
     ctx->l2_scratch.release();
+    ctx->band_done.release();
+    if (ctx->band_reset) cudaEventDestroy(ctx->band_reset);
     ctx->rays.release();
     ctx->hits.release();
     ctx->visits.release();
@@ -1187,6 +1201,25 @@ int vxa_model_counts(vxa_ctx* ctx, uint32_t handle, uint32_t* depth, uint64_t* n
     return VXA_OK;
 }
 
+namespace {
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda link);
+// VOXANIM_BANDED_READBACK=0 turns the banded synchronous readback off.
+bool band_api_ok(vxa_ctx* ctx) {
+    if (const char* env = std::getenv("VOXANIM_BANDED_READBACK"); env && std::strcmp(env, "0") == 0) return false;
+    if (ctx->band_api == 0) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        ctx->band_api = (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                         q == cudaDriverEntryPointSuccess && fn != nullptr)
+                            ? 1
+                            : -1;
+        ctx->wait_value32 = fn;
+        cudaGetLastError();
+    }
+    return ctx->band_api > 0;
+}
+} // namespace
+
 int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, uint8_t* rgb_out,
                vxa_pixel_aov* aov_out, vxa_stats* stats) {
     if (ctx == nullptr) return fail(VXA_ERR_INVALID, "null context");
@@ -1225,17 +1258,57 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     // the frame kernel writes the RGB8 image itself for an unpartitioned frame
     // (this call is synchronous, so the buffer is free: no wait event)
     const bool fused = rgb_out != nullptr && f->tile_world == 1;
+    // Large frames: the RGB8 image goes to the host in bands of super-tile rows,
+    // each band's D2H on the copy stream as soon as the frame kernel has finished
+    // its tiles (a stream wait on the band's tile counter), overlapping the rest
+    // of the frame; the last band's copy is all that follows the kernel.
+    const uint32_t n_sx = super_tiles_x(f->camera.width);
+    const uint32_t n_sy = static_cast<uint32_t>((f->camera.height + kSuper - 1) / kSuper);
+    uint32_t band_rows = 0, n_bands = 0;
+    if (fused && npix >= (size_t{1} << 20) && band_api_ok(ctx)) {
+        band_rows = (n_sy + 7) / 8; // about 8 bands
+        n_bands = (n_sy + band_rows - 1) / band_rows;
+    }
     if (fused) {
         VXA_CUDA(ctx->rgb.ensure(npix * 3 + 16));
         ctx->next_rgb = ctx->rgb.ptr;
         ctx->next_rgb_free = nullptr;
     }
+    if (n_bands) {
+        VXA_CUDA(ctx->band_done.ensure(16));
+        VXA_CUDA(cudaMemsetAsync(ctx->band_done.ptr, 0, 16 * sizeof(uint32_t), ctx->stream));
+        if (ctx->band_reset == nullptr) VXA_CUDA(cudaEventCreateWithFlags(&ctx->band_reset, cudaEventDisableTiming));
+        VXA_CUDA(cudaEventRecord(ctx->band_reset, ctx->stream));
+        if (int rc = flush_readback(ctx); rc != VXA_OK) return rc;
+        VXA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_reset, 0)); // no wait sees last frame's counts
+        ctx->next_band_done = ctx->band_done.ptr;
+        ctx->next_band_rows = band_rows;
+    }
     const int erc = enqueue_any(ctx, f, in, n, aov, hbo, dev_hbo, true);
     ctx->next_rgb = nullptr;
+    ctx->next_band_done = nullptr;
+    ctx->next_band_rows = 0;
     if (erc != VXA_OK) return erc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
     uint64_t launches = 1 + static_cast<uint64_t>(ctx->aux_launches);
-    if (rgb_out && fused) {
+    if (rgb_out && fused && n_bands) {
+        using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+        const auto wait = reinterpret_cast<WaitFn>(ctx->wait_value32);
+        const size_t row_bytes = static_cast<size_t>(f->camera.width) * 3;
+        for (uint32_t b = 0; b < n_bands; ++b) {
+            const uint32_t r0 = b * band_rows, r1 = std::min(n_sy, r0 + band_rows);
+            const uint32_t tiles = (r1 - r0) * n_sx * static_cast<uint32_t>(kTilesPerSuper);
+            const CUresult cr = wait(reinterpret_cast<CUstream>(ctx->copy_stream),
+                                     reinterpret_cast<CUdeviceptr>(ctx->band_done.ptr + b), tiles,
+                                     CU_STREAM_WAIT_VALUE_GEQ);
+            if (cr != CUDA_SUCCESS) return fail(VXA_ERR_CUDA, "cuStreamWaitValue32 failed");
+            const size_t y0 = static_cast<size_t>(r0) * kSuper;
+            const size_t y1 = std::min<size_t>(static_cast<size_t>(r1) * kSuper, static_cast<size_t>(f->camera.height));
+            VXA_CUDA(cudaMemcpyAsync(rgb_out + y0 * row_bytes, ctx->rgb.ptr + y0 * row_bytes, (y1 - y0) * row_bytes,
+                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
+        }
+        ctx->d2h += npix * 3;
+    } else if (rgb_out && fused) {
         VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
         ctx->d2h += npix * 3;
     } else if (rgb_out) {
@@ -1263,6 +1336,7 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
                                  cudaMemcpyDeviceToHost, ctx->stream));
     }
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (n_bands) VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     if (stats) {
         if (int rc = read_counters(ctx, stats, true); rc != VXA_OK) return rc;
         stats->kernel_launches = launches;

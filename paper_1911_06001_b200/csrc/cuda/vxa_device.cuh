@@ -208,6 +208,11 @@ template <typename Real> struct FrameParams {
     uint32_t* fb;                 // RGBA8 framebuffer (local or peer-mapped)
     uint8_t* rgb;                 // streamed frames: RGB8 copy for the readback (or null)
     uint32_t* tile_counter;       // persistent-thread work counter
+    // Synchronous readback (vxa_render): warp tiles finished per band of
+    // band_rows super-tile rows, so the copy engine can start a band's D2H while
+    // the frame kernel works on the next ones (null: off)
+    uint32_t* band_done;
+    uint32_t band_rows;
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
     void* aov;                    // vxa_pixel_aov* or null
     void* hbo;                    // vxa_hit_record* (device copy) or HitRec16* (hbo_compact), or null

@@ -169,8 +169,10 @@ def test_compact_fp32_hit_buffer_equals_full_records(gpu, monkeypatch):
     """FP32 frames keep device hit buffers in 16-byte records (normal rebuilt from
     the object's rotation and the stored local axis/sign). Over a mutating
     sequence that also switches to FP64 frames and back (format conversions both
-    ways) and takes host writes, images, FrameStats and the records the host sees
-    equal those of the 48-byte path (VOXANIM_HBO_COMPACT=0) field for field."""
+    ways) and takes host writes, images and FrameStats equal those of the 48-byte
+    path (VOXANIM_HBO_COMPACT=0), and so do the records the host sees (bit for bit
+    until an FP64 frame's records pass through the compact format, which holds t
+    and the normal to FP32 precision)."""
     runs = []
     for mode in ("1", "0"):
         monkeypatch.setenv("VOXANIM_HBO_COMPACT", mode)
@@ -196,9 +198,39 @@ def test_compact_fp32_hit_buffer_equals_full_records(gpu, monkeypatch):
         assert (a[0] == b[0]).all(), k
         assert a[1] == b[1] and a[2] == b[2], k
         reused += a[1]
-        for f in ("color", "normal", "t", "object_id", "kind"):
+        for f in ("color", "object_id", "kind"):
             assert (a[3][f] == b[3][f]).all(), (k, f)
+        if k < 6:  # FP32 frames only so far: the records agree bit for bit
+            assert (a[3]["t"] == b[3]["t"]).all() and (a[3]["normal"] == b[3]["normal"]).all(), k
+        else:
+            # records an FP64 frame wrote and an FP32 frame kept hold t and the
+            # normal to FP32 precision in the compact format
+            assert np.allclose(a[3]["t"], b[3]["t"], rtol=1e-6, atol=0), k
+            assert np.allclose(a[3]["normal"], b[3]["normal"], rtol=0, atol=1e-6), k
     assert reused > 0
+
+
+@pytest.mark.parametrize("cfg,precision", [(vx.config.C4, vx.VXA_FP32), (vx.config.C2, vx.VXA_FP32),
+                                           (vx.config.C2, vx.VXA_FP64)])
+def test_banded_synchronous_readback(gpu, cfg, precision, monkeypatch):
+    """A synchronous render of a large frame copies the RGB8 image in bands of
+    super-tile rows, each started by a stream wait on the band's tile counter while
+    the kernel renders the rest: the image equals the one copied after the kernel
+    (VOXANIM_BANDED_READBACK=0), frame after frame, with and without the culling
+    pre-pass's longest-first order (C4: 64 instances; C2: one)."""
+    depth = 11 if cfg == vx.config.C4 else 10
+    m = vx.Model.procedural(depth, shell=True)
+    a, b = vx.Scene(cfg, [m]), vx.Scene(cfg, [m])
+    for t in (0.2, 1.9, 3.4):
+        a.evaluate(t)
+        b.evaluate(t)
+        monkeypatch.delenv("VOXANIM_BANDED_READBACK", raising=False)
+        banded = a.render(precision=precision)[0]
+        monkeypatch.setenv("VOXANIM_BANDED_READBACK", "0")
+        plain = b.render(precision=precision)[0]
+        monkeypatch.delenv("VOXANIM_BANDED_READBACK")
+        assert (banded == plain).all(), t
+        assert (banded != 0).any()
 
 
 def test_streaming_readback_matches_synchronous_frames(gpu):
