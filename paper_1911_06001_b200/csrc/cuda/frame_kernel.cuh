@@ -74,8 +74,8 @@ template <typename Real> struct Best {
 // FP32 kernel: few registers live across the candidate loop (they spill at the
 // 64-register cap). Instance, axis, sign and the have-flag share one word; the
 // object id is read back from the instance record when needed (exact t ties,
-// outputs); t is in the pixel's traversal units (unnormalised camera direction,
-// see trace_candidate): t_world = t * rn.
+// outputs); t is in the pixel's traversal units (unnormalised camera direction
+// u, see camera_dir_f64): t_world = t |u|.
 template <> struct Best<float> {
     float t = 0.0f;
     uint32_t key = 0; // bit 31 have | bit 26 pos_dir | bits 24-25 axis | bits 0-23 instance
@@ -170,7 +170,7 @@ __device__ __forceinline__ SphereRes<Real> sphere_of(const FrameParams<Real>& p,
 // FP32 rounding. The FP32 kernel forms each instance's local direction from it
 // in FP64 and rounds once (a plane entry t = (A + i s) / d_a is only as accurate
 // as the small component d_a), without normalising: a pixel's traversals all run
-// in the same units (t_world = t |u|^-1), recomputed per candidate from (px, py)
+// in the same units (t_world = t |u|), recomputed per candidate from (px, py)
 // instead of being held in registers across the candidate loop.
 template <typename Real>
 __device__ __forceinline__ void camera_dir_f64(const FrameParams<Real>& p, int px, int py, double& dcx, double& dcy) {
@@ -447,8 +447,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         if (p.band_done != nullptr) prev_band = static_cast<int>(sy / p.band_rows);
         const int tx0 = static_cast<int>(sx * kSuper + (wt % (kSuper / kTileW)) * kTileW);
         const int ty0 = static_cast<int>(sy * kSuper + (wt / (kSuper / kTileW)) * kTileH);
-        const int px = tx0 + static_cast<int>(lane % kTileW);
-        const int py = ty0 + static_cast<int>(lane / kTileW);
+        int px = tx0 + static_cast<int>(lane % kTileW);
+        int py = ty0 + static_cast<int>(lane / kTileW);
 
         // ---- tile candidate list (culling on). Conservative: a sphere missing the
         // inflated tile cone misses every ray of the tile, in either kernel; the
@@ -482,11 +482,23 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         // warp-uniform: no lane of the tile leaves the frame (the RGB8 store gathers across lanes)
         const bool tile_inside = tx0 + kTileW <= p.width && ty0 + kTileH <= p.height;
         if (px >= p.width || py >= p.height) continue;
-        const size_t pix = static_cast<size_t>(py) * static_cast<size_t>(p.width) + static_cast<size_t>(px);
+        // the tile origin packed in one register; the pixel's coordinates and
+        // index are rebuilt from it where needed instead of staying live
+        uint32_t txy = (static_cast<uint32_t>(ty0) << 16) | static_cast<uint32_t>(tx0);
+        const auto pixel_xy = [&](int& x, int& y) {
+            asm volatile("" : "+r"(txy));
+            x = static_cast<int>(txy & 0xffffu) + static_cast<int>(lane % kTileW);
+            y = static_cast<int>(txy >> 16) + static_cast<int>(lane / kTileW);
+        };
+        const auto pixel_index = [&]() {
+            int x, y;
+            pixel_xy(x, y);
+            return static_cast<size_t>(y) * static_cast<size_t>(p.width) + static_cast<size_t>(x);
+        };
 
         // ---- primary ray (renderer.cpp:11-23)
         Real dw[3];
-        float rn = 1.0f; // FP32: 1 / |u| -- the pixel's traversal units to world units (t_world = t rn)
+        float ulen = 1.0f; // FP32: |u| -- the pixel's traversal units to world units (t_world = t |u|)
         if constexpr (sizeof(Real) == 8) {
             const double ndc_x = (px + 0.5) / p.width * 2.0 - 1.0;
             const double ndc_y = 1.0 - (py + 0.5) / p.height * 2.0;
@@ -498,11 +510,14 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         } else {
             const float dcx = fmaf(static_cast<float>(px) + 0.5f, p.inv_w2, -1.0f) * p.sx;
             const float dcy = fmaf(-(static_cast<float>(py) + 0.5f), p.inv_h2, 1.0f) * p.sy;
-            rn = rsqrtf(fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f)));
+            const float uu = fmaf(dcx, dcx, fmaf(dcy, dcy, 1.0f));
+            const float rn = rsqrtf(uu);
+            ulen = uu * rn;
             for (int k = 0; k < 3; ++k) dw[k] = (p.C[3 * k] * dcx + p.C[3 * k + 1] * dcy - p.C[3 * k + 2]) * rn;
         }
-        // world-units t of the best hit (the FP32 kernel traverses in units of |u|)
-        const auto world_t = [&](Real t) { return sizeof(Real) == 8 ? t : static_cast<Real>(static_cast<float>(t) * rn); };
+        // world-units t of the best hit: the FP32 kernel traverses along the
+        // unnormalised direction u, whose parameter is t_world / |u|
+        const auto world_t = [&](Real t) { return sizeof(Real) == 8 ? t : static_cast<Real>(static_cast<float>(t) * ulen); };
 
         // ---- sphere pass: count hits, remember the single hit (HBO rule)
         uint32_t n_hits = 0, only = 0;
@@ -522,7 +537,11 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         }
 
         Best<Real> best;
-        uint32_t traversals = 0, fetches = 0, kind = kMiss;
+        // per-pixel traversal / fetch counts (AOV kernels); otherwise the traversals
+        // count straight into the warp's totals (two fewer live registers)
+        uint32_t px_trav = 0, px_fetch = 0, kind = kMiss;
+        uint32_t& traversals = kAov ? px_trav : n_trav;
+        uint32_t& fetches = kAov ? px_fetch : n_fetch;
         bool reused = false;
         bool single_trace = false;
         HitRec prev;
@@ -535,10 +554,10 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 bool same = false;
                 if (!o.dirty) {
                     if (compact_hbo) {
-                        prev16 = reinterpret_cast<const HitRec16*>(p.hbo)[pix];
+                        prev16 = reinterpret_cast<const HitRec16*>(p.hbo)[pixel_index()];
                         same = (prev16.meta & 3u) == kSingle && prev16.object_id == o.id;
                     } else {
-                        prev = reinterpret_cast<const HitRec*>(p.hbo)[pix];
+                        prev = reinterpret_cast<const HitRec*>(p.hbo)[pixel_index()];
                         same = prev.kind == kSingle && prev.object_id == o.id;
                     }
                 }
@@ -612,6 +631,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 // sorted orders: skip (do not break) when the best hit is nearer than the
                 // candidate's sphere (renderer.cpp:70-72); id orders carry t_boundary = 0
                 if ((mode == kListSorted || mode == kAllSorted) && best.have() && world_t(best.t) < cand_tb) continue;
+                pixel_xy(px, py);
                 trace_candidate<Real, kAov, kCompact>(p, cand, dw, px, py, best, traversals, fetches, stack);
             }
             if (best.have()) kind = n_cand > 1 ? kMulti : kSingle;
@@ -619,8 +639,10 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 if (!p.camera_dirty && p.culling && n_hits == 0) reused = true; // trivial reuse of a miss
             }
         }
-        n_trav += traversals;
-        n_fetch += fetches;
+        if constexpr (kAov) {
+            n_trav += px_trav;
+            n_fetch += px_fetch;
+        }
         if (reused) ++n_reuse;
 
         // ---- shade + store
@@ -646,7 +668,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 best_normal(p, b, nrm);
                 rgba = shade_rgba(rec.color, nrm, dw);
             }
-            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec16*>(p.hbo)[pix] = rec; // a reused record is unchanged
+            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec16*>(p.hbo)[pixel_index()] = rec; // a reused record is unchanged
         } else if constexpr (kHbo) {
             HitRec rec;
             if (reused && n_hits == 1) {
@@ -669,7 +691,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                                      static_cast<Real>(rec.normal[2])};
                 rgba = shade_rgba(rec.color, nrm, dw);
             }
-            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec*>(p.hbo)[pix] = rec; // a reused record is unchanged
+            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec*>(p.hbo)[pixel_index()] = rec; // a reused record is unchanged
         } else {
             if (best.have()) {
                 const uint32_t color = __ldg(p.inst[best.inst()].model.attrs + best.attr);
@@ -681,6 +703,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             }
         }
         if (best.have()) ++n_leaf;
+        const size_t pix = pixel_index();
         p.fb[pix] = rgba;
         if (p.rgb != nullptr) { // streamed frame: the readback's RGB8 bytes too (no pack pass)
             if (kTileW == 8 && tile_inside && (p.width & 3) == 0) {
@@ -696,8 +719,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 const uint32_t j3 = j - 3u * (j / 3u);
                 const uint32_t sel = j3 == 0 ? 0x4210u : (j3 == 1 ? 0x5421u : 0x6542u);
                 if (j < 6u) {
-                    const size_t row = static_cast<size_t>(ty0 + static_cast<int>(r)) * static_cast<size_t>(p.width) +
-                                       static_cast<size_t>(tx0);
+                    const size_t row = static_cast<size_t>((txy >> 16) + r) * static_cast<size_t>(p.width) +
+                                       static_cast<size_t>(txy & 0xffffu);
                     *reinterpret_cast<uint32_t*>(p.rgb + 3 * row + 4 * j) = __byte_perm(v0, v1, sel);
                 }
             } else {
