@@ -372,7 +372,8 @@ __device__ __forceinline__ uint32_t shade_rgba(uint32_t color, const Real n[3], 
     return out;
 }
 
-template <typename Real, bool kAov, bool kHbo, bool kCompact>
+// kHbo: 0 no hit buffer, 1 48-byte host-layout records, 2 16-byte records (FP32)
+template <typename Real, bool kAov, int kHbo, bool kCompact>
 __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : VXA_MIN_BLOCKS_F64) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
     extern __shared__ uint2 smem_stack[]; // FP32 traversal stack: [level][thread]
     __shared__ uint16_t s_list[kWarps][kListCap];
@@ -544,9 +545,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         uint32_t& fetches = kAov ? px_fetch : n_fetch;
         bool reused = false;
         bool single_trace = false;
-        HitRec prev;
-        HitRec16 prev16;
-        const bool compact_hbo = sizeof(Real) == 4 && p.hbo_compact != 0;
+        constexpr bool compact_hbo = sizeof(Real) == 4 && kHbo == 2;
         if constexpr (kHbo) {
             if (!p.camera_dirty && n_hits == 1) {
                 const DevInstance<Real>& o = p.inst[only];
@@ -554,11 +553,13 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 bool same = false;
                 if (!o.dirty) {
                     if (compact_hbo) {
-                        prev16 = reinterpret_cast<const HitRec16*>(p.hbo)[pixel_index()];
+                        // only kind and id decide; a reused record is read again for shading
+                        // (nothing of it stays live across the traversal)
+                        const HitRec16 prev16 = reinterpret_cast<const HitRec16*>(p.hbo)[pixel_index()];
                         same = (prev16.meta & 3u) == kSingle && prev16.object_id == o.id;
                     } else {
-                        prev = reinterpret_cast<const HitRec*>(p.hbo)[pixel_index()];
-                        same = prev.kind == kSingle && prev.object_id == o.id;
+                        const HitRec* const pr = reinterpret_cast<const HitRec*>(p.hbo) + pixel_index();
+                        same = pr->kind == kSingle && pr->object_id == o.id;
                     }
                 }
                 if (same) {
@@ -647,12 +648,12 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 
         // ---- shade + store
         uint32_t rgba;
-        if (kHbo && compact_hbo) {
+        if constexpr (compact_hbo) {
             // 16-byte records: a reused record's normal is the object's current R
             // times its stored local normal (the object is not dirty)
             HitRec16 rec;
             if (reused && n_hits == 1) {
-                rec = prev16;
+                rec = reinterpret_cast<const HitRec16*>(p.hbo)[pixel_index()];
             } else {
                 rec.color = best.have() ? __ldg(p.inst[best.inst()].model.attrs + best.attr) : 0xff000000u;
                 rec.t = best.have() ? static_cast<float>(world_t(best.t)) : 0.0f;
@@ -669,10 +670,10 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 rgba = shade_rgba(rec.color, nrm, dw);
             }
             if (!(reused && n_hits == 1)) reinterpret_cast<HitRec16*>(p.hbo)[pixel_index()] = rec; // a reused record is unchanged
-        } else if constexpr (kHbo) {
+        } else if constexpr (kHbo == 1) {
             HitRec rec;
             if (reused && n_hits == 1) {
-                rec = prev;
+                rec = reinterpret_cast<const HitRec*>(p.hbo)[pixel_index()];
             } else {
                 rec.color = best.have() ? __ldg(p.inst[best.inst()].model.attrs + best.attr) : 0xff000000u;
                 rec.pad0 = 0;
@@ -734,7 +735,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         if constexpr (kAov) {
             PixelAov a;
             a.t = best.have() ? static_cast<double>(world_t(best.t)) : 0.0;
-            a.object_id = best.have() ? best.id(p) : (kHbo && reused && n_hits == 1 ? -2 : -1);
+            a.object_id = best.have() ? best.id(p) : (kHbo != 0 && reused && n_hits == 1 ? -2 : -1);
             a.node_index = best.parent;
             a.attr_index = best.attr;
             a.voxel[0] = best.vox[0];

@@ -6,12 +6,16 @@
 namespace vxa {
 
 namespace {
-template <bool A, bool H, bool K> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<float, A, H, K>); }
-template <bool K> void* pick_k(bool aov, bool hbo) {
-    if (aov) return hbo ? frame_fn<true, true, K>() : frame_fn<true, false, K>();
-    return hbo ? frame_fn<false, true, K>() : frame_fn<false, false, K>();
+template <bool A, int H, bool K> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<float, A, H, K>); }
+template <bool A, bool K> void* pick_h(int hbo) {
+    return hbo == 2 ? frame_fn<A, 2, K>() : hbo == 1 ? frame_fn<A, 1, K>() : frame_fn<A, 0, K>();
 }
-void* pick(bool aov, bool hbo, bool compact) { return compact ? pick_k<true>(aov, hbo) : pick_k<false>(aov, hbo); }
+// hbo: 0 none, 1 48-byte records, 2 16-byte records
+void* pick(bool aov, int hbo, bool compact) {
+    if (aov) return compact ? pick_h<true, true>(hbo) : pick_h<true, false>(hbo);
+    return compact ? pick_h<false, true>(hbo) : pick_h<false, false>(hbo);
+}
+int hbo_mode(const FrameParams<float>& p, bool hbo) { return hbo ? (p.hbo_compact ? 2 : 1) : 0; }
 } // namespace
 
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l) {
@@ -28,10 +32,11 @@ cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, co
         attr.val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelExC(&cfg, pick(aov, hbo, p.compact != 0), args);
+        return cudaLaunchKernelExC(&cfg, pick(aov, hbo_mode(p, hbo), p.compact != 0), args);
     }
 #endif
-    return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f32(p.max_depth), l.stream);
+    return cudaLaunchKernel(pick(aov, hbo_mode(p, hbo), p.compact != 0), dim3(l.grid), dim3(kBlock), args,
+                            frame_smem_bytes_f32(p.max_depth), l.stream);
 }
 
 cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint32_t* count, uint32_t* done,
@@ -46,7 +51,7 @@ size_t frame_smem_bytes_f32(uint32_t max_depth) {
     return sizeof(uint2) * kBlock * (max_depth > 0 ? max_depth : 1) + 4u * VXA_SMEM_TOP;
 }
 
-int frame_blocks_per_sm_f32(bool aov, bool hbo, bool compact, uint32_t max_depth) {
+int frame_blocks_per_sm_f32(bool aov, int hbo, bool compact, uint32_t max_depth) {
     int b = 0;
     void* fn = pick(aov, hbo, compact);
     const size_t smem = frame_smem_bytes_f32(max_depth);

@@ -7,7 +7,7 @@
 namespace vxa {
 
 namespace {
-template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<double, A, H, false>); }
+template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<double, A, H ? 1 : 0, false>); }
 void* pick(bool aov, bool hbo, bool /*compact: FP64 keeps the general words*/) {
     if (aov) return hbo ? frame_fn<true, true>() : frame_fn<true, false>();
     return hbo ? frame_fn<false, true>() : frame_fn<false, false>();
@@ -31,7 +31,7 @@ size_t frame_smem_bytes_f64(uint32_t max_depth) {
     return 0;
 }
 
-int frame_blocks_per_sm_f64(bool aov, bool hbo, bool compact, uint32_t max_depth) {
+int frame_blocks_per_sm_f64(bool aov, int hbo, bool compact, uint32_t max_depth) {
     int b = 0;
     void* fn = pick(aov, hbo, compact);
     const size_t smem = frame_smem_bytes_f64(max_depth);

@@ -319,7 +319,7 @@ struct vxa_ctx {
     int rb_pending_slot = 0;
     uint8_t* rb_pending_out = nullptr;
     size_t rb_pending_bytes = 0;
-    int occ[2][2][2][2][kMaxDepth + 1] = {}; // [precision][aov][hbo][compact][stack height]
+    int occ[2][2][3][2][kMaxDepth + 1] = {}; // [precision][aov][hbo mode][compact][stack height]
 
     // Frame-kernel timing ring: events recorded tight around every frame
     // kernel launch; vxa_stats_read sums them (gpu_ms) since the last reset.
@@ -615,10 +615,6 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     const bool is64 = sizeof(Real) == 8;
     const bool a = aov != nullptr, h = hbo != nullptr || dev_hbo != nullptr;
 
-    int& occ = ctx->occ[is64][a][h][p.compact][p.max_depth];
-    if (occ == 0)
-        occ = is64 ? frame_blocks_per_sm_f64(a, h, false, p.max_depth) : frame_blocks_per_sm_f32(a, h, p.compact, p.max_depth);
-    FrameLaunch l{ctx->sm_count * occ, ctx->stream};
     // device hit buffer: bring its records into the format this frame uses
     // (once per switch; both formats describe the same HitRecords)
     if (dev_hbo != nullptr) {
@@ -642,6 +638,12 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
             p.hbo = dev_hbo->rec;
         }
     }
+    const int hmode = h ? (p.hbo_compact ? 2 : 1) : 0;
+    int& occ = ctx->occ[is64][a][hmode][p.compact][p.max_depth];
+    if (occ == 0)
+        occ = is64 ? frame_blocks_per_sm_f64(a, hmode, false, p.max_depth)
+                   : frame_blocks_per_sm_f32(a, hmode, p.compact, p.max_depth);
+    FrameLaunch l{ctx->sm_count * occ, ctx->stream};
     const int slot_k = ctx->k_count % vxa_ctx::kRing;
     if (ctx->k_begin[slot_k] == nullptr) {
         VXA_CUDA(cudaEventCreate(&ctx->k_begin[slot_k]));

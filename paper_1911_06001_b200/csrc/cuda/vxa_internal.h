@@ -42,8 +42,9 @@ cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint
                               cudaStream_t s);
 cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, const FrameLaunch& l);
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l);
-int frame_blocks_per_sm_f32(bool aov, bool hbo, bool compact, uint32_t max_depth);
-int frame_blocks_per_sm_f64(bool aov, bool hbo, bool compact, uint32_t max_depth);
+// hbo: 0 none, 1 48-byte records, 2 16-byte records (FP32 only)
+int frame_blocks_per_sm_f32(bool aov, int hbo, bool compact, uint32_t max_depth);
+int frame_blocks_per_sm_f64(bool aov, int hbo, bool compact, uint32_t max_depth);
 size_t frame_smem_bytes_f32(uint32_t max_depth);
 
 size_t frame_smem_bytes_f64(uint32_t max_depth);
