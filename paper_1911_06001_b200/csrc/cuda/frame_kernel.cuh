@@ -431,11 +431,16 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     while (true) {
         __syncwarp();
         if (prev_band >= 0) {
-            // the previous tile's RGB8 bytes are in L2 before its band count moves
-            // (the copy engine starts the band's D2H when the count is complete)
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) atomicAdd(p.band_done + prev_band, 1u);
+            // the previous tile's RGB8 bytes are visible before its band count moves
+            // (the copy engine starts the band's D2H when the count is complete): the
+            // warp barrier orders the lanes' stores before lane 0's gpu-scope release
+            // increment (cumulative) -- one release per tile, not 32 fences. (Adding a
+            // warp's tiles per band once it leaves the band costs fewer releases but
+            // signals the bands late: the D2H overlapped less.)
+            if (lane == 0) {
+                unsigned int* const cnt = p.band_done + prev_band;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+            }
         }
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
@@ -771,14 +776,18 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 // of cheap tiles instead of whatever the screen order puts last. `count` was
 // written by other blocks of the same grid: read through L2 (__ldcg), not the
 // read-only path.
+// With band_rows (a banded synchronous readback): super-tile rows in bands of
+// band_rows, bands in screen order so they complete one after another, and
+// longest-first inside each band so a band's slowest tiles start first. The
+// bucket offsets come from a block-wide scan (up to 16 x 66 buckets).
 __device__ __forceinline__ void order_by_count(const uint32_t* count, uint32_t n, uint32_t* order, uint32_t n_super_x,
                                                uint32_t band_rows) {
-    // With band_rows (synchronous readback): bands of super-tile rows first, in
-    // screen order, longest-first inside each band, so bands complete one by one.
     constexpr uint32_t kPer = 66; // overflow, 64 .. 0 candidates
     constexpr uint32_t kBands = 16;
-    __shared__ uint32_t start[kPer * kBands];
-    const uint32_t n_buckets = band_rows ? kPer * kBands : kPer;
+    constexpr uint32_t kMax = kPer * kBands;
+    __shared__ uint32_t start[kMax];
+    __shared__ uint32_t warp_sum[32];
+    const uint32_t n_buckets = band_rows ? kMax : kPer;
     const auto bucket = [&](uint32_t i) {
         const uint32_t c = __ldcg(count + i);
         const uint32_t b = c == 0xffffffffu ? 0u : 65u - min(c, 64u);
@@ -788,13 +797,26 @@ __device__ __forceinline__ void order_by_count(const uint32_t* count, uint32_t n
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[bucket(i)], 1u);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t acc = 0;
-        for (uint32_t b = 0; b < n_buckets; ++b) {
-            const uint32_t c = start[b];
-            start[b] = acc;
-            acc += c;
-        }
+    // exclusive scan: each thread a contiguous chunk, then the chunk totals across the block
+    const uint32_t per = (n_buckets + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = min(threadIdx.x * per, n_buckets), b1 = min(b0 + per, n_buckets);
+    uint32_t local = 0;
+    for (uint32_t b = b0; b < b1; ++b) local += start[b];
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    uint32_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += v;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    uint32_t base = 0;
+    for (uint32_t w = 0; w < wid; ++w) base += warp_sum[w];
+    uint32_t acc = base + incl - local;
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t c = start[b];
+        start[b] = acc;
+        acc += c;
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(i)], 1u)] = i;

@@ -313,6 +313,7 @@ struct vxa_ctx {
     uint32_t* next_band_done = nullptr;
     uint32_t next_band_rows = 0;
     cudaEvent_t band_reset = nullptr;
+    cudaStream_t copy_stream2 = nullptr; // second D2H stream of the banded readback (bands alternate)
     int band_api = 0; // 0 unknown, 1 cuStreamWaitValue32 usable, -1 not
     void* wait_value32 = nullptr;
     cudaEvent_t next_rgb_free = nullptr;  // its slot's previous D2H
@@ -659,7 +660,11 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
         p.super_list = ctx->super_list.ptr;
         p.super_count = ctx->super_count.ptr;
         p.super_cap = kSuperCap;
-        if (VXA_LPT) {
+        // Longest-first super-tile order (for a banded synchronous readback: bands in
+        // screen order, longest-first inside each); VOXANIM_LPT=0 forces screen order
+        // (experiments)
+        const char* lpt_env = std::getenv("VOXANIM_LPT");
+        if (VXA_LPT && !(lpt_env && std::strcmp(lpt_env, "0") == 0)) {
             VXA_CUDA(ctx->super_order.ensure(std::max<size_t>(mine_super, 1)));
             p.super_order = ctx->super_order.ptr;
         }
@@ -862,6 +867,10 @@ int vxa_destroy(vxa_ctx* ctx) {
         if (ctx->rb_done[k]) cudaEventDestroy(ctx->rb_done[k]);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->copy_stream2) {
+        cudaStreamSynchronize(ctx->copy_stream2);
+        cudaStreamDestroy(ctx->copy_stream2);
+    }
     if (ctx->upload_stream) cudaStreamDestroy(ctx->upload_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->counters_host) cudaFreeHost(ctx->counters_host);
@@ -1268,7 +1277,11 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     const uint32_t n_sy = static_cast<uint32_t>((f->camera.height + kSuper - 1) / kSuper);
     uint32_t band_rows = 0, n_bands = 0;
     if (fused && npix >= (size_t{1} << 20) && band_api_ok(ctx)) {
-        band_rows = (n_sy + 7) / 8; // about 8 bands
+        // about VOXANIM_READBACK_BANDS bands (default 16, at most 16: the frame kernel's band counters)
+        uint32_t want = 16;
+        if (const char* env = std::getenv("VOXANIM_READBACK_BANDS"); env && std::atoi(env) > 0)
+            want = std::min<uint32_t>(16, static_cast<uint32_t>(std::atoi(env)));
+        band_rows = (n_sy + want - 1) / want;
         n_bands = (n_sy + band_rows - 1) / band_rows;
     }
     if (fused) {
@@ -1283,6 +1296,8 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         VXA_CUDA(cudaEventRecord(ctx->band_reset, ctx->stream));
         if (int rc = flush_readback(ctx); rc != VXA_OK) return rc;
         VXA_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_reset, 0)); // no wait sees last frame's counts
+        if (ctx->copy_stream2 == nullptr) VXA_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream2, cudaStreamNonBlocking));
+        VXA_CUDA(cudaStreamWaitEvent(ctx->copy_stream2, ctx->band_reset, 0));
         ctx->next_band_done = ctx->band_done.ptr;
         ctx->next_band_rows = band_rows;
     }
@@ -1294,22 +1309,50 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
     uint64_t launches = 1 + static_cast<uint64_t>(ctx->aux_launches);
     if (rgb_out && fused && n_bands) {
+        // VOXANIM_BAND_TRACE=1: per-band copy completion times relative to the frame (stderr)
+        static const bool trace = [] {
+            const char* e = std::getenv("VOXANIM_BAND_TRACE");
+            return e && std::strcmp(e, "1") == 0;
+        }();
+        static cudaEvent_t trace_ev[16] = {};
+        if (trace && trace_ev[0] == nullptr)
+            for (auto& e : trace_ev) VXA_CUDA(cudaEventCreate(&e));
         using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
         const auto wait = reinterpret_cast<WaitFn>(ctx->wait_value32);
         const size_t row_bytes = static_cast<size_t>(f->camera.width) * 3;
+        // bands alternate between two copy streams (two DMA engines: one D2H stream
+        // alone reaches ~45 GB/s on these band sizes); VOXANIM_READBACK_STREAMS=1: one
+        const char* ns_env = std::getenv("VOXANIM_READBACK_STREAMS");
+        const bool two = !(ns_env && std::strcmp(ns_env, "1") == 0);
         for (uint32_t b = 0; b < n_bands; ++b) {
             const uint32_t r0 = b * band_rows, r1 = std::min(n_sy, r0 + band_rows);
             const uint32_t tiles = (r1 - r0) * n_sx * static_cast<uint32_t>(kTilesPerSuper);
-            const CUresult cr = wait(reinterpret_cast<CUstream>(ctx->copy_stream),
+            cudaStream_t cs = (two && (b & 1u)) ? ctx->copy_stream2 : ctx->copy_stream;
+            const CUresult cr = wait(reinterpret_cast<CUstream>(cs),
                                      reinterpret_cast<CUdeviceptr>(ctx->band_done.ptr + b), tiles,
                                      CU_STREAM_WAIT_VALUE_GEQ);
             if (cr != CUDA_SUCCESS) return fail(VXA_ERR_CUDA, "cuStreamWaitValue32 failed");
             const size_t y0 = static_cast<size_t>(r0) * kSuper;
             const size_t y1 = std::min<size_t>(static_cast<size_t>(r1) * kSuper, static_cast<size_t>(f->camera.height));
             VXA_CUDA(cudaMemcpyAsync(rgb_out + y0 * row_bytes, ctx->rgb.ptr + y0 * row_bytes, (y1 - y0) * row_bytes,
-                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
+                                     cudaMemcpyDeviceToHost, cs));
+            if (trace) VXA_CUDA(cudaEventRecord(trace_ev[b], cs));
         }
         ctx->d2h += npix * 3;
+        if (trace) {
+            VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+            VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream2));
+            VXA_CUDA(cudaStreamSynchronize(ctx->stream));
+            float k = 0.f;
+            cudaEventElapsedTime(&k, ctx->ev_a, ctx->ev_b);
+            std::fprintf(stderr, "band trace: frame end %.3f ms; band copies done at", k);
+            for (uint32_t b = 0; b < n_bands; ++b) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ctx->ev_a, trace_ev[b]);
+                std::fprintf(stderr, " %.3f", ms);
+            }
+            std::fprintf(stderr, "\n");
+        }
     } else if (rgb_out && fused) {
         VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
         ctx->d2h += npix * 3;
@@ -1338,7 +1381,10 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
                                  cudaMemcpyDeviceToHost, ctx->stream));
     }
     VXA_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (n_bands) VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    if (n_bands) {
+        VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+        VXA_CUDA(cudaStreamSynchronize(ctx->copy_stream2));
+    }
     if (stats) {
         if (int rc = read_counters(ctx, stats, true); rc != VXA_OK) return rc;
         stats->kernel_launches = launches;
