@@ -424,7 +424,8 @@ def run_reference(args):
         "fps": round(1000.0 / frame_ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
-                   "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False},
+                   "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False,
+                   "l2": "n/a: CPU reference (the 108 MB model and 33 MB frame exceed the host caches)"},
         "cpu_baseline": {"value": round(value, 4), "unit": "Mrays/s", "cores": threads, "kind": "reference",
                          "sample": sample + f", reference render_frame/trace_ray on {threads} host threads"},
         "e2e": {"value": round(value, 4), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -876,21 +877,22 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.workload], "width": W, "height": H, "svo_depth": depth,
                        "instances": 64 if cfg == 4 else 1, "culling": True, "sorting": True, "hbo": False,
-                       "partition": (f"64x64 super-tiles round-robin over {world} ranks sharing one GPU "
-                                     f"(multi-rank correctness run, not a scaling measurement)"
-                                     if world > 1 and args.same_device else
-                                     f"64x64 super-tiles round-robin over {world} GPU(s)"),
-                       "composition": composition,
-                       "l2": "flushed between timed steps (256 MB write)" if not args.no_flush else "warm",
-                       "timed_region": timed_region,
-                       "frame_sync": (None if world == 1 else
-                                      "device flags (vxa_frame_open/close: go/done flags in rank 0's HBM, 1-thread "
-                                      "release/acquire kernels over NVLink, no host barrier)"
-                                      if sync == _abi.VXA_SYNC_DEVICE else
-                                      "host-polled flags (vxa_frame_open/close; ranks share one GPU)"
-                                      if sync == _abi.VXA_SYNC_HOST else
-                                      "host synchronisation + collective gather + barrier per frame"),
-                       "model_bytes_device": None},
+                       "l2": "flushed between timed steps (256 MB write)" if not args.no_flush else "warm"},
+            # how this arm ran the workload (kept out of `config`, which names the workload itself and
+            # matches the reference arm's)
+            "run": {"partition": (f"64x64 super-tiles round-robin over {world} ranks sharing one GPU "
+                                  f"(multi-rank correctness run, not a scaling measurement)"
+                                  if world > 1 and args.same_device else
+                                  f"64x64 super-tiles round-robin over {world} GPU(s)"),
+                    "composition": composition,
+                    "timed_region": timed_region,
+                    "frame_sync": (None if world == 1 else
+                                   "device flags (vxa_frame_open/close: go/done flags in rank 0's HBM, 1-thread "
+                                   "release/acquire kernels over NVLink, no host barrier)"
+                                   if sync == _abi.VXA_SYNC_DEVICE else
+                                   "host-polled flags (vxa_frame_open/close; ranks share one GPU)"
+                                   if sync == _abi.VXA_SYNC_HOST else
+                                   "host synchronisation + collective gather + barrier per frame")},
             "roofline": {"bound": "hbm", "achieved": round(achieved_o, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved_o / peak, 5), "traffic": traffic,
                          "peak_source": peak_src,

@@ -41,7 +41,8 @@ constexpr int kBlock = 128;
 #endif
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
-struct BlockStack : SmemStack<kBlock * sizeof(uint2)> {
+constexpr uint32_t kStackEntry = VXA_STACK_TEN ? 16u : 8u; // bytes per thread per level
+struct BlockStack : SmemStack<kBlock * kStackEntry> {
     uint32_t base_top; // shared address of the staged top node words (VXA_SMEM_TOP)
 };
 
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     uint32_t n_trav = 0, n_reuse = 0, n_fetch = 0, n_leaf = 0;
     const uint32_t n = p.n_inst;
     BlockStack stack;
-    stack.base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack + threadIdx.x));
+    stack.base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack)) + kStackEntry * threadIdx.x;
     stack.base_top = 0;
     if constexpr (sizeof(Real) == 4 && VXA_SMEM_TOP > 0) {
         // Stage the scene model's first VXA_SMEM_TOP node words (its top levels, BFS
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         // completing on an mbarrier, issued by one thread.
         __shared__ __align__(8) unsigned long long top_bar;
         const uint32_t top = static_cast<uint32_t>(__cvta_generic_to_shared(
-            reinterpret_cast<unsigned char*>(smem_stack) + sizeof(uint2) * kBlock * p.max_depth));
+            reinterpret_cast<unsigned char*>(smem_stack) + kStackEntry * kBlock * p.max_depth));
         stack.base_top = top;
         if (p.top_words != nullptr && p.top_n > 0) {
             const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&top_bar));

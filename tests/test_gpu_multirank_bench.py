@@ -34,12 +34,12 @@ def test_two_ranks_compose_the_single_device_frame(gpu, compose, port, flag):
     assert len(lines) == 1, res.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2
-    assert d["config"]["composition"].startswith("CUDA IPC stores" if compose == "ipc" else "collective gather")
-    assert "sharing one GPU" in d["config"]["partition"]
+    assert d["run"]["composition"].startswith("CUDA IPC stores" if compose == "ipc" else "collective gather")
+    assert "sharing one GPU" in d["run"]["partition"]
     assert d["multi_gpu_frame_identical"] is True
     assert d["e2e"] is not None and d["e2e"]["value"] > 0
     # ranks sharing one GPU run the flag protocol with host polls (never device waits)
-    assert d["config"]["frame_sync"].startswith("host-polled flags" if compose == "ipc" else "host synchronisation")
+    assert d["run"]["frame_sync"].startswith("host-polled flags" if compose == "ipc" else "host synchronisation")
     assert d["frame_sync_timed_out"] in (None, False)
 
 
