@@ -39,9 +39,16 @@ constexpr int kBlock = 128;
 #ifndef VXA_ZERO_SPLIT
 #define VXA_ZERO_SPLIT 1
 #endif
+// VXA_TILE_PREFETCH: claim the next warp tile while the current one renders.
+#ifndef VXA_TILE_PREFETCH
+#define VXA_TILE_PREFETCH 0
+#endif
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
-constexpr uint32_t kStackEntry = VXA_STACK_TEN ? 16u : 8u; // bytes per thread per level
+// bytes per thread per level (the node-word part's stride; layout 2 keeps the
+// entry parameters in a second array of half that stride)
+constexpr uint32_t kStackEntry = (VXA_STACK_TEN && VXA_STACK_LAYOUT != 2) ? 16u : 8u;
+constexpr uint32_t kStackBytes = VXA_STACK_TEN ? (VXA_STACK_LAYOUT == 2 ? 12u : 16u) : 8u; // per thread per level
 struct BlockStack : SmemStack<kBlock * kStackEntry> {
     uint32_t base_top; // shared address of the staged top node words (VXA_SMEM_TOP)
 };
@@ -223,6 +230,35 @@ __device__ __forceinline__ TileCone region_cone(const FrameParams<Real>& p, int 
     return c;
 }
 
+// The same cone computed by one thread (the culling pre-pass's per-tile masks):
+// the four corner rays in a loop instead of across lanes, the same arithmetic.
+template <typename Real>
+__device__ __forceinline__ TileCone region_cone_serial(const FrameParams<Real>& p, int x0, int y0, float w, float h) {
+    const float inv_w2 = static_cast<float>(p.inv_w2), inv_h2 = static_cast<float>(p.inv_h2);
+    const float sx = static_cast<float>(p.sx), sy = static_cast<float>(p.sy);
+    const float cxs = fmaf(static_cast<float>(x0) + 0.5f * w, inv_w2, -1.0f) * sx;
+    const float cys = fmaf(-(static_cast<float>(y0) + 0.5f * h), inv_h2, 1.0f) * sy;
+    const float cn = rsqrtf(cxs * cxs + cys * cys + 1.0f);
+    const float ax = cxs * cn, ay = cys * cn, az = -cn;
+    float smax = 0.0f;
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k) {
+        const float xs = fmaf(static_cast<float>(x0) + ((k & 1u) ? w - 0.5f : 0.5f), inv_w2, -1.0f) * sx;
+        const float ys = fmaf(-(static_cast<float>(y0) + ((k & 2u) ? h - 0.5f : 0.5f)), inv_h2, 1.0f) * sy;
+        const float n = rsqrtf(xs * xs + ys * ys + 1.0f);
+        const float bx = xs * n, by = ys * n, bz = -n;
+        const float cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+        smax = fmaxf(smax, sqrtf(cx * cx + cy * cy + cz * cz));
+    }
+    TileCone c;
+    c.sin_a = fminf(1.0f, smax * 1.01f + 1e-6f);
+    c.cos_a = sqrtf(fmaxf(0.0f, 1.0f - c.sin_a * c.sin_a));
+    for (int k = 0; k < 3; ++k)
+        c.a[k] = static_cast<float>(p.C[3 * k]) * ax + static_cast<float>(p.C[3 * k + 1]) * ay +
+                 static_cast<float>(p.C[3 * k + 2]) * az;
+    return c;
+}
+
 template <typename Real> __device__ __forceinline__ TileCone tile_cone(const FrameParams<Real>& p, int x0, int y0) {
     return region_cone(p, x0, y0, static_cast<float>(kTileW), static_cast<float>(kTileH));
 }
@@ -385,6 +421,11 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     const uint32_t n = p.n_inst;
     BlockStack stack;
     stack.base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack)) + kStackEntry * threadIdx.x;
+#if VXA_STACK_TEN && VXA_STACK_LAYOUT == 2
+    stack.base_ten = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack)) + 8u * kBlock * p.max_depth +
+                     4u * threadIdx.x;
+    asm volatile("" : "+r"(stack.base_ten));
+#endif
     stack.base_top = 0;
     if constexpr (sizeof(Real) == 4 && VXA_SMEM_TOP > 0) {
         // Stage the scene model's first VXA_SMEM_TOP node words (its top levels, BFS
@@ -392,7 +433,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         // completing on an mbarrier, issued by one thread.
         __shared__ __align__(8) unsigned long long top_bar;
         const uint32_t top = static_cast<uint32_t>(__cvta_generic_to_shared(
-            reinterpret_cast<unsigned char*>(smem_stack) + kStackEntry * kBlock * p.max_depth));
+            reinterpret_cast<unsigned char*>(smem_stack) + kStackBytes * kBlock * p.max_depth));
         stack.base_top = top;
         if (p.top_words != nullptr && p.top_n > 0) {
             const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&top_bar));
@@ -429,6 +470,9 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     const uint16_t* const list = s_list[warp];
 
     int prev_band = -1; // band of the warp's previous tile (synchronous readback)
+#if VXA_TILE_PREFETCH
+    uint32_t next_tile = lane == 0 ? atomicAdd(p.tile_counter, 1u) : 0u;
+#endif
     while (true) {
         __syncwarp();
         if (prev_band >= 0) {
@@ -443,10 +487,17 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
             }
         }
+#if VXA_TILE_PREFETCH
+        // the next tile is claimed while this one renders (the atomic's latency hidden)
+        const uint32_t tile = __shfl_sync(0xffffffffu, next_tile, 0);
+        if (tile >= p.n_tiles) break;
+        if (lane == 0) next_tile = atomicAdd(p.tile_counter, 1u);
+#else
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= p.n_tiles) break;
+#endif
         const uint32_t st_k = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
         const uint32_t st = p.super_order != nullptr ? __ldg(p.super_order + st_k) : st_k;
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
@@ -464,7 +515,6 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         uint32_t list_n = 0xffffffffu; // 0xffffffff: per-ray pass over every instance
         {
             if (p.culling && n <= 0xffffu) {
-                const TileCone cone = tile_cone(p, tx0, ty0);
                 // source: the super-tile's candidate list when the pre-pass ran
                 const uint16_t* src = nullptr;
                 uint32_t src_n = n;
@@ -472,11 +522,18 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                     const uint32_t c = __ldg(p.super_count + st);
                     if (c != 0xffffffffu) src = p.super_list + static_cast<size_t>(st) * p.super_cap, src_n = c;
                 }
+                // the pre-pass's per-tile mask over the super-tile's list when it has one
+                // (the same cone tests, done once per tile by one thread instead of per warp)
+                const bool masked = src != nullptr && p.tile_mask != nullptr && src_n <= kListCap;
+                const unsigned long long tmask =
+                    masked ? __ldg(p.tile_mask + static_cast<size_t>(st) * kTilesPerSuper + wt) : 0ull;
+                TileCone cone{};
+                if (!masked) cone = tile_cone(p, tx0, ty0); // warp-uniform branch (the cone shuffles)
                 uint32_t cnt = 0;
                 for (uint32_t base = 0; base < src_n; base += 32) {
                     const uint32_t j = base + lane;
                     const uint32_t i = j < src_n ? (src ? __ldg(src + j) : j) : 0u;
-                    const bool c = j < src_n && cone_candidate(__ldg(p.cull + i), cone);
+                    const bool c = j < src_n && (masked ? ((tmask >> j) & 1ull) != 0 : cone_candidate(__ldg(p.cull + i), cone));
                     const uint32_t m = __ballot_sync(0xffffffffu, c);
                     const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
                     if (c && pos < kListCap) s_list[warp][pos] = static_cast<uint16_t>(i);
@@ -857,6 +914,23 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
             cnt += __popc(m);
         }
         if (lane == 0) count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
+        if (p.tile_mask != nullptr && cnt <= kListCap) {
+            // per 8x4 tile of the super-tile, which entries of its list meet the tile's
+            // cone: lane j takes tiles j, j + 32, ... (one thread per cone)
+            __syncwarp(); // the list entries written above are visible to the whole warp
+            for (uint32_t wt = lane; wt < kTilesPerSuper; wt += 32) {
+                const int tx0 = x0 + static_cast<int>((wt % (kSuper / kTileW)) * kTileW);
+                const int ty0 = y0 + static_cast<int>((wt / (kSuper / kTileW)) * kTileH);
+                unsigned long long m = 0;
+                if (tx0 < p.width && ty0 < p.height) {
+                    const TileCone tc =
+                        region_cone_serial(p, tx0, ty0, static_cast<float>(kTileW), static_cast<float>(kTileH));
+                    for (uint32_t j = 0; j < cnt; ++j)
+                        if (cone_candidate(__ldg(p.cull + out[j]), tc)) m |= 1ull << j;
+                }
+                p.tile_mask[static_cast<size_t>(st) * kTilesPerSuper + wt] = m;
+            }
+        }
     }
     if (p.super_order == nullptr) return;
     __shared__ bool last;

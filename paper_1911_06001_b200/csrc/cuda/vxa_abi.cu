@@ -272,6 +272,7 @@ struct vxa_ctx {
     DevBuf<uint32_t> super_count;
     DevBuf<uint32_t> super_order; // longest-first super-tile order (VXA_LPT)
     DevBuf<uint32_t> super_done;  // pre-pass block tickets (the last block sorts; reset by it)
+    DevBuf<unsigned long long> tile_mask; // per-tile candidate masks over the super-tile lists
     int aux_launches = 0;         // pre-pass kernels since the last stats reset
     unsigned char* inst_host[2] = {nullptr, nullptr};
     size_t inst_host_cap = 0;
@@ -660,6 +661,10 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
         p.super_list = ctx->super_list.ptr;
         p.super_count = ctx->super_count.ptr;
         p.super_cap = kSuperCap;
+        if (VXA_TILE_MASKS) { // per-tile candidate masks from the pre-pass
+            VXA_CUDA(ctx->tile_mask.ensure(std::max<size_t>(mine_super * kTilesPerSuper, 1)));
+            p.tile_mask = ctx->tile_mask.ptr;
+        }
         // Longest-first super-tile order (for a banded synchronous readback: bands in
         // screen order, longest-first inside each); VOXANIM_LPT=0 forces screen order
         // (experiments)
@@ -839,6 +844,7 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->super_count.release();
     ctx->super_order.release();
     ctx->super_done.release();
+    ctx->tile_mask.release();
     ctx->aov.release();
     ctx->hbo.release();
     ctx->rgb.release();

@@ -51,6 +51,11 @@ constexpr int kTilesPerSuper = (kSuper / kTileW) * (kSuper / kTileH); // 128
 #define VXA_SUPER_MIN 32
 #endif
 constexpr uint32_t kSuperCullMin = VXA_SUPER_MIN;
+// The culling pre-pass also writes per-tile candidate masks (1) or the frame
+// kernel tests each tile's cone itself (0).
+#ifndef VXA_TILE_MASKS
+#define VXA_TILE_MASKS 1
+#endif
 constexpr uint32_t kSuperCap = 1024; // super-tile list capacity (overflow: scan all)
 
 // Screen partition: 64x64 super-tile s = (y / 64) * n_super_x + x / 64 belongs
@@ -118,6 +123,24 @@ struct WideNodes {
 // (16-byte entries), so a pop needs no near planes (-3.7 %).
 #ifndef VXA_STACK_TEN
 #define VXA_STACK_TEN 1
+#endif
+// Shared-memory layout of those entries: 0 = 16-byte entries read as 8 + 4 bytes,
+// 1 = 16-byte entries read as one 16-byte access, 2 = an 8-byte and a 4-byte
+// array (12 bytes per level and thread); DESIGN.md §7.
+#ifndef VXA_STACK_LAYOUT
+#define VXA_STACK_LAYOUT 0
+#endif
+// traverse_pos carries the entry parameter clamped at 0 (max(t_enter, 0), the
+// leaf's t rule): the cull's t_exit >= 0 test folds into t_enter < t_exit, and
+// first_node starts at the child holding the origin -- the children before it
+// end behind the origin and are culled by the reference anyway (build variant).
+#ifndef VXA_CLAMP_ENTRY
+#define VXA_CLAMP_ENTRY 0
+#endif
+// inv = 2h / |d| by the approximate division (any per-ray value keeps the planes
+// watertight; 2 ulp) instead of the correctly rounded one (build variant).
+#ifndef VXA_FAST_INV
+#define VXA_FAST_INV 0
 #endif
 #ifndef VXA_FC_SIGN
 #define VXA_FC_SIGN 1
@@ -202,6 +225,10 @@ template <typename Real> struct FrameParams {
     const uint16_t* super_list;
     const uint32_t* super_count;
     uint32_t super_cap;
+    // per 8x4 tile (super-tile major, kTilesPerSuper per super-tile): bit j = entry j of
+    // its super-tile's list meets the tile's cone; written by the pre-pass when the list
+    // has at most 64 entries (null: the frame kernel tests the cones itself)
+    unsigned long long* tile_mask;
     // Processing order of the rank-local super-tiles (super_cull_kernel's last block: most
     // candidates first, so the grid's tail is cheap tiles), or null: natural order.
     const uint32_t* super_order;
@@ -622,7 +649,7 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
             if (m) r.mirror |= axis_bit(a);
             const float A = m ? -A_hi[a] : A_lo[a];
             const float Ar = m ? -Ar_hi[a] : Ar_lo[a];
-            r.inv[a] = __fdiv_rn(h2[a], fabsf(d[a]));
+            r.inv[a] = VXA_FAST_INV ? __fdividef(h2[a], fabsf(d[a])) : __fdiv_rn(h2[a], fabsf(d[a]));
             if (VXA_POSLOOP && r.zero == 0) {
                 // position form: t(P) = fma(P, inv, B), B folded in FP64 and rounded once
                 r.A[a] = __double2float_rn(((static_cast<double>(A) - 1.0) + static_cast<double>(Ar)) *
@@ -662,6 +689,22 @@ template <uint32_t kStride> struct SmemStack {
         asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(base + level * kStride), "r"(v.x), "r"(v.y));
     }
     // VXA_STACK_TEN entries: node word, next octant, and that child's entry parameter
+#if VXA_STACK_LAYOUT == 2
+    // separate [level][thread] arrays: node word + next octant (8 B), entry parameter (4 B)
+    uint32_t base_ten;
+    __device__ __forceinline__ uint2 load3(int level, float& ten) const {
+        uint2 v;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%3];\n\tld.shared.f32 %2, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=f"(ten)
+                     : "r"(base + level * kStride), "r"(base_ten + level * (kStride / 2)));
+        return v;
+    }
+    __device__ __forceinline__ void store3(int level, uint2 v, float ten) const {
+        asm volatile("st.shared.v2.u32 [%0], {%2, %3};\n\tst.shared.f32 [%1], %4;" ::"r"(base + level * kStride),
+                     "r"(base_ten + level * (kStride / 2)), "r"(v.x), "r"(v.y), "f"(ten));
+    }
+#elif VXA_STACK_LAYOUT == 1
+    // 16-byte entries, one 16-byte access
     __device__ __forceinline__ uint2 load3(int level, float& ten) const {
         uint2 v;
         uint32_t t, pad;
@@ -675,6 +718,20 @@ template <uint32_t kStride> struct SmemStack {
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %3};" ::"r"(base + level * kStride), "r"(v.x), "r"(v.y),
                      "r"(__float_as_uint(ten)));
     }
+#else
+    // 16-byte entries, an 8-byte and a 4-byte access
+    __device__ __forceinline__ uint2 load3(int level, float& ten) const {
+        uint2 v;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%3];\n\tld.shared.f32 %2, [%3+8];"
+                     : "=r"(v.x), "=r"(v.y), "=f"(ten)
+                     : "r"(base + level * kStride));
+        return v;
+    }
+    __device__ __forceinline__ void store3(int level, uint2 v, float ten) const {
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n\tst.shared.f32 [%0+8], %3;" ::"r"(base + level * kStride),
+                     "r"(v.x), "r"(v.y), "f"(ten));
+    }
+#endif
 };
 
 struct LocalStack {
@@ -884,6 +941,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
             t1[a] = __fmaf_rn(2.0f, r.inv[a], r.A[a]);
         }
         ten = fmaxf(fmaxf(t0[0], t0[1]), t0[2]);
+        if constexpr (VXA_CLAMP_ENTRY) ten = fmaxf(ten, 0.0f);
     }
     typename Nodes::Word fw = nodes.load(0);
     uint32_t fidx = 0, fetches = 1;
@@ -919,7 +977,10 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
                 t1[a] = __fmaf_rn(lo + size, r.inv[a], r.A[a]);
                 if constexpr (!VXA_STACK_TEN) c0[a] = (q & axis_bit(a)) ? tm[a] : __fmaf_rn(lo, r.inv[a], r.A[a]);
             }
-            if constexpr (!VXA_STACK_TEN) ten = fmaxf(fmaxf(c0[0], c0[1]), c0[2]); // entry of the saved next child
+            if constexpr (!VXA_STACK_TEN) {
+                ten = fmaxf(fmaxf(c0[0], c0[1]), c0[2]); // entry of the saved next child
+                if constexpr (VXA_CLAMP_ENTRY) ten = fmaxf(ten, 0.0f);
+            }
             // (falls through: the ancestor's saved next child is stepped now)
         }
         const uint32_t q = fcur;
@@ -938,7 +999,11 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         const uint32_t bit = 1u << oct;
         const uint32_t valid = Nodes::valid(fw);
         if (!(valid & bit)) continue;
-        if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
+        if constexpr (VXA_CLAMP_ENTRY) {
+            if (!(t_enter < fminf(t_exit, r.t_lim))) continue; // t_enter >= 0: also culls t_exit < 0
+        } else {
+            if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
+        }
         bool is_leaf;
         uint32_t leafm;
         if constexpr (Nodes::kLastLevelLeaves) {
@@ -950,7 +1015,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         }
         if (is_leaf) {
             out.attr = nodes.attr_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & leafm, bit);
-            out.t = fmaxf(t_enter, 0.0f);
+            out.t = VXA_CLAMP_ENTRY ? t_enter : fmaxf(t_enter, 0.0f);
             out.parent = fidx;
             out.level = static_cast<uint32_t>(level + 1);
             // entry axis: argmax of the child's near planes, ties to the lower axis
