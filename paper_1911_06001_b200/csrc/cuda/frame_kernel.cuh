@@ -49,6 +49,16 @@ constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions
 // entry parameters in a second array of half that stride)
 constexpr uint32_t kStackEntry = (VXA_STACK_TEN && VXA_STACK_LAYOUT != 2) ? 16u : 8u;
 constexpr uint32_t kStackBytes = VXA_STACK_TEN ? (VXA_STACK_LAYOUT == 2 ? 12u : 16u) : 8u; // per thread per level
+// Stack levels a frame needs: a node is saved only when one of its internal
+// children is pushed, i.e. at levels <= depth - 2 (VXA_STACK_TRIM; else depth).
+// Together with layout 2: 15 KB of stack per block at C4 instead of 22.5 (-1.1 %).
+#ifndef VXA_STACK_TRIM
+#define VXA_STACK_TRIM 1
+#endif
+__host__ __device__ inline uint32_t stack_levels(uint32_t max_depth) {
+    const uint32_t d = max_depth > 0 ? max_depth : 1u;
+    return VXA_STACK_TRIM ? (d > 1 ? d - 1 : 1u) : d;
+}
 struct BlockStack : SmemStack<kBlock * kStackEntry> {
     uint32_t base_top; // shared address of the staged top node words (VXA_SMEM_TOP)
 };
@@ -422,7 +432,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     BlockStack stack;
     stack.base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack)) + kStackEntry * threadIdx.x;
 #if VXA_STACK_TEN && VXA_STACK_LAYOUT == 2
-    stack.base_ten = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack)) + 8u * kBlock * p.max_depth +
+    stack.base_ten = static_cast<uint32_t>(__cvta_generic_to_shared(smem_stack)) + 8u * kBlock * stack_levels(p.max_depth) +
                      4u * threadIdx.x;
     asm volatile("" : "+r"(stack.base_ten));
 #endif
@@ -433,7 +443,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         // completing on an mbarrier, issued by one thread.
         __shared__ __align__(8) unsigned long long top_bar;
         const uint32_t top = static_cast<uint32_t>(__cvta_generic_to_shared(
-            reinterpret_cast<unsigned char*>(smem_stack) + kStackBytes * kBlock * p.max_depth));
+            reinterpret_cast<unsigned char*>(smem_stack) + kStackBytes * kBlock * stack_levels(p.max_depth)));
         stack.base_top = top;
         if (p.top_words != nullptr && p.top_n > 0) {
             const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&top_bar));

@@ -48,7 +48,7 @@ cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint3
 }
 
 size_t frame_smem_bytes_f32(uint32_t max_depth) {
-    return kStackBytes * kBlock * (max_depth > 0 ? max_depth : 1) + 4u * VXA_SMEM_TOP;
+    return kStackBytes * kBlock * stack_levels(max_depth) + 4u * VXA_SMEM_TOP;
 }
 
 int frame_blocks_per_sm_f32(bool aov, int hbo, bool compact, uint32_t max_depth) {

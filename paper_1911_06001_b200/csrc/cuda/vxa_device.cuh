@@ -126,9 +126,9 @@ struct WideNodes {
 #endif
 // Shared-memory layout of those entries: 0 = 16-byte entries read as 8 + 4 bytes,
 // 1 = 16-byte entries read as one 16-byte access, 2 = an 8-byte and a 4-byte
-// array (12 bytes per level and thread); DESIGN.md §7.
+// array (12 bytes per level and thread: less shared memory, more L1).
 #ifndef VXA_STACK_LAYOUT
-#define VXA_STACK_LAYOUT 0
+#define VXA_STACK_LAYOUT 2
 #endif
 // traverse_pos carries the entry parameter clamped at 0 (max(t_enter, 0), the
 // leaf's t rule): the cull's t_exit >= 0 test folds into t_enter < t_exit, and

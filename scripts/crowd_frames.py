@@ -1,5 +1,8 @@
 """Renders a few frames of the CROWD configuration (for ncu captures)."""
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_1911_06001_b200 as vx
 
