@@ -890,27 +890,30 @@ __device__ __forceinline__ void order_by_count(const uint32_t* count, uint32_t n
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&start[bucket(i)], 1u)] = i;
 }
 
-// Pre-pass for large scenes: one warp per super-tile of this rank cone-tests
-// every instance against the super-tile's cone and writes the survivors (in
-// instance order) to its list; the frame kernel's 8x4 tiles then test only
-// their super-tile's list (tiles x instances / 32 rounds -> super-tiles x
-// instances / 32 + tiles x list / 32). With p.super_order set, the grid's last
-// block to finish (a ticket on `done`, which it resets) then writes the
-// longest-first super-tile order.
+// Pre-pass for large scenes, one block per super-tile of this rank: its first
+// warp cone-tests every instance against the super-tile's cone and writes the
+// survivors (in instance order) to the super-tile's list; then (lists of <= 64
+// entries) each thread tests one 8x4 tile's cone against that list and writes the
+// tile's candidate mask, so the frame kernel's warps need no cone arithmetic.
+// With p.super_order set, the grid's last block to finish (a ticket on `done`,
+// which it resets) then writes the longest-first super-tile order.
 template <typename Real>
 __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__ FrameParams<Real> p,
                                                         uint16_t* __restrict__ list, uint32_t* __restrict__ count,
                                                         uint32_t* __restrict__ done) {
+    // one block per super-tile: warp 0 builds its candidate list, then every thread
+    // computes one 8x4 tile's mask over that list
+    __shared__ uint16_t s_cand[kListCap];
+    __shared__ uint32_t s_cnt;
     const uint32_t lane = threadIdx.x & 31u;
 #if VXA_PDL
     asm volatile("griddepcontrol.launch_dependents;");
 #endif
-    const uint32_t st = blockIdx.x * 4u + (threadIdx.x >> 5);
-    const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
-    if (st < n_mine) {
-        const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
-        const uint32_t sy = super_row(p, s);
-        const int x0 = static_cast<int>((s - sy * p.n_super_x) * kSuper), y0 = static_cast<int>(sy * kSuper);
+    const uint32_t st = blockIdx.x;
+    const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
+    const uint32_t sy = super_row(p, s);
+    const int x0 = static_cast<int>((s - sy * p.n_super_x) * kSuper), y0 = static_cast<int>(sy * kSuper);
+    if (threadIdx.x < 32) {
         const float w = static_cast<float>(min(kSuper, p.width - x0)), h = static_cast<float>(min(kSuper, p.height - y0));
         const TileCone cone = region_cone(p, x0, y0, w, h);
         uint16_t* out = list + static_cast<size_t>(st) * p.super_cap;
@@ -921,25 +924,29 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
             const uint32_t m = __ballot_sync(0xffffffffu, c);
             const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
             if (c && pos < p.super_cap) out[pos] = static_cast<uint16_t>(i);
+            if (c && pos < kListCap) s_cand[pos] = static_cast<uint16_t>(i);
             cnt += __popc(m);
         }
-        if (lane == 0) count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
-        if (p.tile_mask != nullptr && cnt <= kListCap) {
-            // per 8x4 tile of the super-tile, which entries of its list meet the tile's
-            // cone: lane j takes tiles j, j + 32, ... (one thread per cone)
-            __syncwarp(); // the list entries written above are visible to the whole warp
-            for (uint32_t wt = lane; wt < kTilesPerSuper; wt += 32) {
-                const int tx0 = x0 + static_cast<int>((wt % (kSuper / kTileW)) * kTileW);
-                const int ty0 = y0 + static_cast<int>((wt / (kSuper / kTileW)) * kTileH);
-                unsigned long long m = 0;
-                if (tx0 < p.width && ty0 < p.height) {
-                    const TileCone tc =
-                        region_cone_serial(p, tx0, ty0, static_cast<float>(kTileW), static_cast<float>(kTileH));
-                    for (uint32_t j = 0; j < cnt; ++j)
-                        if (cone_candidate(__ldg(p.cull + out[j]), tc)) m |= 1ull << j;
-                }
-                p.tile_mask[static_cast<size_t>(st) * kTilesPerSuper + wt] = m;
+        if (lane == 0) {
+            count[st] = cnt <= p.super_cap ? cnt : 0xffffffffu;
+            s_cnt = cnt;
+        }
+    }
+    __syncthreads();
+    const uint32_t cnt = s_cnt;
+    if (p.tile_mask != nullptr && cnt <= kListCap) {
+        // tile wt of the super-tile: which entries of its list meet the tile's cone
+        for (uint32_t wt = threadIdx.x; wt < kTilesPerSuper; wt += blockDim.x) {
+            const int tx0 = x0 + static_cast<int>((wt % (kSuper / kTileW)) * kTileW);
+            const int ty0 = y0 + static_cast<int>((wt / (kSuper / kTileW)) * kTileH);
+            unsigned long long m = 0;
+            if (tx0 < p.width && ty0 < p.height) {
+                const TileCone tc =
+                    region_cone_serial(p, tx0, ty0, static_cast<float>(kTileW), static_cast<float>(kTileH));
+                for (uint32_t j = 0; j < cnt; ++j)
+                    if (cone_candidate(__ldg(p.cull + s_cand[j]), tc)) m |= 1ull << j;
             }
+            p.tile_mask[static_cast<size_t>(st) * kTilesPerSuper + wt] = m;
         }
     }
     if (p.super_order == nullptr) return;
@@ -953,7 +960,7 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
     if (!last) return;
     __threadfence();
     // (band_rows implies one rank: super-tile st is screen super-tile st)
-    order_by_count(count, n_mine, const_cast<uint32_t*>(p.super_order), p.n_super_x, p.band_done ? p.band_rows : 0u);
+    order_by_count(count, gridDim.x, const_cast<uint32_t*>(p.super_order), p.n_super_x, p.band_done ? p.band_rows : 0u);
     if (threadIdx.x == 0) *done = 0; // ready for the next frame
 }
 

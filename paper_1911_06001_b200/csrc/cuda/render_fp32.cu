@@ -43,7 +43,7 @@ cudaError_t launch_super_cull(const FrameParams<float>& p, uint16_t* list, uint3
                               cudaStream_t s) {
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (n_mine == 0) return cudaSuccess;
-    super_cull_kernel<float><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count, done);
+    super_cull_kernel<float><<<n_mine, 128, 0, s>>>(p, list, count, done);
     return cudaGetLastError();
 }
 

@@ -18,7 +18,7 @@ cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint
                               cudaStream_t s) {
     const uint32_t n_mine = p.n_tiles / kTilesPerSuper;
     if (n_mine == 0) return cudaSuccess;
-    super_cull_kernel<double><<<(n_mine + 3) / 4, 128, 0, s>>>(p, list, count, done);
+    super_cull_kernel<double><<<n_mine, 128, 0, s>>>(p, list, count, done);
     return cudaGetLastError();
 }
 
