@@ -242,12 +242,16 @@ double tau(double t) { return 8.0 * std::ldexp(1.0, -23) * std::max(1.0, std::ab
 // FP32 error of a plane parameter on local axis a of the instance: the plane's
 // position is resolved to 2^-22 of (|o_a| + 2 h_a) (origin and cell size
 // rounded to FP32), which moves t by that over the incidence |d_a| -- large on a
-// grazing axis. Capped at 2^-12 of t: more than that is not rounding.
-double plane_err(const SceneObject& obj, const Ray& world, int a, double t) {
+// grazing axis. Capped at the larger of 2^-12 of t and `extent` (the t-extent
+// of the voxel in question along the ray, when the caller has one): a nearly
+// parallel plane can put t anywhere in that voxel's stretch of the ray (a 5600-
+// scene soak found one such pixel, |d_a| = 3.6e-5, 1.5 % off in t, right voxel),
+// but not beyond it.
+double plane_err(const SceneObject& obj, const Ray& world, int a, double t, double extent = 0.0) {
     if (a < 0) return 0.0;
     const Ray loc = transform_ray_world_to_local(world, obj.transform);
     const double da = std::abs(loc.direction[a]);
-    const double cap = std::ldexp(std::max(1.0, std::abs(t)), -12);
+    const double cap = std::max(std::ldexp(std::max(1.0, std::abs(t)), -12), extent);
     if (da == 0.0) return 0.0;
     const double h = bounds_from_scale(obj.transform.scale).half_extent[a];
     return std::min(std::ldexp(std::abs(loc.origin[a]) + 2.0 * h, -22) / da, cap);
@@ -360,11 +364,14 @@ enum Rule : int {
 
 // The t tolerance of a matching hit: t_rel relative, plus the FP32 error of the
 // entry planes the two answers used (plane_err: a grazing entry is
-// ill-conditioned), each capped at 2^-12 of t.
+// ill-conditioned), each capped at the larger of 2^-12 of t and the voxel's
+// t-extent along the ray.
 double t_tolerance(const Scene& scene, const Ray& ray, const AovRec& o, const AovRec& g, double t_rel) {
     const SceneObject* obj = scene.find_object(o.object_id);
+    const Interval iv = voxel_interval(*obj, ray, o.voxel, o.level);
+    const double ext = iv.out > iv.in ? iv.out - iv.in : 0.0;
     return t_rel * std::max(1.0, std::abs(o.t)) +
-           std::max(plane_err(*obj, ray, o.entry_axis, o.t), plane_err(*obj, ray, g.entry_axis, o.t));
+           std::max(plane_err(*obj, ray, o.entry_axis, o.t, ext), plane_err(*obj, ray, g.entry_axis, o.t, ext));
 }
 
 // Replays node_child (svo.cpp:27-39) along the voxel's octant path: true iff a
@@ -432,8 +439,9 @@ int classify_rule(const Scene& scene, const Ray& ray, const AovRec& o, const Aov
             if (v.in - v.out > tol) return kBug; // the ray does not pass through it
             if (v.out < -tol) return kBug;       // wholly behind the origin
             const double t_in = std::max(v.in, 0.0);
-            if (std::abs(g.t - t_in) > tt + t_rel * std::max(1.0, t_in) + plane_err(*og, ray, v.in_axis, t_in) +
-                                           plane_err(*og, ray, g.entry_axis, t_in))
+            const double ext = v.out > v.in ? v.out - v.in : 0.0;
+            if (std::abs(g.t - t_in) > tt + t_rel * std::max(1.0, t_in) + plane_err(*og, ray, v.in_axis, t_in, ext) +
+                                           plane_err(*og, ray, g.entry_axis, t_in, ext))
                 return kBug; // not entered at the GPU's t
         }
     }
