@@ -142,10 +142,6 @@ struct WideNodes {
 #ifndef VXA_FAST_INV
 #define VXA_FAST_INV 0
 #endif
-// traverse_pos prefetches a node's children's words into L1 at its steps (variant).
-#ifndef VXA_PREFETCH
-#define VXA_PREFETCH 0
-#endif
 #ifndef VXA_FC_SIGN
 #define VXA_FC_SIGN 1
 #endif
@@ -181,9 +177,6 @@ struct CompactNodes {
         return __ldg(w + i);
     }
     __device__ __forceinline__ static uint32_t valid(Word x) { return x & 0xffu; }
-    __device__ __forceinline__ void prefetch(uint32_t i) const {
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(w + i));
-    }
     __device__ __forceinline__ static uint32_t leaves(Word x, int level, int depth) {
         return level + 1 == depth ? (x & 0xffu) : 0u;
     }
@@ -1005,11 +998,6 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         const uint32_t oct = q ^ r.mirror;
         const uint32_t bit = 1u << oct;
         const uint32_t valid = Nodes::valid(fw);
-        if constexpr (VXA_PREFETCH && Nodes::kLastLevelLeaves) {
-            // the node's internal children are contiguous: bring their words' line into
-            // L1 now, so the push into one of them finds it there
-            if (level + 2 < depth) nodes.prefetch(Nodes::child_base(fw));
-        }
         if (!(valid & bit)) continue;
         if constexpr (VXA_CLAMP_ENTRY) {
             if (!(t_enter < fminf(t_exit, r.t_lim))) continue; // t_enter >= 0: also culls t_exit < 0
