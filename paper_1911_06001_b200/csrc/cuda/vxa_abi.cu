@@ -118,10 +118,22 @@ __device__ __forceinline__ uint32_t local_normal_meta(const float* R, const doub
     return (axis << 2) | (neg << 4);
 }
 
-// 48-byte records -> 16-byte ones against the frame's instance table (first
-// instance with the record's id, the reference's find_object rule).
+// Instance of an object id: binary search of a (id, first instance index) table
+// sorted by id (the reference's find_object rule: the first object with the id).
+__device__ __forceinline__ int find_instance(const int2* __restrict__ map, uint32_t n, int32_t id) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (map[mid].x < id) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < n && map[lo].x == id) ? map[lo].y : -1;
+}
+
+// 48-byte records -> 16-byte ones against the frame's instance table.
 __global__ void hbo_compress(const HitRec* __restrict__ in, HitRec16* __restrict__ out, size_t n,
-                             const DevInstance<float>* __restrict__ inst, uint32_t n_inst) {
+                             const DevInstance<float>* __restrict__ inst, const int2* __restrict__ map,
+                             uint32_t map_n) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const HitRec r = in[i];
@@ -131,27 +143,23 @@ __global__ void hbo_compress(const HitRec* __restrict__ in, HitRec16* __restrict
     c.object_id = r.object_id;
     c.meta = r.kind & 3u;
     if (r.kind != 0) {
-        for (uint32_t k = 0; k < n_inst; ++k)
-            if (inst[k].id == r.object_id) {
-                c.meta |= local_normal_meta(inst[k].R, r.normal);
-                break;
-            }
+        const int k = find_instance(map, map_n, r.object_id);
+        if (k >= 0) c.meta |= local_normal_meta(inst[k].R, r.normal);
     }
     out[i] = c;
 }
 
-// The rotation and id of every instance of an FP32 frame (for later expansion).
+// The rotation of every instance of an FP32 frame (for later expansion).
 __global__ void hbo_save_table(const DevInstance<float>* __restrict__ inst, uint32_t n_inst, float* __restrict__ tab) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_inst) return;
-    for (int j = 0; j < 9; ++j) tab[10 * k + j] = inst[k].R[j];
-    tab[10 * k + 9] = __int_as_float(inst[k].id);
+    for (int j = 0; j < 9; ++j) tab[9 * k + j] = inst[k].R[j];
 }
 
 // 16-byte records -> 48-byte host-layout ones: the normal is +-column `axis` of
 // the object's R (the FP32 kernel's best_normal), as the 48-byte path stores it.
 __global__ void hbo_expand(const HitRec16* __restrict__ in, HitRec* __restrict__ out, size_t n,
-                           const float* __restrict__ tab, uint32_t n_inst) {
+                           const float* __restrict__ tab, const int2* __restrict__ map, uint32_t map_n) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const HitRec16 c = in[i];
@@ -166,13 +174,11 @@ __global__ void hbo_expand(const HitRec16* __restrict__ in, HitRec* __restrict__
     if (r.kind != 0) {
         const uint32_t axis = (c.meta >> 2) & 3u;
         const bool neg = (c.meta & 16u) != 0;
-        for (uint32_t k = 0; k < n_inst; ++k)
-            if (__float_as_int(tab[10 * k + 9]) == c.object_id) {
-                for (int j = 0; j < 3; ++j) {
-                    const float v = tab[10 * k + 3 * j + axis];
-                    r.normal[j] = static_cast<double>(neg ? -v : v);
-                }
-                break;
+        const int k = find_instance(map, map_n, c.object_id);
+        if (k >= 0)
+            for (int j = 0; j < 3; ++j) {
+                const float v = tab[9 * k + 3 * j + axis];
+                r.normal[j] = static_cast<double>(neg ? -v : v);
             }
     }
     out[i] = r;
@@ -273,6 +279,7 @@ struct vxa_ctx {
     DevBuf<uint32_t> super_order; // longest-first super-tile order (VXA_LPT)
     DevBuf<uint32_t> super_done;  // pre-pass block tickets (the last block sorts; reset by it)
     DevBuf<unsigned long long> tile_mask; // per-tile candidate masks over the super-tile lists
+    DevBuf<int2> id_map;                  // (object id, first instance) sorted by id: hit-buffer conversions
     int aux_launches = 0;         // pre-pass kernels since the last stats reset
     unsigned char* inst_host[2] = {nullptr, nullptr};
     size_t inst_host_cap = 0;
@@ -283,7 +290,8 @@ struct vxa_ctx {
         HitRec* rec = nullptr;     // 48-byte host-layout records (FP64 frames, host access)
         HitRec16* rec16 = nullptr; // 16-byte records of FP32 frames (allocated on first FP32 use)
         bool compact = false;      // rec16 holds the current records
-        DevBuf<float> tab;         // R (9 floats) + id bits per instance of the last FP32 frame (expansion)
+        DevBuf<float> tab;         // R (9 floats) per instance of the last FP32 frame (expansion)
+        std::vector<int32_t> tab_ids; // that frame's object ids, in instance order
         uint32_t tab_n = 0;
         int32_t w = 0, h = 0;
     };
@@ -314,6 +322,7 @@ struct vxa_ctx {
     uint32_t* next_band_done = nullptr;
     uint32_t next_band_rows = 0;
     cudaEvent_t band_reset = nullptr;
+    cudaEvent_t band_trace[16] = {}; // VOXANIM_BAND_TRACE: per-band copy completion events
     cudaStream_t copy_stream2 = nullptr; // second D2H stream of the banded readback (bands alternate)
     int band_api = 0; // 0 unknown, 1 cuStreamWaitValue32 usable, -1 not
     void* wait_value32 = nullptr;
@@ -486,6 +495,23 @@ int check_frame(const vxa_frame_desc* f) {
     return VXA_OK;
 }
 
+// Uploads the (object id, first instance index) table of `ids`, sorted by id, for
+// the hit-buffer conversions; returns its length.
+int upload_id_map(vxa_ctx* ctx, const int32_t* ids, uint32_t n, uint32_t* map_n) {
+    std::vector<int2> m;
+    m.reserve(n);
+    for (uint32_t k = 0; k < n; ++k) m.push_back(make_int2(ids[k], static_cast<int>(k)));
+    std::stable_sort(m.begin(), m.end(), [](const int2& a, const int2& b) { return a.x < b.x; });
+    m.erase(std::unique(m.begin(), m.end(), [](const int2& a, const int2& b) { return a.x == b.x; }), m.end());
+    VXA_CUDA(ctx->id_map.ensure(std::max<size_t>(m.size(), 1)));
+    if (!m.empty())
+        VXA_CUDA(cudaMemcpyAsync(ctx->id_map.ptr, m.data(), m.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    VXA_CUDA(cudaStreamSynchronize(ctx->stream)); // the host vector goes out of scope
+    *map_n = static_cast<uint32_t>(m.size());
+    return VXA_OK;
+}
+
 // Enqueues one frame. aov/hbo are device buffers or null.
 template <typename Real>
 int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov,
@@ -623,8 +649,13 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
         const unsigned blocks = static_cast<unsigned>((npix_hbo + 255) / 256);
         if (want_compact) {
             if (!dev_hbo->compact) {
+                std::vector<int32_t> ids(n);
+                for (uint32_t k = 0; k < n; ++k) ids[k] = in[k].id;
+                uint32_t map_n = 0;
+                if (int rc = upload_id_map(ctx, ids.data(), n, &map_n); rc != VXA_OK) return rc;
                 hbo_compress<<<blocks, 256, 0, ctx->stream>>>(dev_hbo->rec, dev_hbo->rec16, npix_hbo,
-                                                              reinterpret_cast<const DevInstance<float>*>(p.inst), n);
+                                                              reinterpret_cast<const DevInstance<float>*>(p.inst),
+                                                              ctx->id_map.ptr, map_n);
                 VXA_CUDA(cudaGetLastError());
                 dev_hbo->compact = true;
             }
@@ -632,8 +663,11 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
             p.hbo_compact = 1;
         } else {
             if (dev_hbo->compact) {
+                uint32_t map_n = 0;
+                if (int rc = upload_id_map(ctx, dev_hbo->tab_ids.data(), dev_hbo->tab_n, &map_n); rc != VXA_OK)
+                    return rc;
                 hbo_expand<<<blocks, 256, 0, ctx->stream>>>(dev_hbo->rec16, dev_hbo->rec, npix_hbo, dev_hbo->tab.ptr,
-                                                            dev_hbo->tab_n);
+                                                            ctx->id_map.ptr, map_n);
                 VXA_CUDA(cudaGetLastError());
                 dev_hbo->compact = false;
             }
@@ -686,11 +720,13 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     VXA_CUDA(cudaEventRecord(ctx->k_end[slot_k], ctx->stream));
     if (dev_hbo != nullptr && p.hbo_compact) {
         // the instances the records refer to, for a later expansion (download, FP64 frame)
-        VXA_CUDA(dev_hbo->tab.ensure(std::max<size_t>(size_t{10} * n, 10)));
+        VXA_CUDA(dev_hbo->tab.ensure(std::max<size_t>(size_t{9} * n, 9)));
         if (n) hbo_save_table<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
             reinterpret_cast<const DevInstance<float>*>(p.inst), n, dev_hbo->tab.ptr);
         VXA_CUDA(cudaGetLastError());
         dev_hbo->tab_n = n;
+        dev_hbo->tab_ids.resize(n);
+        for (uint32_t k = 0; k < n; ++k) dev_hbo->tab_ids[k] = in[k].id;
     }
     VXA_CUDA(cudaEventRecord(ctx->inst_free[slot], ctx->stream)); // this table slot may be overwritten now
     ++ctx->k_count;
@@ -845,12 +881,15 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->super_order.release();
     ctx->super_done.release();
     ctx->tile_mask.release();
+    ctx->id_map.release();
     ctx->aov.release();
     ctx->hbo.release();
     ctx->rgb.release();
     ctx->l2_scratch.release();
     ctx->band_done.release();
     if (ctx->band_reset) cudaEventDestroy(ctx->band_reset);
+    for (cudaEvent_t e : ctx->band_trace)
+        if (e) cudaEventDestroy(e);
     ctx->rays.release();
     ctx->hits.release();
     ctx->visits.release();
@@ -1320,9 +1359,9 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
             const char* e = std::getenv("VOXANIM_BAND_TRACE");
             return e && std::strcmp(e, "1") == 0;
         }();
-        static cudaEvent_t trace_ev[16] = {};
+        cudaEvent_t* const trace_ev = ctx->band_trace;
         if (trace && trace_ev[0] == nullptr)
-            for (auto& e : trace_ev) VXA_CUDA(cudaEventCreate(&e));
+            for (int b = 0; b < 16; ++b) VXA_CUDA(cudaEventCreate(&trace_ev[b]));
         using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
         const auto wait = reinterpret_cast<WaitFn>(ctx->wait_value32);
         const size_t row_bytes = static_cast<size_t>(f->camera.width) * 3;
@@ -1444,8 +1483,10 @@ int vxa_hbo_download(vxa_ctx* ctx, uint32_t handle, vxa_hit_record* out) {
     const HitRec* src = it->second.rec;
     if (it->second.compact) { // FP32 frames left 16-byte records: expand them (the buffer stays compact)
         VXA_CUDA(ctx->hbo.ensure(n));
+        uint32_t map_n = 0;
+        if (int rc = upload_id_map(ctx, it->second.tab_ids.data(), it->second.tab_n, &map_n); rc != VXA_OK) return rc;
         hbo_expand<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
-            it->second.rec16, ctx->hbo.ptr, n, it->second.tab.ptr, it->second.tab_n);
+            it->second.rec16, ctx->hbo.ptr, n, it->second.tab.ptr, ctx->id_map.ptr, map_n);
         VXA_CUDA(cudaGetLastError());
         src = ctx->hbo.ptr;
     }
