@@ -39,10 +39,6 @@ constexpr int kBlock = 128;
 #ifndef VXA_ZERO_SPLIT
 #define VXA_ZERO_SPLIT 1
 #endif
-// VXA_TILE_PREFETCH: claim the next warp tile while the current one renders.
-#ifndef VXA_TILE_PREFETCH
-#define VXA_TILE_PREFETCH 0
-#endif
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kListCap = 64; // per-warp tile candidate list (bit positions of a u64 mask)
 // bytes per thread per level (the node-word part's stride; layout 2 keeps the
@@ -480,9 +476,6 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
     const uint16_t* const list = s_list[warp];
 
     int prev_band = -1; // band of the warp's previous tile (synchronous readback)
-#if VXA_TILE_PREFETCH
-    uint32_t next_tile = lane == 0 ? atomicAdd(p.tile_counter, 1u) : 0u;
-#endif
     while (true) {
         __syncwarp();
         if (prev_band >= 0) {
@@ -497,17 +490,10 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
             }
         }
-#if VXA_TILE_PREFETCH
-        // the next tile is claimed while this one renders (the atomic's latency hidden)
-        const uint32_t tile = __shfl_sync(0xffffffffu, next_tile, 0);
-        if (tile >= p.n_tiles) break;
-        if (lane == 0) next_tile = atomicAdd(p.tile_counter, 1u);
-#else
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(p.tile_counter, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= p.n_tiles) break;
-#endif
         const uint32_t st_k = tile / kTilesPerSuper, wt = tile % kTilesPerSuper;
         const uint32_t st = p.super_order != nullptr ? __ldg(p.super_order + st_k) : st_k;
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);

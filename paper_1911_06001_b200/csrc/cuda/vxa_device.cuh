@@ -125,22 +125,10 @@ struct WideNodes {
 #define VXA_STACK_TEN 1
 #endif
 // Shared-memory layout of those entries: 0 = 16-byte entries read as 8 + 4 bytes,
-// 1 = 16-byte entries read as one 16-byte access, 2 = an 8-byte and a 4-byte
-// array (12 bytes per level and thread: less shared memory, more L1).
+// 2 = an 8-byte and a 4-byte array (12 bytes per level and thread: less shared
+// memory, more L1).
 #ifndef VXA_STACK_LAYOUT
 #define VXA_STACK_LAYOUT 2
-#endif
-// traverse_pos carries the entry parameter clamped at 0 (max(t_enter, 0), the
-// leaf's t rule): the cull's t_exit >= 0 test folds into t_enter < t_exit, and
-// first_node starts at the child holding the origin -- the children before it
-// end behind the origin and are culled by the reference anyway (build variant).
-#ifndef VXA_CLAMP_ENTRY
-#define VXA_CLAMP_ENTRY 0
-#endif
-// inv = 2h / |d| by the approximate division (any per-ray value keeps the planes
-// watertight; 2 ulp) instead of the correctly rounded one (build variant).
-#ifndef VXA_FAST_INV
-#define VXA_FAST_INV 0
 #endif
 #ifndef VXA_FC_SIGN
 #define VXA_FC_SIGN 1
@@ -649,7 +637,7 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
             if (m) r.mirror |= axis_bit(a);
             const float A = m ? -A_hi[a] : A_lo[a];
             const float Ar = m ? -Ar_hi[a] : Ar_lo[a];
-            r.inv[a] = VXA_FAST_INV ? __fdividef(h2[a], fabsf(d[a])) : __fdiv_rn(h2[a], fabsf(d[a]));
+            r.inv[a] = __fdiv_rn(h2[a], fabsf(d[a]));
             if (VXA_POSLOOP && r.zero == 0) {
                 // position form: t(P) = fma(P, inv, B), B folded in FP64 and rounded once
                 r.A[a] = __double2float_rn(((static_cast<double>(A) - 1.0) + static_cast<double>(Ar)) *
@@ -702,21 +690,6 @@ template <uint32_t kStride> struct SmemStack {
     __device__ __forceinline__ void store3(int level, uint2 v, float ten) const {
         asm volatile("st.shared.v2.u32 [%0], {%2, %3};\n\tst.shared.f32 [%1], %4;" ::"r"(base + level * kStride),
                      "r"(base_ten + level * (kStride / 2)), "r"(v.x), "r"(v.y), "f"(ten));
-    }
-#elif VXA_STACK_LAYOUT == 1
-    // 16-byte entries, one 16-byte access
-    __device__ __forceinline__ uint2 load3(int level, float& ten) const {
-        uint2 v;
-        uint32_t t, pad;
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(t), "=r"(pad)
-                     : "r"(base + level * kStride));
-        ten = __uint_as_float(t);
-        return v;
-    }
-    __device__ __forceinline__ void store3(int level, uint2 v, float ten) const {
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %3};" ::"r"(base + level * kStride), "r"(v.x), "r"(v.y),
-                     "r"(__float_as_uint(ten)));
     }
 #else
     // 16-byte entries, an 8-byte and a 4-byte access
@@ -941,7 +914,6 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
             t1[a] = __fmaf_rn(2.0f, r.inv[a], r.A[a]);
         }
         ten = fmaxf(fmaxf(t0[0], t0[1]), t0[2]);
-        if constexpr (VXA_CLAMP_ENTRY) ten = fmaxf(ten, 0.0f);
     }
     typename Nodes::Word fw = nodes.load(0);
     uint32_t fidx = 0, fetches = 1;
@@ -977,10 +949,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
                 t1[a] = __fmaf_rn(lo + size, r.inv[a], r.A[a]);
                 if constexpr (!VXA_STACK_TEN) c0[a] = (q & axis_bit(a)) ? tm[a] : __fmaf_rn(lo, r.inv[a], r.A[a]);
             }
-            if constexpr (!VXA_STACK_TEN) {
-                ten = fmaxf(fmaxf(c0[0], c0[1]), c0[2]); // entry of the saved next child
-                if constexpr (VXA_CLAMP_ENTRY) ten = fmaxf(ten, 0.0f);
-            }
+            if constexpr (!VXA_STACK_TEN) ten = fmaxf(fmaxf(c0[0], c0[1]), c0[2]); // entry of the saved next child
             // (falls through: the ancestor's saved next child is stepped now)
         }
         const uint32_t q = fcur;
@@ -999,11 +968,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         const uint32_t bit = 1u << oct;
         const uint32_t valid = Nodes::valid(fw);
         if (!(valid & bit)) continue;
-        if constexpr (VXA_CLAMP_ENTRY) {
-            if (!(t_enter < fminf(t_exit, r.t_lim))) continue; // t_enter >= 0: also culls t_exit < 0
-        } else {
-            if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
-        }
+        if (!(t_enter < fminf(t_exit, r.t_lim)) || t_exit < 0.0f) continue;
         bool is_leaf;
         uint32_t leafm;
         if constexpr (Nodes::kLastLevelLeaves) {
@@ -1015,7 +980,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         }
         if (is_leaf) {
             out.attr = nodes.attr_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & leafm, bit);
-            out.t = VXA_CLAMP_ENTRY ? t_enter : fmaxf(t_enter, 0.0f);
+            out.t = fmaxf(t_enter, 0.0f);
             out.parent = fidx;
             out.level = static_cast<uint32_t>(level + 1);
             // entry axis: argmax of the child's near planes, ties to the lower axis
