@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             // warp barrier orders the lanes' stores before lane 0's gpu-scope release
             // increment (cumulative) -- one release per tile, not 32 fences. (Adding a
             // warp's tiles per band once it leaves the band costs fewer releases but
-            // signals the bands late: the D2H overlapped less, DESIGN.md §12.)
+            // signals the bands late: the D2H overlapped less, DESIGN.md §11.)
             if (lane == 0) {
                 unsigned int* const cnt = p.band_done + prev_band;
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
