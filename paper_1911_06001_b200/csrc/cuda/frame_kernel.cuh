@@ -663,9 +663,18 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                     if (!best.have() && rem != 0 && (rem & (rem - 1)) == 0) {
                         kb = __ffsll(rem) - 1;
                     } else {
+                        // A candidate whose t_boundary is beyond the best hit is skipped
+                        // whenever its turn comes (the best t only decreases), so it
+                        // leaves the set now: the passes stop once nothing left can be
+                        // traced, instead of visiting every skipped candidate in order.
+                        const Real bt = best.have() ? world_t(best.t) : pos_inf<Real>();
                         for (unsigned long long it = rem; it; it &= it - 1) {
                             const int k = __ffsll(it) - 1;
                             const SphereRes<Real> sr = sphere_of(p, list[k], dw);
+                            if (bt < sr.tb) {
+                                rem &= ~(1ull << k);
+                                continue;
+                            }
                             if (kb < 0 || sr.tc < tcb) kb = k, tcb = sr.tc, cand_tb = sr.tb;
                         }
                     }
@@ -675,11 +684,15 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 } else if (mode == kAllSorted) {
                     int k = -1;
                     Real k_tc = Real(0);
+                    const Real bt = best.have() ? world_t(best.t) : pos_inf<Real>();
                     for (uint32_t i = 0; i < n; ++i) {
                         const SphereRes<Real> sr = sphere_of(p, i, dw);
                         if (p.culling && !sr.hit) continue;
                         const bool after = sr.tc > last_tc || (sr.tc == last_tc && static_cast<int>(i) > last_i);
                         if (!after) continue;
+                        // skipped whenever it comes up (sphere hits: t_boundary; the
+                        // no-culling order's misses carry 0 and are never skipped)
+                        if (sr.hit && bt < sr.tb) continue;
                         if (k < 0 || sr.tc < k_tc) k = static_cast<int>(i), k_tc = sr.tc, cand_tb = sr.hit ? sr.tb : Real(0);
                     }
                     if (k >= 0) found = true, cand = static_cast<uint32_t>(k), last_tc = k_tc, last_i = k;
