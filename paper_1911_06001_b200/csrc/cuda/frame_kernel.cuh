@@ -394,6 +394,49 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
     }
 }
 
+// Direct readback of one finished super-tile (called by the whole warp that
+// finished its last tile): its RGB8 rows, written to the device image by the
+// tiles' warps, are copied into the caller's page-locked host image (mapped)
+// with 16-byte stores over PCIe -- 192-byte row segments, 64-byte aligned --
+// while the rest of the frame renders. Loads bypass L1 (other SMs wrote the
+// rows). Out of line, with scalar arguments: the frame kernel's register
+// allocation is not disturbed by this cold path.
+static __device__ __noinline__ void flush_rows(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint32_t row_bytes,
+                                        uint32_t seg_bytes, uint32_t rows, uint32_t lane) {
+    __threadfence(); // every lane reads after lane 0's acquire
+    if ((seg_bytes & 15u) == 0 && (row_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        const uint32_t per_row = seg_bytes >> 4, n = per_row * rows;
+        constexpr uint32_t kBatch = 4; // loads in flight per lane before their stores
+        for (uint32_t base = 0; base < n; base += 32u * kBatch) {
+            uint4 v[kBatch];
+#pragma unroll
+            for (uint32_t j = 0; j < kBatch; ++j) {
+                const uint32_t i = base + lane + 32u * j, r = i / per_row;
+                if (i < n) v[j] = __ldcg(reinterpret_cast<const uint4*>(src + r * row_bytes + 16u * (i - r * per_row)));
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < kBatch; ++j) {
+                const uint32_t i = base + lane + 32u * j, r = i / per_row;
+                if (i < n) *reinterpret_cast<uint4*>(dst + r * row_bytes + 16u * (i - r * per_row)) = v[j];
+            }
+        }
+    } else {
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t b = lane; b < seg_bytes; b += 32u) dst[r * row_bytes + b] = __ldcg(src + r * row_bytes + b);
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ void flush_super_rgb(const FrameParams<Real>& p, uint32_t s, uint32_t lane) {
+    const uint32_t sy = super_row(p, s), sx = s - sy * p.n_super_x;
+    const uint32_t x0 = sx * kSuper, y0 = sy * kSuper;
+    const uint32_t w = min(static_cast<uint32_t>(kSuper), static_cast<uint32_t>(p.width) - x0);
+    const uint32_t h = min(static_cast<uint32_t>(kSuper), static_cast<uint32_t>(p.height) - y0);
+    const size_t o0 = 3 * (static_cast<size_t>(y0) * static_cast<size_t>(p.width) + x0);
+    flush_rows(p.rgb + o0, p.rgb_host + o0, 3u * static_cast<uint32_t>(p.width), 3u * w, h, lane);
+}
+
 // Shade (renderer.cpp:102-113): ambient 0.2 + 0.8 headlight Lambert,
 // round half away from zero.
 template <typename Real>
@@ -416,7 +459,9 @@ __device__ __forceinline__ uint32_t shade_rgba(uint32_t color, const Real n[3], 
 }
 
 // kHbo: 0 no hit buffer, 1 48-byte host-layout records, 2 16-byte records (FP32)
-template <typename Real, bool kAov, int kHbo, bool kCompact>
+// kDirect: direct synchronous readback (p.super_done / p.rgb_host set; no AOV or
+// hit buffer) -- its own instantiation, so the other kernels carry none of it
+template <typename Real, bool kAov, int kHbo, bool kCompact, bool kDirect = false>
 __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : VXA_MIN_BLOCKS_F64) frame_kernel(const __grid_constant__ FrameParams<Real> p) {
     extern __shared__ uint2 smem_stack[]; // FP32 traversal stack: [level][thread]
     __shared__ uint16_t s_list[kWarps][kListCap];
@@ -475,17 +520,32 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
 #endif
     const uint16_t* const list = s_list[warp];
 
-    int prev_band = -1; // band of the warp's previous tile (synchronous readback)
+    // band (banded readback) or super-tile (direct readback) of the warp's previous tile
+    int prev_band = -1;
     while (true) {
         __syncwarp();
         if (prev_band >= 0) {
-            // the previous tile's RGB8 bytes are visible before its band count moves
-            // (the copy engine starts the band's D2H when the count is complete): the
+            // the previous tile's RGB8 bytes are visible before its count moves: the
             // warp barrier orders the lanes' stores before lane 0's gpu-scope release
-            // increment (cumulative) -- one release per tile, not 32 fences. (Adding a
-            // warp's tiles per band once it leaves the band costs fewer releases but
-            // signals the bands late: the D2H overlapped less.)
-            if (lane == 0) {
+            // increment (cumulative) -- one release per tile, not 32 fences.
+            if constexpr (kDirect) {
+                // direct readback: the warp that completes a super-tile (its count's
+                // acquire sees every other tile's release) stores its rows to the host
+                uint32_t last = 0;
+                if (lane == 0) {
+                    uint32_t old;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                                 : "=r"(old)
+                                 : "l"(p.super_done + prev_band)
+                                 : "memory");
+                    last = old == static_cast<uint32_t>(kTilesPerSuper) - 1u ? 1u : 0u;
+                }
+                if (__shfl_sync(0xffffffffu, last, 0)) flush_super_rgb(p, static_cast<uint32_t>(prev_band), lane);
+            } else if (lane == 0) {
+                // banded readback: the copy engine starts a band's D2H when its count is
+                // complete. (Adding a warp's tiles per band once it leaves the band costs
+                // fewer releases but signals the bands late: the D2H overlapped less,
+                // DESIGN.md §11.)
                 unsigned int* const cnt = p.band_done + prev_band;
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
             }
@@ -499,6 +559,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
         const uint32_t sy = super_row(p, s), sx = s - sy * p.n_super_x;
         if (p.band_done != nullptr) prev_band = static_cast<int>(sy / p.band_rows);
+        if constexpr (kDirect) prev_band = static_cast<int>(s);
         const int tx0 = static_cast<int>(sx * kSuper + (wt % (kSuper / kTileW)) * kTileW);
         const int ty0 = static_cast<int>(sy * kSuper + (wt / (kSuper / kTileW)) * kTileH);
         int px = tx0 + static_cast<int>(lane % kTileW);
@@ -958,8 +1019,8 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // (band_rows implies one rank: super-tile st is screen super-tile st)
-    order_by_count(count, gridDim.x, const_cast<uint32_t*>(p.super_order), p.n_super_x, p.band_done ? p.band_rows : 0u);
+    // (band_rows > 0 -- a banded order -- implies one rank: super-tile st is screen super-tile st)
+    order_by_count(count, gridDim.x, const_cast<uint32_t*>(p.super_order), p.n_super_x, p.band_rows);
     if (threadIdx.x == 0) *done = 0; // ready for the next frame
 }
 

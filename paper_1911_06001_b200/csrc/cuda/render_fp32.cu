@@ -11,7 +11,10 @@ template <bool A, bool K> void* pick_h(int hbo) {
     return hbo == 2 ? frame_fn<A, 2, K>() : hbo == 1 ? frame_fn<A, 1, K>() : frame_fn<A, 0, K>();
 }
 // hbo: 0 none, 1 48-byte records, 2 16-byte records
-void* pick(bool aov, int hbo, bool compact) {
+void* pick(bool aov, int hbo, bool compact, bool direct = false) {
+    if (direct) // direct synchronous readback (vxa_render: no AOV, no hit buffer)
+        return compact ? reinterpret_cast<void*>(&frame_kernel<float, false, 0, true, true>)
+                       : reinterpret_cast<void*>(&frame_kernel<float, false, 0, false, true>);
     if (aov) return compact ? pick_h<true, true>(hbo) : pick_h<true, false>(hbo);
     return compact ? pick_h<false, true>(hbo) : pick_h<false, false>(hbo);
 }
@@ -32,10 +35,10 @@ cudaError_t launch_frame_f32(const FrameParams<float>& p, bool aov, bool hbo, co
         attr.val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelExC(&cfg, pick(aov, hbo_mode(p, hbo), p.compact != 0), args);
+        return cudaLaunchKernelExC(&cfg, pick(aov, hbo_mode(p, hbo), p.compact != 0, p.super_done != nullptr), args);
     }
 #endif
-    return cudaLaunchKernel(pick(aov, hbo_mode(p, hbo), p.compact != 0), dim3(l.grid), dim3(kBlock), args,
+    return cudaLaunchKernel(pick(aov, hbo_mode(p, hbo), p.compact != 0, p.super_done != nullptr), dim3(l.grid), dim3(kBlock), args,
                             frame_smem_bytes_f32(p.max_depth), l.stream);
 }
 

@@ -8,7 +8,8 @@ namespace vxa {
 
 namespace {
 template <bool A, bool H> void* frame_fn() { return reinterpret_cast<void*>(&frame_kernel<double, A, H ? 1 : 0, false>); }
-void* pick(bool aov, bool hbo, bool /*compact: FP64 keeps the general words*/) {
+void* pick(bool aov, bool hbo, bool /*compact: FP64 keeps the general words*/, bool direct = false) {
+    if (direct) return reinterpret_cast<void*>(&frame_kernel<double, false, 0, false, true>); // direct readback
     if (aov) return hbo ? frame_fn<true, true>() : frame_fn<true, false>();
     return hbo ? frame_fn<false, true>() : frame_fn<false, false>();
 }
@@ -24,7 +25,7 @@ cudaError_t launch_super_cull(const FrameParams<double>& p, uint16_t* list, uint
 
 cudaError_t launch_frame_f64(const FrameParams<double>& p, bool aov, bool hbo, const FrameLaunch& l) {
     void* args[] = {const_cast<FrameParams<double>*>(&p)};
-    return cudaLaunchKernel(pick(aov, hbo, p.compact != 0), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f64(p.max_depth), l.stream);
+    return cudaLaunchKernel(pick(aov, hbo, p.compact != 0, p.super_done != nullptr), dim3(l.grid), dim3(kBlock), args, frame_smem_bytes_f64(p.max_depth), l.stream);
 }
 
 size_t frame_smem_bytes_f64(uint32_t max_depth) {

@@ -325,6 +325,12 @@ struct vxa_ctx {
     cudaEvent_t band_trace[16] = {}; // VOXANIM_BAND_TRACE: per-band copy completion events
     cudaStream_t copy_stream2 = nullptr; // second D2H stream of the banded readback (bands alternate)
     int band_api = 0; // 0 unknown, 1 cuStreamWaitValue32 usable, -1 not
+    // direct synchronous readback (vxa_render into page-locked host memory): per
+    // super-tile tile counters and the device alias of the caller's image
+    DevBuf<uint32_t> direct_done;
+    uint32_t* next_super_done = nullptr;
+    uint8_t* next_rgb_host = nullptr;
+    bool next_screen_order = false; // the frame being submitted keeps the screen order of its super-tiles
     void* wait_value32 = nullptr;
     cudaEvent_t next_rgb_free = nullptr;  // its slot's previous D2H
     int rb_pending_slot = 0;
@@ -584,6 +590,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     p.rgb = ctx->next_rgb; // set by vxa_submit_readback for this frame only
     p.band_done = p.rgb != nullptr ? ctx->next_band_done : nullptr;
     p.band_rows = ctx->next_band_rows;
+    p.super_done = p.rgb != nullptr ? ctx->next_super_done : nullptr;
+    p.rgb_host = p.super_done != nullptr ? ctx->next_rgb_host : nullptr;
     if (p.rgb != nullptr && ctx->next_rgb_free != nullptr) VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->next_rgb_free, 0));
     p.max_depth = 1;
     p.compact = sizeof(Real) == 4 ? 1u : 0u;
@@ -703,7 +711,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
         // screen order, longest-first inside each); VOXANIM_LPT=0 forces screen order
         // (experiments)
         const char* lpt_env = std::getenv("VOXANIM_LPT");
-        if (VXA_LPT && !(lpt_env && std::strcmp(lpt_env, "0") == 0)) {
+        if (VXA_LPT && !ctx->next_screen_order && !(lpt_env && std::strcmp(lpt_env, "0") == 0)) {
             VXA_CUDA(ctx->super_order.ensure(std::max<size_t>(mine_super, 1)));
             p.super_order = ctx->super_order.ptr;
         }
@@ -887,6 +895,7 @@ int vxa_destroy(vxa_ctx* ctx) {
     ctx->rgb.release();
     ctx->l2_scratch.release();
     ctx->band_done.release();
+    ctx->direct_done.release();
     if (ctx->band_reset) cudaEventDestroy(ctx->band_reset);
     for (cudaEvent_t e : ctx->band_trace)
         if (e) cudaEventDestroy(e);
@@ -1320,8 +1329,24 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
     // of the frame; the last band's copy is all that follows the kernel.
     const uint32_t n_sx = super_tiles_x(f->camera.width);
     const uint32_t n_sy = static_cast<uint32_t>((f->camera.height + kSuper - 1) / kSuper);
+    // Direct mode: when the caller's image is page-locked and mapped (vxa_host_register,
+    // cudaHostAlloc), the warp finishing a super-tile stores its rows straight into it
+    // over PCIe (frame_kernel.cuh: flush_super_rgb), so the transfer runs alongside
+    // the frame from its first finished super-tile on and only the last one's rows
+    // follow the kernel. VOXANIM_DIRECT_READBACK=0 turns it off.
+    uint8_t* direct_host = nullptr;
+    if (fused && npix >= (size_t{1} << 20) && aov_out == nullptr && hbo == nullptr && dev_hbo == nullptr) {
+        const char* env = std::getenv("VOXANIM_DIRECT_READBACK");
+        if (!(env && std::strcmp(env, "0") == 0)) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, rgb_out) == cudaSuccess && a.type == cudaMemoryTypeHost &&
+                a.devicePointer != nullptr)
+                direct_host = static_cast<uint8_t*>(a.devicePointer);
+            cudaGetLastError();
+        }
+    }
     uint32_t band_rows = 0, n_bands = 0;
-    if (fused && npix >= (size_t{1} << 20) && band_api_ok(ctx)) {
+    if (fused && direct_host == nullptr && npix >= (size_t{1} << 20) && band_api_ok(ctx)) {
         // about VOXANIM_READBACK_BANDS bands (default 16, at most 16: the frame kernel's band counters)
         uint32_t want = 16;
         if (const char* env = std::getenv("VOXANIM_READBACK_BANDS"); env && std::atoi(env) > 0)
@@ -1346,10 +1371,29 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
         ctx->next_band_done = ctx->band_done.ptr;
         ctx->next_band_rows = band_rows;
     }
+    if (direct_host) {
+        const size_t n_super = static_cast<size_t>(n_sx) * n_sy;
+        VXA_CUDA(ctx->direct_done.ensure(n_super));
+        VXA_CUDA(cudaMemsetAsync(ctx->direct_done.ptr, 0, n_super * sizeof(uint32_t), ctx->stream));
+        ctx->next_super_done = ctx->direct_done.ptr;
+        ctx->next_rgb_host = direct_host;
+        // super-tile order (VOXANIM_DIRECT_ORDER): screen order (default: the finished
+        // super-tiles and their PCIe stores spread over the frame), longest-first ("lpt":
+        // the cheap super-tiles finish in a burst at the end and their stores queue
+        // behind the kernel), or banded ("banded": 16 bands in screen order,
+        // longest-first inside each)
+        const char* ord = std::getenv("VOXANIM_DIRECT_ORDER");
+        const std::string order = ord ? ord : "screen";
+        ctx->next_screen_order = order == "screen";
+        if (order == "banded") ctx->next_band_rows = (n_sy + 15) / 16;
+    }
     const int erc = enqueue_any(ctx, f, in, n, aov, hbo, dev_hbo, true);
     ctx->next_rgb = nullptr;
     ctx->next_band_done = nullptr;
     ctx->next_band_rows = 0;
+    ctx->next_super_done = nullptr;
+    ctx->next_rgb_host = nullptr;
+    ctx->next_screen_order = false;
     if (erc != VXA_OK) return erc;
     VXA_CUDA(cudaEventRecord(ctx->ev_b, ctx->stream));
     uint64_t launches = 1 + static_cast<uint64_t>(ctx->aux_launches);
@@ -1398,6 +1442,8 @@ int vxa_render(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, ui
             }
             std::fprintf(stderr, "\n");
         }
+    } else if (rgb_out && fused && direct_host) {
+        ctx->d2h += npix * 3; // stored by the frame kernel; visible once the stream is synchronised
     } else if (rgb_out && fused) {
         VXA_CUDA(cudaMemcpyAsync(rgb_out, ctx->rgb.ptr, npix * 3, cudaMemcpyDeviceToHost, ctx->stream));
         ctx->d2h += npix * 3;

@@ -252,6 +252,12 @@ template <typename Real> struct FrameParams {
     // the frame kernel works on the next ones (null: off)
     uint32_t* band_done;
     uint32_t band_rows;
+    // Synchronous readback into page-locked host memory (vxa_render, direct mode):
+    // warp tiles finished per super-tile; the warp finishing a super-tile's last
+    // tile stores its RGB8 rows into rgb_host (the caller's image, mapped) over
+    // PCIe while the frame goes on (null: off)
+    uint32_t* super_done;
+    uint8_t* rgb_host;
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
     void* aov;                    // vxa_pixel_aov* or null
     void* hbo;                    // vxa_hit_record* (device copy) or HitRec16* (hbo_compact), or null

@@ -1,6 +1,8 @@
 """Synchronous render_frame at C4 (the drop-in call, RGB8 into page-locked host
-memory): wall time per call for several readback band counts (0 = one copy
-after the kernel), next to the frame kernels' event time."""
+memory): wall time per call for the direct readback (the frame kernel stores
+each finished super-tile's rows into the mapped host image) and for several
+readback band counts (0 = one copy after the kernel), next to the frame
+kernels' event time."""
 import ctypes as C
 import os
 import sys
@@ -18,10 +20,15 @@ sc = vx.Scene(vx.config.C4, [vx.Model.procedural(11, shell=True)])
 W, H = sc.width, sc.height
 buf = np.empty((H, W, 3), np.uint8)
 lib.vxa_host_register(ctx, buf.ctypes.data, buf.nbytes)
-CASES = [("0", "1"), ("8", "1"), ("16", "1"), ("8", "0"), ("16", "0")]  # (bands, two copy streams)
-for bands, lpt in CASES:
-    os.environ["VOXANIM_READBACK_STREAMS"] = "2" if lpt == "1" else "1"
-    if bands == "0":
+# (readback, option): direct with its super-tile order, or bands with one / two copy streams
+CASES = [("direct", "screen"), ("direct", "banded"), ("direct", "lpt"), ("0", "2"), ("16", "2"), ("16", "1")]
+for bands, opt in CASES:
+    os.environ["VOXANIM_DIRECT_READBACK"] = "1" if bands == "direct" else "0"
+    if bands == "direct":
+        os.environ["VOXANIM_DIRECT_ORDER"] = opt
+    else:
+        os.environ["VOXANIM_READBACK_STREAMS"] = opt
+    if bands in ("0", "direct"):
         os.environ["VOXANIM_BANDED_READBACK"] = "0"
     else:
         os.environ.pop("VOXANIM_BANDED_READBACK", None)
@@ -38,5 +45,5 @@ for bands, lpt in CASES:
         host.append(time.perf_counter() - a)
         gpu.append(st["gpu_ms"])
     el = (time.perf_counter() - t0) / steps
-    print(f"bands {bands:>2} streams {2 if lpt == '1' else 1}: {el * 1e3:.3f} ms/step ({W * H / el / 1e6:.0f} Mrays/s), render call median "
+    print(f"readback {bands:>6} {opt:>6}: {el * 1e3:.3f} ms/step ({W * H / el / 1e6:.0f} Mrays/s), render call median "
           f"{np.median(host) * 1e3:.3f} ms, kernels (events) median {np.median(gpu):.3f} ms", flush=True)

@@ -233,6 +233,40 @@ def test_banded_synchronous_readback(gpu, cfg, precision, monkeypatch):
         assert (banded != 0).any()
 
 
+@pytest.mark.parametrize("cfg,precision,size", [(vx.config.C4, vx.VXA_FP32, None), (vx.config.C2, vx.VXA_FP32, None),
+                                                (vx.config.C2, vx.VXA_FP64, None),
+                                                (vx.config.C4, vx.VXA_FP32, (1008, 1040))])
+def test_direct_synchronous_readback(gpu, cfg, precision, size, monkeypatch):
+    """A synchronous render into a page-locked (registered) host image: the warp
+    finishing each super-tile stores its RGB8 rows into the image over PCIe during
+    the frame. The image equals the one copied after the kernel
+    (VOXANIM_DIRECT_READBACK=0 and VOXANIM_BANDED_READBACK=0), frame after frame;
+    1008x1040 has partial super-tiles on the right and bottom edges."""
+    lib, ctx = vx.vxa(), vx.context()
+    depth = 11 if cfg == vx.config.C4 else 10
+    m = vx.Model.procedural(depth, shell=True)
+    args = (0,) + size if size else ()
+    a, b = vx.Scene(cfg, [m], *args), vx.Scene(cfg, [m], *args)
+    img = np.zeros((a.height, a.width, 3), np.uint8)
+    assert lib.vxa_host_register(ctx, img.ctypes.data, img.nbytes) == 0
+    try:
+        for t in (0.2, 1.9, 3.4):
+            a.evaluate(t)
+            b.evaluate(t)
+            img[...] = 7
+            monkeypatch.delenv("VOXANIM_DIRECT_READBACK", raising=False)
+            a.render(precision=precision, rgb=img)
+            monkeypatch.setenv("VOXANIM_DIRECT_READBACK", "0")
+            monkeypatch.setenv("VOXANIM_BANDED_READBACK", "0")
+            plain = b.render(precision=precision)[0]
+            monkeypatch.delenv("VOXANIM_DIRECT_READBACK")
+            monkeypatch.delenv("VOXANIM_BANDED_READBACK")
+            assert (img == plain).all(), t
+            assert (img != 0).any()
+    finally:
+        lib.vxa_host_unregister(ctx, img.ctypes.data)
+
+
 def test_streaming_readback_matches_synchronous_frames(gpu):
     """vxa_submit_readback (frame k's D2H overlapping frame k+1) delivers the same
     images as synchronous render_frame calls."""
