@@ -966,7 +966,10 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         const float t_exit = fminf(fminf(c1[0], c1[1]), c1[2]);
         {
             const uint32_t xb = c1[0] == t_exit ? 4u : (c1[1] == t_exit ? 2u : 1u);
-            fcur = (q | xb) + ((q & xb) << 3); // >= kExit iff the exit axis bit is already set
+            // (q | xb) + 8 (q & xb), >= kExit iff the exit axis bit is already set; as
+            // q + xb + 7 (q & xb) the multiply-add runs on the FMA pipe (the ALU pipe is
+            // the loop's busiest: -0.5 %)
+            fcur = q + xb + 7u * (q & xb);
         }
         const float t_enter = ten;
         ten = fmaxf(ten, t_exit);
