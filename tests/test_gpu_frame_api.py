@@ -235,13 +235,15 @@ def test_banded_synchronous_readback(gpu, cfg, precision, monkeypatch):
 
 @pytest.mark.parametrize("cfg,precision,size", [(vx.config.C4, vx.VXA_FP32, None), (vx.config.C2, vx.VXA_FP32, None),
                                                 (vx.config.C2, vx.VXA_FP64, None),
-                                                (vx.config.C4, vx.VXA_FP32, (1008, 1040))])
+                                                (vx.config.C4, vx.VXA_FP32, (1008, 1040)),
+                                                (vx.config.C4, vx.VXA_FP32, (1000, 1050))])
 def test_direct_synchronous_readback(gpu, cfg, precision, size, monkeypatch):
     """A synchronous render into a page-locked (registered) host image: the warp
     finishing each super-tile stores its RGB8 rows into the image over PCIe during
     the frame. The image equals the one copied after the kernel
     (VOXANIM_DIRECT_READBACK=0 and VOXANIM_BANDED_READBACK=0), frame after frame;
-    1008x1040 has partial super-tiles on the right and bottom edges."""
+    1008x1040 has partial super-tiles on the right and bottom edges, 1000x1050 rows
+    that are not 16-byte multiples (the byte-wise copy)."""
     lib, ctx = vx.vxa(), vx.context()
     depth = 11 if cfg == vx.config.C4 else 10
     m = vx.Model.procedural(depth, shell=True)
