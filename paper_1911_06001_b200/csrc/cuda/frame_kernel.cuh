@@ -304,7 +304,8 @@ __device__ __forceinline__ void trace_candidate(const FrameParams<Real>& p, uint
         setup_root(lr, in.A_lo, in.A_hi, in.zflags, in.zbits);
         TravHit<Real> h;
         NoLog nolog;
-        const bool hit = traverse_model(in.model, lr, h, nolog);
+        const bool hit = (VXA_F64_SPLIT && lr.zero == 0) ? traverse_model<Real, NoLog, false>(in.model, lr, h, nolog)
+                                                         : traverse_model(in.model, lr, h, nolog);
         fetches += h.fetches;
         if (!hit) return;
         for (int k = 0; k < 3; ++k) ld[k] = lr.d[k];

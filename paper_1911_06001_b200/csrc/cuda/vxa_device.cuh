@@ -133,6 +133,11 @@ struct WideNodes {
 #ifndef VXA_FC_SIGN
 #define VXA_FC_SIGN 1
 #endif
+// FP64 parity kernel: rays without a zero local direction component take a
+// traverse_model instantiation without the zero-direction midplane convention
+#ifndef VXA_F64_SPLIT
+#define VXA_F64_SPLIT 1
+#endif
 
 // Octant of the first child (first_node, traversal.cpp:63-86): bit a iff the
 // midplane is crossed before the entry, tm[a] < te. The sign of the rounded
@@ -415,8 +420,12 @@ struct NoLog {
 };
 
 // Returns true on a hit. The stack holds the ancestors of the current frame;
-// the current frame lives in registers.
-template <typename Real, class Log>
+// the current frame lives in registers, with its midplane parameters computed
+// once when it becomes the frame (push or pop) instead of at every child step
+// -- the same 0.5 (t0 + t1) of the same operands, so the same values. kZero =
+// false: the caller guarantees no zero direction component (r.zero == 0), so
+// the zero-direction midplane convention compiles out (VXA_F64_SPLIT).
+template <typename Real, class Log, bool kZero = true>
 __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravHit<Real>& out, Log& log) {
     Real te = r.t0[0];
     if (r.t0[1] > te) te = r.t0[1];
@@ -433,18 +442,19 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
     uint2 sw[kMaxDepth];
     uint32_t sidx[kMaxDepth], scur[kMaxDepth];
 
+    const auto mid = [&](int a, Real t0, Real t1, int lv) {
+        if constexpr (kZero) return midplane(r, a, t0, t1, lv);
+        else return Real(0.5) * (t0 + t1);
+    };
     Real f0[3] = {r.t0[0], r.t0[1], r.t0[2]};
     Real f1[3] = {r.t1[0], r.t1[1], r.t1[2]};
+    Real fm[3]; // the frame's midplane parameters (traversal.cpp:139,167)
     uint32_t fidx = 0;
     uint2 fw = load_node(m, 0);
     uint32_t fetches = 1;
-    uint32_t fcur;
-    {
-        Real tm[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) tm[a] = midplane(r, a, f0[a], f1[a], 0);
-        fcur = first_child(f0, tm);
-    }
+    for (int a = 0; a < 3; ++a) fm[a] = mid(a, f0[a], f1[a], 0);
+    uint32_t fcur = first_child(f0, fm);
     int level = 0;
     unsigned long long path = 0;
     const int depth = static_cast<int>(m.depth);
@@ -464,6 +474,7 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
             for (int a = 0; a < 3; ++a) {
                 f0[a] = st0[level][a];
                 f1[a] = st1[level][a];
+                fm[a] = mid(a, f0[a], f1[a], level);
             }
             fw = sw[level];
             fidx = sidx[level];
@@ -473,26 +484,20 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
         Real c0[3], c1[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const Real tm = midplane(r, a, f0[a], f1[a], level);
             if (q & axis_bit(a)) {
-                c0[a] = tm;
+                c0[a] = fm[a];
                 c1[a] = f1[a];
             } else {
                 c0[a] = f0[a];
-                c1[a] = tm;
+                c1[a] = fm[a];
             }
         }
         fcur = next_child(c1, q);
-        int entry = 0;
+        // entry parameter = max c0 (the entry axis, argmax with ties to the lower
+        // axis, only matters on a hit: taken there)
         Real t_enter = c0[0];
-        if (c0[1] > t_enter) {
-            entry = 1;
-            t_enter = c0[1];
-        }
-        if (c0[2] > t_enter) {
-            entry = 2;
-            t_enter = c0[2];
-        }
+        if (c0[1] > t_enter) t_enter = c0[1];
+        if (c0[2] > t_enter) t_enter = c0[2];
         Real t_exit = c1[0];
         if (c1[1] < t_exit) t_exit = c1[1];
         if (c1[2] < t_exit) t_exit = c1[2];
@@ -507,6 +512,13 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
         log.visit(static_cast<double>(t_enter), static_cast<uint32_t>(level + 1), is_leaf);
         path = (path & ~(0xfull << (4 * level))) | (static_cast<unsigned long long>(oct) << (4 * level));
         if (is_leaf) {
+            int entry = 0; // traversal.cpp:214-222
+            Real te = c0[0];
+            if (c0[1] > te) {
+                entry = 1;
+                te = c0[1];
+            }
+            if (c0[2] > te) entry = 2;
             const uint32_t abase = (fw.x & kMixed) ? __ldg(m.side + fw.y) : fw.y;
             out.attr = abase + popc8_below(valid & leafm, bit);
             out.t = t_enter < Real(0) ? Real(0) : t_enter;
@@ -531,19 +543,17 @@ __device__ bool traverse_model(const DevModel& m, const LocalRay<Real>& r, TravH
             sidx[level] = fidx;
             scur[level] = fcur;
         }
+        ++level;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             f0[a] = c0[a];
             f1[a] = c1[a];
+            fm[a] = mid(a, f0[a], f1[a], level);
         }
-        ++level;
         fidx = child;
         fw = load_node(m, child);
         ++fetches;
-        Real tm[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) tm[a] = midplane(r, a, f0[a], f1[a], level);
-        fcur = first_child(f0, tm);
+        fcur = first_child(f0, fm);
     }
     out.fetches = fetches;
     return false;
