@@ -644,9 +644,18 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
         // ---- sphere pass: count hits, remember the single hit (HBO rule)
         uint32_t n_hits = 0, only = 0;
         unsigned long long hitmask = 0; // list mode: bit k = s_list[warp][k] hit
+        // list mode: 1 + the (t_center, index) minimum of the hits -- the first candidate
+        // of the sorted order, so its pick needs no second pass over the hits
+        uint32_t first_pick = 0;
         if (list_n != 0xffffffffu) {
-            for (uint32_t k = 0; k < list_n; ++k)
-                if (sphere_of(p, list[k], dw).hit) hitmask |= 1ull << k;
+            Real first_tc = Real(0);
+            for (uint32_t k = 0; k < list_n; ++k) {
+                const SphereRes<Real> sr = sphere_of(p, list[k], dw);
+                if (sr.hit) {
+                    hitmask |= 1ull << k;
+                    if (first_pick == 0 || sr.tc < first_tc) first_pick = k + 1, first_tc = sr.tc;
+                }
+            }
             n_hits = __popcll(hitmask);
             if (n_hits) only = list[__ffsll(hitmask) - 1];
         } else if (p.sphere_pass) {
@@ -708,7 +717,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             unsigned long long rem = hitmask; // list modes: hit bits not yet visited
             Real last_tc = -pos_inf<Real>();  // kAllSorted: last (t_center, index) taken
             int last_i = -1;
-            uint32_t next_i = 0;              // kAllIdOrder cursor
+            uint32_t next_i = mode == kListSorted ? first_pick : 0u; // kAllIdOrder cursor; kListSorted: the pending first pick
             bool one_left = true;
             while (true) {
                 uint32_t cand = 0;
@@ -717,13 +726,14 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 if (mode == kOne) {
                     found = one_left, cand = only, one_left = false;
                 } else if (mode == kListSorted) {
-                    // (t_center, index) minimum over the remaining hit bits. A lone
-                    // first candidate needs no sphere values: nothing to order, and
-                    // its t_boundary only matters once there is a best hit.
+                    // (t_center, index) minimum over the remaining hit bits. The first
+                    // one is the sphere pass's (its t_boundary only matters once there
+                    // is a best hit: none yet).
                     int kb = -1;
                     Real tcb = Real(0);
-                    if (!best.have() && rem != 0 && (rem & (rem - 1)) == 0) {
-                        kb = __ffsll(rem) - 1;
+                    if (next_i != 0) {
+                        kb = static_cast<int>(next_i) - 1;
+                        next_i = 0;
                     } else {
                         // A candidate whose t_boundary is beyond the best hit is skipped
                         // whenever its turn comes (the best t only decreases), so it
