@@ -101,8 +101,14 @@ template <> struct Best<float> {
     __device__ __forceinline__ bool pos_dir() const { return ((key >> 26) & 1u) != 0; }
     __device__ __forceinline__ int32_t id(const FrameParams<float>& p) const { return p.inst[inst()].id; }
     __device__ __forceinline__ void set(uint32_t inst, int32_t, uint32_t axis, bool pos_dir) {
-        key = 0x80000000u | (pos_dir ? 1u << 26 : 0u) | (axis << 24) | inst;
+        key = (key & kFlagMask) | 0x80000000u | (pos_dir ? 1u << 26 : 0u) | (axis << 24) | inst;
     }
+    // Compact hit-buffer kernels: per-pixel facts the store needs, kept in spare key
+    // bits across the traversal instead of in registers of their own (set() keeps them)
+    static constexpr uint32_t kMultiCand = 1u << 27; // more than one candidate: a hit is kMulti
+    static constexpr uint32_t kNoSphere = 1u << 28;  // no sphere hit: a trivially reusable miss
+    static constexpr uint32_t kReuse = 1u << 29;     // the record is reused (instance field: the object)
+    static constexpr uint32_t kFlagMask = kMultiCand | kNoSphere | kReuse;
 };
 
 // World normal of the nearest hit: R n_local with n_local = sign e_axis
@@ -699,6 +705,11 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 }
             }
         }
+        if constexpr (compact_hbo && !kAov) {
+            // what the store needs from the sphere pass, in spare bits of the best key
+            if (reused) best.key = Best<Real>::kReuse | only; // n_hits == 1: the object
+            if (n_hits == 0) best.key |= Best<Real>::kNoSphere;
+        }
 
         if (!reused) {
             // One traversal call site; the candidate order comes from a small
@@ -714,6 +725,8 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             } else {
                 mode = kAllIdOrder, n_cand = p.culling ? n_hits : n;
             }
+            if constexpr (compact_hbo && !kAov)
+                if (n_cand > 1) best.key |= Best<Real>::kMultiCand;
             unsigned long long rem = hitmask; // list modes: hit bits not yet visited
             Real last_tc = -pos_inf<Real>();  // kAllSorted: last (t_center, index) taken
             int last_i = -1;
@@ -779,14 +792,26 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 pixel_xy(px, py);
                 trace_candidate<Real, kAov, kCompact>(p, cand, dw, px, py, best, traversals, fetches, stack);
             }
-            if (best.have()) kind = n_cand > 1 ? kMulti : kSingle;
-            if constexpr (kHbo) {
-                if (!p.camera_dirty && p.culling && n_hits == 0) reused = true; // trivial reuse of a miss
+            if constexpr (!(compact_hbo && !kAov)) {
+                if (best.have()) kind = n_cand > 1 ? kMulti : kSingle;
+                if constexpr (kHbo) {
+                    if (!p.camera_dirty && p.culling && n_hits == 0) reused = true; // trivial reuse of a miss
+                }
             }
         }
         if constexpr (kAov) {
             n_trav += px_trav;
             n_fetch += px_fetch;
+        }
+        // compact hit buffer (production): the reuse facts come back from the key
+        bool reuse_rec; // the record is reused as it is (reused with one sphere hit)
+        if constexpr (compact_hbo && !kAov) {
+            const uint32_t f = best.key;
+            reuse_rec = (f & Best<Real>::kReuse) != 0;
+            kind = (f >> 31) ? ((f & Best<Real>::kMultiCand) ? kMulti : kSingle) : kMiss;
+            reused = reuse_rec || (!p.camera_dirty && p.culling && (f & Best<Real>::kNoSphere) != 0);
+        } else {
+            reuse_rec = reused && n_hits == 1;
         }
         if (reused) ++n_reuse;
 
@@ -796,7 +821,7 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
             // 16-byte records: a reused record's normal is the object's current R
             // times its stored local normal (the object is not dirty)
             HitRec16 rec;
-            if (reused && n_hits == 1) {
+            if (reuse_rec) {
                 rec = reinterpret_cast<const HitRec16*>(p.hbo)[pixel_index()];
             } else {
                 rec.color = best.have() ? __ldg(p.inst[best.inst()].model.attrs + best.attr) : 0xff000000u;
@@ -808,12 +833,15 @@ __global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? VXA_MIN_BLOCKS : V
                 rgba = p.background;
             } else {
                 Best<Real> b = best;
-                if (reused && n_hits == 1) b.set(only, rec.object_id, (rec.meta >> 2) & 3u, (rec.meta & 16u) != 0);
+                if (reuse_rec) {
+                    const uint32_t obj = (compact_hbo && !kAov) ? best.inst() : only;
+                    b.set(obj, rec.object_id, (rec.meta >> 2) & 3u, (rec.meta & 16u) != 0);
+                }
                 Real nrm[3];
                 best_normal(p, b, nrm);
                 rgba = shade_rgba(rec.color, nrm, dw);
             }
-            if (!(reused && n_hits == 1)) reinterpret_cast<HitRec16*>(p.hbo)[pixel_index()] = rec; // a reused record is unchanged
+            if (!reuse_rec) reinterpret_cast<HitRec16*>(p.hbo)[pixel_index()] = rec; // a reused record is unchanged
         } else if constexpr (kHbo == 1) {
             HitRec rec;
             if (reused && n_hits == 1) {
