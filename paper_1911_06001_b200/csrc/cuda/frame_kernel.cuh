@@ -1008,6 +1008,13 @@ __global__ void __launch_bounds__(128) super_cull_kernel(const __grid_constant__
 #if VXA_PDL
     asm volatile("griddepcontrol.launch_dependents;");
 #endif
+    if (blockIdx.x == 0 && threadIdx.x < 8) {
+        // the frame kernel's work counter and (when asked) the frame's statistics start
+        // at zero: the previous frame kernel is done (stream order), this frame's has
+        // not started
+        if (threadIdx.x == 0) *p.tile_counter = 0;
+        if (p.reset_stats) p.counters[threadIdx.x] = 0;
+    }
     const uint32_t st = blockIdx.x;
     const uint32_t s = st * static_cast<uint32_t>(p.world) + static_cast<uint32_t>(p.rank);
     const uint32_t sy = super_row(p, s);

@@ -645,8 +645,15 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     ctx->h2d += bytes;
     VXA_CUDA(cudaEventRecord(ctx->inst_done[slot], ctx->upload_stream));
     VXA_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->inst_done[slot], 0));
-    VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, sizeof(uint32_t), ctx->stream));
-    if (reset_counters) VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
+    // the culling pre-pass (larger scenes) zeroes the work counter and the frame's
+    // statistics itself (its first thread): two memset nodes fewer per frame
+    const bool prepass = p.culling && n > kSuperCullMin && n <= 0xffffu && p.n_tiles / kTilesPerSuper > 0;
+    p.reset_stats = prepass && reset_counters ? 1u : 0u;
+    if (!prepass) {
+        VXA_CUDA(cudaMemsetAsync(ctx->tile_counter.ptr, 0, sizeof(uint32_t), ctx->stream));
+        if (reset_counters)
+            VXA_CUDA(cudaMemsetAsync(ctx->counters.ptr, 0, 8 * sizeof(unsigned long long), ctx->stream));
+    }
 
     const bool is64 = sizeof(Real) == 8;
     const bool a = aov != nullptr, h = hbo != nullptr || dev_hbo != nullptr;
@@ -696,7 +703,7 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
     VXA_CUDA(cudaEventRecord(ctx->k_begin[slot_k], ctx->stream));
     cudaError_t e = cudaSuccess;
     // larger scenes: per-super-tile candidate lists first (same stream; both kernels)
-    if (p.culling && n > kSuperCullMin && n <= 0xffffu) {
+    if (prepass) {
         const size_t mine_super = p.n_tiles / kTilesPerSuper;
         VXA_CUDA(ctx->super_list.ensure(std::max<size_t>(mine_super * kSuperCap, 1)));
         VXA_CUDA(ctx->super_count.ensure(std::max<size_t>(mine_super, 1)));

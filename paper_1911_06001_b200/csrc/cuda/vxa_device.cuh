@@ -264,6 +264,7 @@ template <typename Real> struct FrameParams {
     uint32_t* super_done;
     uint8_t* rgb_host;
     unsigned long long* counters; // rays, sphere_tests, traversals, reused, fetches, leaf_hits
+    uint32_t reset_stats;         // the culling pre-pass zeroes counters (and always tile_counter)
     void* aov;                    // vxa_pixel_aov* or null
     void* hbo;                    // vxa_hit_record* (device copy) or HitRec16* (hbo_compact), or null
     uint32_t hbo_compact;         // FP32 device hit buffer in the 16-byte format
