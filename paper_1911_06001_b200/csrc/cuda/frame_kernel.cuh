@@ -19,7 +19,10 @@ namespace vxa {
 
 enum : uint32_t { kMiss = 0, kSingle = 1, kMulti = 2 };
 
-constexpr int kBlock = 128;
+#ifndef VXA_BLOCK
+#define VXA_BLOCK 128
+#endif
+constexpr int kBlock = VXA_BLOCK;
 // Minimum resident blocks per SM requested from ptxas for the FP32 kernel
 // (register budget 65536 / (128 * n)); tuned by measurement.
 #ifndef VXA_MIN_BLOCKS_F64
