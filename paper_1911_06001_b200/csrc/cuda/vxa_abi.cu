@@ -750,6 +750,8 @@ int enqueue_frame(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in,
 
 int enqueue_any(vxa_ctx* ctx, const vxa_frame_desc* f, const vxa_instance* in, uint32_t n, PixelAov* aov, HitRec* hbo,
                 vxa_ctx::DeviceHbo* dev_hbo, bool reset) {
+    // the FP32 kernel keeps the nearest hit's instance in 24 bits (frame_kernel.cuh: Best<float>)
+    if (n >= (1u << 24)) return fail(VXA_ERR_INVALID, "too many instances in one frame (at most 16,777,215)");
     if (f->precision == VXA_FP64) return enqueue_frame<double>(ctx, f, in, n, aov, hbo, dev_hbo, reset);
     return enqueue_frame<float>(ctx, f, in, n, aov, hbo, dev_hbo, reset);
 }
