@@ -205,6 +205,41 @@ def crowd_bench(lib, ctx, vxl, prec, count: int = 4096, frames: int = 60) -> dic
             "node_fetches_per_ray": round(st.node_fetches / (frames * 3840 * 2160), 4), "frames": frames}
 
 
+def partition_shares(lib, ctx, vxl, scene, animated, args, W, H, frames: int = 8) -> dict:
+    """C4 rendered as rank r of N (64x64 super-tiles dealt round-robin, the
+    multi-GPU partition) on this one GPU: the device time (CUDA events, L2 flushed)
+    of every rank's share, per N. max over ranks bounds an N-GPU frame's compute;
+    t1 / (N * max) is the strong-scaling efficiency that partition allows before
+    the composition and the frame flags."""
+    from paper_1911_06001_b200 import _abi
+
+    def share_ms(rank, world):
+        for k in range(2):
+            vxl.vxn_scene_submit(scene._h, frame_time(k, animated), _abi.VXA_FP32, rank, world, 0)
+        lib.vxa_synchronize(ctx)
+        tot = 0.0
+        for k in range(frames):
+            lib.vxa_flush_l2(ctx)
+            lib.vxa_stream_delay(ctx, args.headstart_us)
+            lib.vxa_timer_begin(ctx)
+            if vxl.vxn_scene_submit(scene._h, frame_time(args.warmup + k, animated), _abi.VXA_FP32, rank, world, 0) != 0:
+                raise RuntimeError(vxl.vxn_last_error().decode())
+            ms = C.c_double()
+            lib.vxa_timer_end(ctx, C.byref(ms))
+            tot += ms.value
+        return tot / frames
+
+    t1 = share_ms(0, 1)
+    out = {"frames_per_share": frames, "n1_ms": round(t1, 4)}
+    for n in (2, 4, 8):
+        per = [share_ms(r, n) for r in range(n)]
+        out[f"n{n}"] = {"rank_ms": [round(x, 4) for x in per], "max_ms": round(max(per), 4),
+                        "compute_efficiency": round(t1 / (n * max(per)), 3)}
+    out["note"] = ("one GPU renders each rank's super-tiles in turn (vxn_scene_submit rank/world); the N-GPU "
+                   "frame adds the NVLink composition and the device-side frame flags")
+    return out
+
+
 def model_build_bench(lib, ctx, reps: int = 5) -> dict:
     """build_from_grid on the device (vxa_build_model)
     for the reference's dense sphere grid at depth 10 (1024^3 bitset, 128 MiB,
@@ -829,6 +864,11 @@ def run_ours(args):
                                  "mrays_per_s": round(W * H / msf / 1e3, 1), "frames": nf, "dtype": "f64",
                                  "note": "FP64 parity kernel (reference operation order, bit-exact image, AOVs "
                                          "and FrameStats), same workload, timing and L2 flush as value"}
+        # the screen partition of the multi-GPU path, one rank's share at a time on this
+        # GPU: per-rank device time of the C4 frame for N = 2, 4, 8 (the compute side of
+        # strong scaling; composition over NVLink and the frame flags not included)
+        if args.precision == "fp32" and args.workload == "c4":
+            extras["partition_shares"] = partition_shares(lib, ctx, vxl, scene, animated, args, W, H)
         extras["animated_vs_static"] = round(extras["c2_animated_1080p"]["ms_per_frame"] /
                                              extras["c3_static_1080p"]["ms_per_frame"], 4)
         extras["model_build"] = model_build_bench(lib, ctx)
