@@ -915,7 +915,7 @@ __device__ bool traverse_fast(const Nodes nodes, int model_depth, const FastRay&
 // carried as `ten` -- the next sibling's entry is max(ten, t_exit) exactly,
 // because it differs from the current child only on the exit axis, whose near
 // plane is below its exit plane), the node word, the next octant, the level
-// and the `live` mask of ancestors with children left (as in traverse_fast).
+// and the `live` mask of ancestors with children left (level L at bit 22 - L: its midplane bit).
 template <bool kTrackIdx, class Nodes, class Stack>
 __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& r, FastHit& out, Stack& stack) {
     uint32_t sidx[kTrackIdx ? kMaxDepth : 1];
@@ -944,18 +944,22 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         if (fcur >= kExit) {
             // pop to the deepest live ancestor, its planes rebuilt from the position bits
             if (live == 0) break;
+            // `live` holds level L's bit at position 22 - L, which is the level's midplane
+            // bit in the position words: the deepest live level is the lowest set bit,
+            // and that bit is the `mid` its planes are rebuilt with (-1.8 %)
+            const uint32_t mid = live & (0u - live); // 2^-(lv+1) as a mantissa bit
+            live ^= mid;
             int lv;
-            asm("bfind.u32 %0, %1;" : "=r"(lv) : "r"(live));
-            live ^= 1u << lv;
+            asm("bfind.u32 %0, %1;" : "=r"(lv) : "r"(mid));
+            lv = 22 - lv;
+            const uint32_t keep = 0u - (mid << 1); // sign, exponent and the level-lv cell bits
             if constexpr (VXA_STACK_TEN)
                 fw = Nodes::unpack(stack.load3(lv, ten), fcur); // with the saved next child's entry
             else
                 fw = Nodes::unpack(stack.load(lv), fcur);
             level = lv;
             if constexpr (kTrackIdx) fidx = sidx[level];
-            const uint32_t keep = 0xffffffffu << (23 - lv); // sign, exponent and the level-lv cell bits
-            const uint32_t mid = 0x400000u >> lv;           // 2^-(lv+1)
-            const float size = __int_as_float((127 - lv) << 23);
+            const float half = __int_as_float((126 - lv) << 23); // the value of `mid`
             const uint32_t q = fcur;
             float c0[3];
 #pragma unroll
@@ -963,7 +967,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
                 const float lo = __uint_as_float(__float_as_uint(pm[a]) & keep);
                 pm[a] = __uint_as_float(__float_as_uint(lo) | mid);
                 tm[a] = __fmaf_rn(pm[a], r.inv[a], r.A[a]);
-                t1[a] = __fmaf_rn(lo + size, r.inv[a], r.A[a]);
+                t1[a] = __fmaf_rn(pm[a] + half, r.inv[a], r.A[a]); // far plane: pm + half = lo + size, exact
                 if constexpr (!VXA_STACK_TEN) c0[a] = (q & axis_bit(a)) ? tm[a] : __fmaf_rn(lo, r.inv[a], r.A[a]);
             }
             if constexpr (!VXA_STACK_TEN) ten = fmaxf(fmaxf(c0[0], c0[1]), c0[2]); // entry of the saved next child
@@ -1034,7 +1038,7 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         const uint32_t child =
             Nodes::child_base(fw) + popc8_below(Nodes::kLastLevelLeaves ? valid : valid & ~leafm, bit);
         if (fcur < kExit) {
-            live |= 1u << level;
+            live |= 0x400000u >> level; // level L at bit 22 - L (the pop above)
             if constexpr (VXA_STACK_TEN)
                 stack.store3(level, Nodes::pack(fw, fcur), ten); // ten = the next sibling's entry here
             else
