@@ -681,10 +681,6 @@ __device__ __forceinline__ bool fast_setup(FastRay& r, const float d[3], const f
 // threadIdx on every push/pop); LocalStack: a private array (API kernel).
 template <uint32_t kStride> struct SmemStack {
     uint32_t base; // shared address of this thread's level-0 slot; levels kStride bytes apart
-    // child-octant signs (+1 upper / -1 lower half per axis)
-    __device__ __forceinline__ static float4 signs(uint32_t q) {
-        return make_float4((q & 4u) ? 1.0f : -1.0f, (q & 2u) ? 1.0f : -1.0f, (q & 1u) ? 1.0f : -1.0f, 0.0f);
-    }
     __device__ __forceinline__ uint2 load(int level) const {
         uint2 v;
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(base + level * kStride));
@@ -734,9 +730,6 @@ struct LocalStack {
     __device__ __forceinline__ void store3(int level, uint2 v, float ten) {
         a[level] = v;
         ten_[level] = ten;
-    }
-    __device__ __forceinline__ static float4 signs(uint32_t q) {
-        return make_float4((q & 4u) ? 1.0f : -1.0f, (q & 2u) ? 1.0f : -1.0f, (q & 1u) ? 1.0f : -1.0f, 0.0f);
     }
     __device__ __forceinline__ uint2 load(int level) const { return a[level]; }
     __device__ __forceinline__ void store(int level, uint2 v) { a[level] = v; }
@@ -1052,11 +1045,11 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
         ++level;
         fw = nodes.load(child);
         ++fetches;
-        const float4 sg = stack.signs(q);
-        const float sgn[3] = {sg.x, sg.y, sg.z};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            pm[a] = __fmaf_rn(sgn[a], quarter, pm[a]);
+            // child midplane: +- a quarter of the node (exact), picked by the octant bit
+            // (a select of +-quarter and an add: no +-1 constant, -1.3 %)
+            pm[a] = __fadd_rn(pm[a], (q & axis_bit(a)) ? quarter : -quarter);
             tm[a] = __fmaf_rn(pm[a], r.inv[a], r.A[a]);
             t1[a] = c1[a];
         }
