@@ -89,6 +89,11 @@ int vxn_hbo_set_record(vxn_hbo* h, int x, int y, const vxa_hit_record* rec);
 int vxn_render(vxn_scene* s, int culling, int sorting, int precision, vxn_hbo* hbo, uint8_t* rgb,
                vxa_pixel_aov* aov, uint64_t* fs4, double* render_ms, vxa_stats* ds);
 
+/* The drop-in voxanim::render_frame (Image returned by value) `steps` times at
+ * animation times time + k/30: mean wall time per call (ms_per_call) and the
+ * last image's RGB8 bytes copied to last_rgb (width*height*3, or NULL). */
+int vxn_scene_render_image(vxn_scene* s, double time, int steps, double* ms_per_call, uint8_t* last_rgb);
+
 /* voxanim::traverse on a batch of local rays (vxa_local_ray), FP64, through
  * the C++ API (which dispatches to vxa_traverse). */
 int vxn_traverse(const vxn_model* m, const vxa_local_ray* rays, uint32_t n, vxa_traverse_hit* hits);

@@ -184,7 +184,8 @@ VXN_SYMBOLS = [
     "vxn_scene_config", "vxn_scene_evaluate", "vxn_scene_mark_clean", "vxn_scene_set_camera_dirty",
     "vxn_scene_set_camera",
     "vxn_scene_object_count", "vxn_scene_get_object", "vxn_scene_set_object", "vxn_scene_export", "vxn_scene_free", "vxn_scene_submit", "vxn_scene_stream",
-    "vxn_hbo_create", "vxn_hbo_free", "vxn_hbo_records", "vxn_hbo_set_record", "vxn_render", "vxn_traverse", "vxn_context",
+    "vxn_hbo_create", "vxn_hbo_free", "vxn_hbo_records", "vxn_hbo_set_record", "vxn_render", "vxn_scene_render_image",
+    "vxn_traverse", "vxn_context",
 ]
 
 P = C.c_void_p
@@ -286,6 +287,7 @@ def load_voxanim(path: str | None = None) -> C.CDLL:
     _declare(lib, "vxn_scene_free", None, P)
     _declare(lib, "vxn_scene_submit", i, P, d, i, i, i, u32)
     _declare(lib, "vxn_scene_stream", i, P, d, i, P, C.POINTER(u64))
+    _declare(lib, "vxn_scene_render_image", i, P, d, i, C.POINTER(d), P)
     _declare(lib, "vxn_hbo_create", P, i, i)
     _declare(lib, "vxn_hbo_free", None, P)
     _declare(lib, "vxn_hbo_records", i, P, P)

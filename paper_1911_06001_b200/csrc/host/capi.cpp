@@ -1,6 +1,7 @@
 // Flat C binding of the voxanim C++ API (include/voxanim_capi.h).
 #include "voxanim_capi.h"
 
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -367,6 +368,26 @@ int vxn_render(vxn_scene* s, int culling, int sorting, int precision, vxn_hbo* h
                 fs4[3] = st.pixels_reused;
             }
             if (render_ms) *render_ms = st.render_ms;
+            return 0;
+        },
+        -1);
+}
+
+int vxn_scene_render_image(vxn_scene* s, double time, int steps, double* ms_per_call, uint8_t* last_rgb) {
+    return guard(
+        [&] {
+            voxanim::RenderOptions opts;
+            voxanim::FrameStats st;
+            double total = 0.0;
+            for (int k = 0; k < steps; ++k) {
+                voxanim::evaluate_animation(s->s, time + k / 30.0);
+                const auto t0 = std::chrono::steady_clock::now();
+                const voxanim::Image img = voxanim::render_frame(s->s, opts, st); // the drop-in call, by value
+                total += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                voxanim::mark_clean(s->s);
+                if (last_rgb && k == steps - 1) std::memcpy(last_rgb, img.rgb.data(), img.rgb.size());
+            }
+            if (ms_per_call) *ms_per_call = steps > 0 ? total / steps : 0.0;
             return 0;
         },
         -1);

@@ -12,8 +12,15 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
 #include <numbers>
+#include <thread>
 #include <unordered_map>
+#include <vector>
 
 #include "voxanim/gpu.hpp"
 
@@ -235,10 +242,142 @@ void render_frame_into(const Scene& scene, const RenderOptions& opts, const Rend
     if (device_stats) *device_stats = ds;
 }
 
+namespace {
+// render_frame returns its Image by value (renderer.hpp:126): a fresh, zero-filled,
+// pageable vector every call. Rendering straight into it would take the banded
+// pageable copies, and the zero fill alone costs about a frame's kernel time. So
+// the frame is rendered into a page-locked staging image (the direct readback:
+// the frame kernel stores each finished super-tile into it over PCIe) while a
+// worker builds the Image, and the staging image is then copied into the Image by
+// a few threads.
+class ImageStaging {
+public:
+    static ImageStaging& get() {
+        static ImageStaging s;
+        return s;
+    }
+    std::mutex mu; // one render_frame at a time uses the staging image
+
+    // staging image of at least n bytes, page-locked for the context (grow-only)
+    uint8_t* ensure(size_t n) {
+        if (n <= cap_) return buf_;
+        if (buf_) {
+            vxa_host_unregister(context(), buf_);
+            std::free(buf_);
+            buf_ = nullptr;
+            cap_ = 0;
+        }
+        const size_t bytes = (n + 4095) & ~size_t{4095};
+        void* p = std::aligned_alloc(4096, bytes);
+        if (p == nullptr) return nullptr;
+        if (vxa_host_register(context(), p, bytes) != VXA_OK) {
+            std::free(p);
+            return nullptr;
+        }
+        buf_ = static_cast<uint8_t*>(p);
+        cap_ = bytes;
+        return buf_;
+    }
+
+    // f() on a worker; wait() joins it
+    void run_async(std::function<void()> f) { submit({std::move(f)}); }
+    void wait() { wait_all(); }
+
+    // dst[0, n) = src[0, n) in chunks over the workers and the calling thread
+    void parallel_copy(uint8_t* dst, const uint8_t* src, size_t n) {
+        const size_t parts = workers_.size() + 1;
+        const size_t chunk = ((n + parts - 1) / parts + 63) & ~size_t{63};
+        std::vector<std::function<void()>> jobs;
+        for (size_t k = 1; k < parts; ++k) {
+            const size_t a = std::min(n, k * chunk), b = std::min(n, a + chunk);
+            if (a < b) jobs.emplace_back([=] { std::memcpy(dst + a, src + a, b - a); });
+        }
+        submit(std::move(jobs));
+        std::memcpy(dst, src, std::min(n, chunk));
+        wait_all();
+    }
+
+private:
+    ImageStaging() {
+        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const unsigned n = std::min(8u, hw - 1);
+        for (unsigned k = 0; k < n; ++k) workers_.emplace_back([this] { loop(); });
+    }
+    ~ImageStaging() {
+        {
+            std::lock_guard<std::mutex> lk(q_mu_);
+            stop_ = true;
+        }
+        q_cv_.notify_all();
+        for (auto& t : workers_) t.join();
+        // the staging image stays registered until the process ends (the context may be gone)
+    }
+    void submit(std::vector<std::function<void()>> jobs) {
+        {
+            std::lock_guard<std::mutex> lk(q_mu_);
+            for (auto& j : jobs) queue_.push_back(std::move(j));
+            pending_ += jobs.size();
+        }
+        q_cv_.notify_all();
+    }
+    void wait_all() {
+        std::unique_lock<std::mutex> lk(q_mu_);
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+    }
+    void loop() {
+        while (true) {
+            std::function<void()> job;
+            {
+                std::unique_lock<std::mutex> lk(q_mu_);
+                q_cv_.wait(lk, [this] { return stop_ || !queue_.empty(); });
+                if (stop_ && queue_.empty()) return;
+                job = std::move(queue_.back());
+                queue_.pop_back();
+            }
+            job();
+            {
+                std::lock_guard<std::mutex> lk(q_mu_);
+                if (--pending_ == 0) done_cv_.notify_all();
+            }
+        }
+    }
+    uint8_t* buf_ = nullptr;
+    size_t cap_ = 0;
+    std::vector<std::thread> workers_;
+    std::mutex q_mu_;
+    std::condition_variable q_cv_, done_cv_;
+    std::vector<std::function<void()>> queue_;
+    size_t pending_ = 0;
+    bool stop_ = false;
+};
+} // namespace
+
 Image render_frame_ex(const Scene& scene, const RenderOptions& opts, const RenderOptionsEx& ex, FrameStats& stats,
                       vxa_stats* device_stats) {
     Image image;
-    if (ex.read_image) image = Image(scene.camera.width, scene.camera.height);
+    const int w = scene.camera.width, h = scene.camera.height;
+    const size_t n = static_cast<size_t>(w) * static_cast<size_t>(h) * 3;
+    const char* env = std::getenv("VOXANIM_IMAGE_STAGING");
+    const bool staged = ex.read_image && ex.aov == nullptr && n >= (size_t{3} << 20) &&
+                        !(env && std::strcmp(env, "0") == 0);
+    if (staged) {
+        ImageStaging& st = ImageStaging::get();
+        std::unique_lock<std::mutex> lk(st.mu);
+        if (uint8_t* stage = st.ensure(n)) {
+            // the Image (allocation + zero fill) is built while the GPU renders
+            st.run_async([&image, w, h] { image = Image(w, h); });
+            try {
+                render_frame_into(scene, opts, ex, stats, stage, device_stats);
+            } catch (...) {
+                st.wait();
+                throw;
+            }
+            st.wait();
+            st.parallel_copy(image.rgb.data(), stage, n);
+            return image;
+        }
+    }
+    if (ex.read_image) image = Image(w, h);
     render_frame_into(scene, opts, ex, stats, ex.read_image ? image.rgb.data() : nullptr, device_stats);
     return image;
 }

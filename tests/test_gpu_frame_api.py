@@ -403,3 +403,23 @@ def test_stream_delay_holds_the_stream(gpu):
     assert lib.vxa_stream_delay(ctx, 300) == 0
     assert lib.vxa_timer_end(ctx, C.byref(ms)) == 0
     assert 0.29 <= ms.value < 5.0, ms.value
+
+
+@pytest.mark.parametrize("staged", ["1", "0"])
+def test_drop_in_render_frame_image(gpu, staged, monkeypatch):
+    """The drop-in voxanim::render_frame returns its Image by value; a large frame is
+    rendered into a page-locked staging image (direct readback) while a worker builds
+    the Image, then copied in parallel (VOXANIM_IMAGE_STAGING=0: straight into the
+    Image). Both give the render_frame_into image, frame after frame."""
+    vxl = vx.voxanim()
+    monkeypatch.setenv("VOXANIM_IMAGE_STAGING", staged)
+    m = vx.Model.procedural(10, shell=True)
+    a, b = vx.Scene(vx.config.C4, [m], 0, 1920, 1080), vx.Scene(vx.config.C4, [m], 0, 1920, 1080)
+    last = np.zeros((1080, 1920, 3), np.uint8)
+    ms = C.c_double()
+    for t in (0.3, 2.1):
+        assert vxl.vxn_scene_render_image(a._h, t, 3, C.byref(ms), last.ctypes.data) == 0
+        b.evaluate(t + 2 / 30.0)
+        want = b.render()[0]
+        assert (last == want).all(), t
+        assert ms.value > 0.0
