@@ -792,6 +792,13 @@ def run_ours(args):
         el = time.perf_counter() - t0
         for b in bufs:
             lib.vxa_host_unregister(ctx, b.ctypes.data)
+        # (3) the drop-in voxanim::render_frame: the Image returned by value (a fresh,
+        #     zero-filled pageable vector) per call, evaluate_animation outside the calls
+        ms_di = C.c_double()
+        if vxl.vxn_scene_render_image(scene._h, frame_time(0, animated), 3, C.byref(ms_di), None) != 0:
+            raise RuntimeError(vxl.vxn_last_error().decode())
+        if vxl.vxn_scene_render_image(scene._h, frame_time(3, animated), args.e2e_steps, C.byref(ms_di), None) != 0:
+            raise RuntimeError(vxl.vxn_last_error().decode())
         e2e = {"value": round(rays * args.e2e_steps / el / 1e6, 3), "unit": "Mrays/s",
                "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step,
                "ms_per_step": round(el * 1e3 / args.e2e_steps, 3),
@@ -801,7 +808,11 @@ def run_ours(args):
                        "kernel); wall clock over all steps",
                "sync": {"value": round(rays * args.e2e_steps / el_sync / 1e6, 3),
                         "ms_per_step": round(el_sync * 1e3 / args.e2e_steps, 3),
-                        "path": "voxanim::gpu::render_frame_into, one synchronous call per step"}}
+                        "path": "voxanim::gpu::render_frame_into into a page-locked image, one synchronous "
+                                "call per step"},
+               "drop_in": {"value": round(rays / ms_di.value / 1e3, 3), "ms_per_call": round(ms_di.value, 3),
+                           "path": "voxanim::render_frame returning its Image by value (the reference's "
+                                   "call), wall time per call"}}
 
     # side measurements: animated vs static at 1080p (configs C2 / C3)
     extras = None

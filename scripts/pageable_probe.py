@@ -33,8 +33,9 @@ for name, buf in (("pageable", pageable), ("registered", pinned), ("fresh numpy 
 # (VOXANIM_IMAGE_STAGING=0) rendering straight into the fresh Image
 vxl = vx.voxanim()
 ms = C.c_double()
-for staged in ("1", "0"):
+for staged, spares in (("1", "1"), ("1", "0"), ("0", "0")):
     os.environ["VOXANIM_IMAGE_STAGING"] = staged
+    os.environ["VOXANIM_IMAGE_SPARES"] = spares
     sc2 = vx.Scene(vx.config.C4, [vx.Model.procedural(11, shell=True)])
     assert vxl.vxn_scene_render_image(sc2._h, 0.0, 5, C.byref(ms), None) == 0  # warm-up
     last = np.empty((H, W, 3), np.uint8)
@@ -42,5 +43,5 @@ for staged in ("1", "0"):
     sc3 = vx.Scene(vx.config.C4, [vx.Model.procedural(11, shell=True)])
     sc3.evaluate(1.0 + (steps - 1) / 30.0)
     same = (sc3.render(precision=vx.VXA_FP32)[0] == last).all()
-    print(f"{'render_frame (Image)':>22} staging={staged}: {ms.value:.3f} ms per call "
+    print(f"{'render_frame (Image)':>22} staging={staged} spares={spares}: {ms.value:.3f} ms per call "
           f"({W * H / ms.value / 1e3:.0f} Mrays/s), image equals render_frame_into: {same}", flush=True)

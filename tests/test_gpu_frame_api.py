@@ -405,14 +405,16 @@ def test_stream_delay_holds_the_stream(gpu):
     assert 0.29 <= ms.value < 5.0, ms.value
 
 
-@pytest.mark.parametrize("staged", ["1", "0"])
-def test_drop_in_render_frame_image(gpu, staged, monkeypatch):
+@pytest.mark.parametrize("staged,spares", [("1", "1"), ("1", "0"), ("0", "0")])
+def test_drop_in_render_frame_image(gpu, staged, spares, monkeypatch):
     """The drop-in voxanim::render_frame returns its Image by value; a large frame is
-    rendered into a page-locked staging image (direct readback) while a worker builds
-    the Image, then copied in parallel (VOXANIM_IMAGE_STAGING=0: straight into the
-    Image). Both give the render_frame_into image, frame after frame."""
+    rendered into a page-locked staging image (direct readback) while a worker takes
+    the Image (a ready zero-filled one, or VOXANIM_IMAGE_SPARES=0 built then), then
+    copied in parallel (VOXANIM_IMAGE_STAGING=0: straight into the Image). All give
+    the render_frame_into image, frame after frame, also when the frame size changes."""
     vxl = vx.voxanim()
     monkeypatch.setenv("VOXANIM_IMAGE_STAGING", staged)
+    monkeypatch.setenv("VOXANIM_IMAGE_SPARES", spares)
     m = vx.Model.procedural(10, shell=True)
     a, b = vx.Scene(vx.config.C4, [m], 0, 1920, 1080), vx.Scene(vx.config.C4, [m], 0, 1920, 1080)
     last = np.zeros((1080, 1920, 3), np.uint8)
@@ -423,3 +425,9 @@ def test_drop_in_render_frame_image(gpu, staged, monkeypatch):
         want = b.render()[0]
         assert (last == want).all(), t
         assert ms.value > 0.0
+    # another frame size: the ready images of the old size are not used
+    a2, b2 = vx.Scene(vx.config.C4, [m], 0, 1280, 1024), vx.Scene(vx.config.C4, [m], 0, 1280, 1024)
+    last2 = np.zeros((1024, 1280, 3), np.uint8)
+    assert vxl.vxn_scene_render_image(a2._h, 1.0, 2, C.byref(ms), last2.ctypes.data) == 0
+    b2.evaluate(1.0 + 1 / 30.0)
+    assert (last2 == b2.render()[0]).all()
