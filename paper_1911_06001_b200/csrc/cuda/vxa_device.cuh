@@ -936,11 +936,11 @@ __device__ bool traverse_pos(const Nodes nodes, int model_depth, const FastRay& 
     while (true) {
         if (fcur >= kExit) {
             // pop to the deepest live ancestor, its planes rebuilt from the position bits
-            if (live == 0) break;
             // `live` holds level L's bit at position 22 - L, which is the level's midplane
             // bit in the position words: the deepest live level is the lowest set bit,
             // and that bit is the `mid` its planes are rebuilt with (-1.8 %)
             const uint32_t mid = live & (0u - live); // 2^-(lv+1) as a mantissa bit
+            if (mid == 0) break;                     // every ancestor is exhausted: miss
             live ^= mid;
             int lv;
             asm("bfind.u32 %0, %1;" : "=r"(lv) : "r"(mid));
